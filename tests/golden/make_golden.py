@@ -1,0 +1,299 @@
+"""Generate tests/golden/*.json from the LIVE reference package.
+
+Runs only in the build container, where the reference lives at
+/root/reference (read-only; imported, never copied).  The fixtures pin both
+the C oracle (tests/test_oracle_golden.py, CPU) and the CUDA path
+(tests/test_gpu_parity.py, GPU).  Floats are stored as float.hex() strings so
+every comparison is bit-exact.
+
+    python tests/golden/make_golden.py            # all fixtures
+"""
+
+import itertools
+import json
+import math
+import os
+import random
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+REF_SRC = "/root/reference/pkg/src"
+REF_TESTS = "/root/reference/pkg/tests"
+sys.path.insert(0, REF_SRC)
+sys.path.insert(0, REF_TESTS)
+sys.path.insert(0, REPO)
+
+import pipeplan as P  # noqa: E402  (the reference)
+from conftest import (grid_instances, random_instance, random_weighted_clique,  # noqa: E402
+                      tiny_cluster, tiny_profile, trend_instance)
+
+from paper_2204_10562_b200 import workloads as W  # noqa: E402
+
+SEED = 20260822
+
+
+def hx(x):
+    return None if x is None else float(x).hex()
+
+
+def spec_of(profile, cluster, M):
+    return {
+        "name": profile.name,
+        "fwd": [hx(l.fwd_time) for l in profile.layers],
+        "bwd": [hx(l.bwd_time) for l in profile.layers],
+        "param": [hx(l.param_bytes) for l in profile.layers],
+        "efwd": [hx(e.fwd_bytes) for e in profile.edges],
+        "ebwd": [hx(e.bwd_bytes) for e in profile.edges],
+        "gpu_ids": list(cluster.gpu_ids),
+        "links": [[a, b, hx(w)] for (a, b), w in sorted(cluster.bandwidth.items())],
+        "M": M,
+    }
+
+
+def ref_model(spec: W.InstanceSpec):
+    layers = tuple(P.LayerProfile(id=i + 1, fwd_time=f, bwd_time=b, param_bytes=p)
+                   for i, (f, b, p) in enumerate(zip(spec.fwd, spec.bwd, spec.param)))
+    edges = tuple(P.InterLayerEdge(src=i + 1, dst=i + 2, fwd_bytes=a, bwd_bytes=b)
+                  for i, (a, b) in enumerate(zip(spec.efwd, spec.ebwd)))
+    prof = P.ModelProfile(name=spec.name, microbatch_size=1, layers=layers, edges=edges)
+    return prof, P.make_cluster(spec.gpu_ids, spec.links), spec.M
+
+
+def sched_of(s):
+    return {"events": [[e.resource, e.microbatch, e.block, hx(e.start), hx(e.end)] for e in s.events],
+            "allreduce": [[w.stage, hx(w.start), hx(w.end)] for w in s.allreduce],
+            "makespan": hx(s.makespan)}
+
+
+def plan_of(p):
+    return {"stages": [[s.layer_start, s.layer_end, list(s.devices)] for s in p.stages],
+            "M": p.microbatch_count}
+
+
+def spp_case(profile, cluster, M, events_limit=4000):
+    t0 = time.perf_counter()
+    r = P.spp(profile, cluster, M)
+    dt = time.perf_counter() - t0
+    out = {
+        "input": spec_of(profile, cluster, M),
+        "device_order": list(r.device_order),
+        "sweep": [[e.stage_count, e.feasible, hx(e.workload), hx(e.makespan), hx(e.bound)] for e in r.sweep],
+        "plan": plan_of(r.plan),
+        "makespan": hx(r.makespan),
+        "phi": hx(r.phi),
+        "theorem_factor": hx(r.theorem_factor),
+        "ref_seconds": dt,
+    }
+    if len(r.schedule.events) <= events_limit:
+        out["schedule"] = sched_of(r.schedule)
+    else:
+        out["schedule"] = {"events": None, "allreduce": sched_of(r.schedule)["allreduce"],
+                           "makespan": hx(r.schedule.makespan), "n_events": len(r.schedule.events)}
+    return out
+
+
+def gen_pysum():
+    rng = random.Random(7)
+    cases = []
+    for _ in range(3000):
+        n = rng.randint(1, 60)
+        kind = rng.random()
+        if kind < 0.4:
+            xs = [math.exp(rng.uniform(math.log(1e-3), math.log(2.0))) for _ in range(n)]
+        elif kind < 0.7:
+            xs = [math.exp(rng.uniform(math.log(1e6), math.log(1e10))) for _ in range(n)]
+        elif kind < 0.9:
+            xs = [rng.choice([0.0, 1e-17, 1.0, 3.0, 1e16, 0.1, 0.7]) for _ in range(n)]
+        else:
+            xs = [rng.uniform(0, 1) * 10 ** rng.randint(-20, 20) for _ in range(n)]
+        cases.append({"x": [hx(v) for v in xs], "sum": hx(sum(xs))})
+    return {"python": sys.version, "cases": cases}
+
+
+def gen_spp():
+    cases = []
+    cases.append(spp_case(tiny_profile(), tiny_cluster(), 2))
+    one = P.ModelProfile(name="one", microbatch_size=1,
+                         layers=(P.LayerProfile(id=1, fwd_time=1.0, bwd_time=2.0, param_bytes=1e9),),
+                         edges=())
+    cases.append(spp_case(one, tiny_cluster(), 2))
+    cases.append(spp_case(*trend_instance()))
+    skew_layers = (P.LayerProfile(1, 1.0, 2.0, 1e9), P.LayerProfile(2, 0.5, 1.0, 2e9), P.LayerProfile(3, 2.0, 3.0, 1e9))
+    skew_edges = (P.InterLayerEdge(1, 2, 5e8, 5e8), P.InterLayerEdge(2, 3, 2e9, 1e9))
+    skew = P.ModelProfile("skew", 1, skew_layers, skew_edges)
+    skew_c = P.make_cluster([1, 2, 3], [(1, 2, 4e9), (1, 3, 1e9), (2, 3, 1e9)])
+    for M in (1, 3, 7):
+        cases.append(spp_case(skew, skew_c, M))
+    # non-contiguous, unsorted GPU ids
+    c_odd = P.make_cluster([9, 3, 17, 5], [(9, 3, 2e9), (9, 17, 5e9), (9, 5, 1e9), (3, 17, 1e9), (3, 5, 8e9), (17, 5, 2e9)])
+    cases.append(spp_case(skew, c_odd, 4))
+    for k, inst in enumerate(grid_instances()):
+        if k % 15 == 0:
+            cases.append(spp_case(*inst))
+    rng = random.Random(SEED)
+    for _ in range(150):
+        cases.append(spp_case(*random_instance(rng)))
+    # zero-valued params / bytes
+    rng = random.Random(11)
+    for _ in range(20):
+        prof, clu, M = random_instance(rng)
+        layers = tuple(P.LayerProfile(l.id, l.fwd_time, l.bwd_time, 0.0 if l.id % 2 else l.param_bytes) for l in prof.layers)
+        edges = tuple(P.InterLayerEdge(e.src, e.dst, 0.0, e.bwd_bytes) for e in prof.edges)
+        cases.append(spp_case(P.ModelProfile(prof.name + "z", 1, layers, edges), clu, M))
+    cases.append(spp_case(*ref_model(W.c1_vgg19())))
+    cases.append(spp_case(*ref_model(W.c2_bert24())))
+    for k in range(2):
+        cases.append(spp_case(*ref_model(W.c4_instance(k))))
+    cases.append(spp_case(*ref_model(W.c3_gpt96(M=32, L=48, nodes=2, per_node=8))))
+    cases.append(spp_case(*ref_model(W.c3_gpt96(M=64, jitter_seed=96, L=48, nodes=2, per_node=8))))
+    return {"python": sys.version, "cases": cases}
+
+
+def gen_prm():
+    out = []
+    rng = random.Random(5)
+    insts = [(tiny_profile(), tiny_cluster(), 2)]
+    for _ in range(12):
+        prof, clu, M = random_instance(rng)
+        insts.append((prof, clu, M))
+    insts.append(next(itertools.islice(grid_instances(), 1500, None)))
+    for prof, clu, M in insts:
+        for order_kind in ("rdo", "reversed"):
+            order = P.rdo(clu)
+            if order_kind == "reversed":
+                o = tuple(reversed(order.order))
+                order = P.DeviceOrdering(order=o, rank={v: k + 1 for k, v in enumerate(o)})
+            for allow in (True, False):
+                s = P.PartitionSolver(prof, clu, order, M, allow_replication=allow)
+                L, V = prof.num_layers, clu.num_gpus
+                cells = []
+                for l in range(1, L + 1):
+                    for xi in range(1, V + 2):
+                        for r in range(1, V + 2):
+                            for i in range(1, V + 1):
+                                try:
+                                    res = s.solve(l, xi, r, i)
+                                except P.ValidationError as e:
+                                    cells.append([l, xi, r, i, "error", str(e)])
+                                    continue
+                                cells.append([l, xi, r, i, hx(res.workload),
+                                              None if res.stages is None else [[a, b, list(d)] for a, b, d in res.stages]])
+                best = []
+                for xi in range(1, V + 1):
+                    w, plan = s.best_partition(xi)
+                    best.append([xi, hx(w), None if plan is None else plan_of(plan)])
+                out.append({"input": spec_of(prof, clu, M), "order": list(order.order), "allow_replication": allow,
+                            "cells": cells, "best": best})
+    return {"python": sys.version, "cases": out}
+
+
+def gen_sim():
+    cases = []
+    prof, clu = tiny_profile(), tiny_cluster()
+
+    def split(M):
+        return P.Plan((P.Stage(1, 1, 1, (1,)), P.Stage(2, 2, 2, (2,))), M)
+
+    def add(name, plan, profile, cluster, queues=None, barrier=False):
+        rec = {"name": name, "input": spec_of(profile, cluster, plan.microbatch_count), "plan": plan_of(plan),
+               "forward_barrier": barrier}
+        if queues is None:
+            queues = P.compute_execution_order(plan).queues
+            rec["pe"] = True
+        rec["queues"] = {k: [list(x) for x in v] for k, v in queues.items()}
+        try:
+            s = P.simulate_with_order(plan, profile, cluster, queues, forward_barrier=barrier)
+            rec["schedule"] = sched_of(s)
+        except P.SchedulingError as e:
+            rec["error"] = ["SchedulingError", str(e)]
+        rec["lemma1_bound"] = hx(P.lemma1_bound(plan, profile, cluster))
+        cases.append(rec)
+
+    for M in (1, 2, 3, 5):
+        add(f"tiny_split_pe_M{M}", split(M), prof, clu)
+        add(f"tiny_gpipe_M{M}", split(M), prof, clu,
+            queues=_gpipe_queues(split(M)), barrier=True)
+        add(f"tiny_pe_barrier_M{M}", split(M), prof, clu, barrier=True, queues=P.compute_execution_order(split(M)).queues)
+    q = dict(P.compute_execution_order(split(2)).queues)
+    q["stage1"] = ((1, 5), (2, 5), (1, 1), (2, 1))
+    add("tiny_circular", split(2), prof, clu, queues=q)
+    q = dict(P.compute_execution_order(split(3)).queues)
+    del q["chan1"]
+    add("tiny_missing_queue", split(3), prof, clu, queues=q)
+    add("tiny_replicated", P.Plan((P.Stage(1, 1, 2, (1, 2)),), 2), prof, clu)
+    rng = random.Random(99)
+    for k in range(40):
+        profile, cluster, M = random_instance(rng)
+        L, V = profile.num_layers, cluster.num_gpus
+        N = rng.randint(1, min(L, V))
+        cuts = sorted(rng.sample(range(1, L), N - 1))
+        bounds = [0] + cuts + [L]
+        devs = list(cluster.gpu_ids)
+        rng.shuffle(devs)
+        dcuts = sorted(rng.sample(range(1, V), N - 1)) if N > 1 else []
+        db = [0] + dcuts + [V]
+        stages = tuple(P.Stage(n + 1, bounds[n] + 1, bounds[n + 1], tuple(devs[db[n]:db[n + 1]])) for n in range(N))
+        plan = P.Plan(stages, M)
+        add(f"rand{k}_pe", plan, profile, cluster)
+        if not any(s.replicated for s in stages):
+            add(f"rand{k}_gpipe", plan, profile, cluster, queues=_gpipe_queues(plan), barrier=True)
+        if k % 4 == 0:
+            qq = {kk: tuple(reversed(v)) if kk == "stage1" else v for kk, v in P.compute_execution_order(plan).queues.items()}
+            add(f"rand{k}_reversed_stage1", plan, profile, cluster, queues=qq)
+    return {"python": sys.version, "cases": cases}
+
+
+def _gpipe_queues(plan):
+    blocks = P.build_block_list(plan)
+    M = plan.microbatch_count
+    queues = {}
+    for b in blocks:
+        queues[b.resource] = queues.get(b.resource, ()) + tuple((m, b.position) for m in range(1, M + 1))
+    return queues
+
+
+def gen_ordering():
+    rng = random.Random(SEED)
+    cuts = []
+    for _ in range(300):
+        c = random_weighted_clique(rng)
+        a, b, w = P.global_min_cut(c)
+        cuts.append({"gpu_ids": list(c.gpu_ids), "links": [[x, y, hx(v)] for (x, y), v in sorted(c.bandwidth.items())],
+                     "side_a": list(a), "side_b": list(b), "weight": hx(w)})
+    orders = []
+    clusters = []
+    for k in range(60):
+        clusters.append(random_weighted_clique(rng))
+    ids, links = W.two_tier_cluster(4, 4)
+    clusters.append(P.make_cluster(ids, links))
+    ids, links = W.two_tier_cluster(2, 8)
+    clusters.append(P.make_cluster(ids, links))
+    spec = W.c4_instance(3)
+    clusters.append(P.make_cluster(spec.gpu_ids, spec.links))
+    spec = W.c2_bert24()
+    clusters.append(P.make_cluster(spec.gpu_ids, spec.links))
+    ids = list(range(1, 7))
+    clusters.append(P.make_cluster(ids, [(a, b, 1e9) for i, a in enumerate(ids) for b in ids[i + 1:]]))
+    for c in clusters:
+        o = P.rdo(c)
+        orders.append({"gpu_ids": list(c.gpu_ids), "links": [[x, y, hx(v)] for (x, y), v in sorted(c.bandwidth.items())],
+                       "order": list(o.order)})
+    return {"python": sys.version, "min_cut": cuts, "rdo": orders}
+
+
+def main():
+    which = sys.argv[1:] or ["pysum", "spp", "prm", "sim", "ordering"]
+    gens = {"pysum": gen_pysum, "spp": gen_spp, "prm": gen_prm, "sim": gen_sim, "ordering": gen_ordering}
+    for name in which:
+        t0 = time.time()
+        data = gens[name]()
+        path = os.path.join(HERE, f"{name}.json")
+        with open(path, "w") as f:
+            json.dump(data, f, separators=(",", ":"))
+        print(f"{name}: {os.path.getsize(path) / 1e6:.2f} MB in {time.time() - t0:.1f}s")
+
+
+if __name__ == "__main__":
+    main()

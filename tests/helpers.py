@@ -1,0 +1,67 @@
+"""Shared test helpers: fixture loading and conversions (tests only)."""
+
+import json
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLDEN = os.path.join(HERE, "golden")
+
+
+def load(name):
+    with open(os.path.join(GOLDEN, f"{name}.json")) as f:
+        return json.load(f)
+
+
+def fx(h):
+    return None if h is None else float.fromhex(h)
+
+
+def arrays(spec):
+    """Raw arrays from a fixture input dict: (fwd, bwd, param, efwd, ebwd, bw[V,V], sorted ids, M)."""
+    ids = sorted(spec["gpu_ids"])
+    pos = {g: k for k, g in enumerate(ids)}
+    V = len(ids)
+    bw = np.zeros((V, V))
+    for a, b, w in spec["links"]:
+        bw[pos[a], pos[b]] = bw[pos[b], pos[a]] = fx(w)
+    f = lambda key: np.array([fx(v) for v in spec[key]], dtype=np.float64)
+    return f("fwd"), f("bwd"), f("param"), f("efwd"), f("ebwd"), bw, ids, spec["M"]
+
+
+def oracle_instance(spec, M=None):
+    import oracle as O
+    fwd, bwd, param, efwd, ebwd, bw, ids, m = arrays(spec)
+    return O.Instance(fwd, bwd, param, efwd, ebwd, bw, m if M is None else M), ids
+
+
+def model_of(spec, M=None):
+    """(ModelProfile, ClusterGraph, M) of the product package from a fixture input."""
+    from paper_2204_10562_b200.model import InterLayerEdge, LayerProfile, ModelProfile, make_cluster
+    layers = tuple(LayerProfile(id=k + 1, fwd_time=fx(a), bwd_time=fx(b), param_bytes=fx(c))
+                   for k, (a, b, c) in enumerate(zip(spec["fwd"], spec["bwd"], spec["param"])))
+    edges = tuple(InterLayerEdge(src=k + 1, dst=k + 2, fwd_bytes=fx(a), bwd_bytes=fx(b))
+                  for k, (a, b) in enumerate(zip(spec["efwd"], spec["ebwd"])))
+    prof = ModelProfile(name=spec["name"], microbatch_size=1, layers=layers, edges=edges)
+    clu = make_cluster(spec["gpu_ids"], [(a, b, fx(w)) for a, b, w in spec["links"]])
+    return prof, clu, spec["M"] if M is None else M
+
+
+def block_labels(N):
+    """position -> (resource, label) following the reference block list J."""
+    out = {}
+    if N == 1:
+        return {1: ("stage1", "fwdbwd1")}
+    pos = 1
+    for n in range(1, N):
+        out[pos] = (f"stage{n}", f"fwd{n}")
+        out[pos + 1] = (f"chan{n}", f"comm_fwd{n}")
+        pos += 2
+    out[pos] = (f"stage{N}", f"fwdbwd{N}")
+    pos += 1
+    for n in range(N - 1, 0, -1):
+        out[pos] = (f"chan{n}", f"comm_bwd{n}")
+        out[pos + 1] = (f"stage{n}", f"bwd{n}")
+        pos += 2
+    return out
