@@ -1,0 +1,190 @@
+/*
+ * pipeplan_b200.h — C ABI of libpipeplan_b200.so, the sm_100a planning path
+ * of arXiv 2204.10562 ("pipeplan" reference package).
+ *
+ * The reference has no FFI: its boundary is the Python library API exported
+ * by pipeplan/__init__.py:96-174.  Every entry point below replaces the
+ * inside of one reference function and is bound by the Python drop-in
+ * package (paper_2204_10562_b200/_lib.py, ctypes); INTEGRATION.md shows the
+ * binding.  Conventions:
+ *   - plain C types, caller-allocated DEVICE memory for every array (the
+ *     library never allocates long-lived memory and never frees caller memory;
+ *     scratch comes from the caller's fp64 workspace `ws`);
+ *   - every launch goes to the caller's stream (cudaStream_t passed as void*);
+ *   - status: 0 ok, negative PP_E* on error, message via pp_last_error()
+ *     (thread-local).  Planning infeasibility is a VALUE (+inf / flag 0), as in
+ *     the reference (partition.py:115-121); simulation stalls are reported per
+ *     plan in pp_sim_batch.status (scheduler.py:207-214).
+ *   - device indices are positions in the ascending-sorted GPU id list; the
+ *     bandwidth matrix bw is V*V, symmetric, row-major over those positions.
+ *   - fp64 everywhere, IEEE round-to-nearest, no FMA contraction
+ *     (nvcc -fmad=false): results are bit-identical to the reference's
+ *     Python float arithmetic on the same inputs.
+ */
+#ifndef PIPEPLAN_B200_H
+#define PIPEPLAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PP_OK 0
+#define PP_EINVAL (-1)   /* bad argument / size beyond the build's limits   */
+#define PP_ECUDA (-3)    /* CUDA runtime error (message has the CUDA text)   */
+
+/* pp_instance.flags */
+#define PP_ALLOW_REPLICATION 1   /* PartitionSolver(allow_replication=True) (partition.py:49-51) */
+#define PP_SUM_NAIVE 2           /* CPython <= 3.11 float sum(); default is the 3.12+ Neumaier sum */
+#define PP_GIVEN_ORDER 4         /* order[] is an input (caller's DeviceOrdering); else RDO fills it */
+
+/* Build limits (checked by pp_layout). */
+#define PP_MAX_LAYERS 4096
+#define PP_MAX_GPUS 512
+
+/* One planning instance: spp(profile, cluster, M) (planner.py:57).  All
+ * *_off fields are element offsets into the pp_batch arrays; pp_layout()
+ * fills them. */
+typedef struct {
+    int32_t L, V, M, flags;
+    int64_t layer_off;   /* fwd/bwd/param[layer_off + l-1]; efwd/ebwd[layer_off + l-1], l < L      */
+    int64_t bw_off;      /* bw[bw_off + a*V + b]                                                    */
+    int64_t order_off;   /* order[order_off + rank-1] = device index                                */
+    int64_t sweep_off;   /* sweep_*[sweep_off + xi-1], xi = 1..V                                     */
+    int64_t stage_off;   /* stage_*[stage_off + xi(xi-1)/2 + n-1]: stage n of the best xi-stage plan */
+    int64_t ws_off;      /* fp64 scratch: tables, DP slices W_i, expansion X (pp_layout sizes it)    */
+    int64_t ev_off;      /* ev_start/ev_end[ev_off + (m-1)*(4N-3) + pos-1] for the selected plan    */
+    int64_t ar_off;      /* ar_start/ar_end[ar_off + n-1], selected plan                            */
+} pp_instance;
+
+/* A batch of planning instances and every array they use (device pointers). */
+typedef struct {
+    int32_t n_inst;
+    int32_t max_L, max_V;             /* host copies: maxima over the batch                       */
+    const pp_instance *inst;          /* device [n_inst]                                          */
+    const double *fwd, *bwd, *param;  /* profile (model.py:24-30)                                 */
+    const double *efwd, *ebwd;        /* edges (model.py:33-39)                                   */
+    const double *bw;                 /* cluster (model.py:62-81)                                 */
+    int32_t *order;                   /* device order (ordering.py:94-113)                        */
+    /* per-xi sweep (planner.py:30-37, SweepEntry) */
+    double *sweep_w;                  /* W: best workload, +inf if infeasible                     */
+    double *sweep_mk;                 /* simulated makespan (simulate_pe)                         */
+    double *sweep_bound;              /* lemma1_bound                                             */
+    int32_t *sweep_r;                 /* last-stage width of the best plan, 0 if infeasible       */
+    /* best plan per xi (partition.py:144-162): layer interval and device-rank interval */
+    int32_t *stage_ls, *stage_le, *stage_dlo, *stage_dhi;
+    /* selection (planner.py:66-77) */
+    int32_t *best_xi;                 /* [n_inst]                                                 */
+    double *best_mk;                  /* [n_inst]                                                 */
+    double *phi;                      /* [n_inst] cost.py:131-142                                 */
+    /* schedule of the selected plan (optional: NULL skips event capture) */
+    double *ev_start, *ev_end;
+    double *ar_start, *ar_end;
+    double *ws;                       /* fp64 workspace, pp_layout() doubles                      */
+} pp_batch;
+
+/* ---- host helpers (no device work) ------------------------------------ */
+const char *pp_version(void);
+const char *pp_last_error(void);
+int pp_device_count(void);
+
+/* Fill inst[k] offsets for n instances of sizes L[k], V[k] (M[k], flags[k]
+ * copied).  Returns totals through the out-pointers: layer, bw, order, sweep,
+ * stage, event, allreduce element counts and workspace doubles.  Host only. */
+int pp_layout(int32_t n, const int32_t *L, const int32_t *V, const int32_t *M, const int32_t *flags,
+              pp_instance *inst, int64_t *n_layer, int64_t *n_bw, int64_t *n_order, int64_t *n_sweep,
+              int64_t *n_stage, int64_t *n_ev, int64_t *n_ar, int64_t *n_ws);
+
+/* ---- planning path -------------------------------------------------------
+ * Each call enqueues kernels on `stream` and returns without synchronising. */
+
+/* rdo(cluster) for every instance without PP_GIVEN_ORDER (ordering.py:94-113). */
+int pp_rdo(const pp_batch *b, void *stream);
+
+/* PartitionSolver over all cells + best_partition(xi) for every xi
+ * (partition.py:41-162): fills sweep_w, sweep_r, stage_*. */
+int pp_prm(const pp_batch *b, void *stream);
+
+/* simulate_pe + lemma1_bound for every feasible xi plan (scheduler.py:75-238):
+ * fills sweep_mk, sweep_bound. */
+int pp_pe_sweep(const pp_batch *b, void *stream);
+
+/* spp selection (planner.py:66-88): best_xi, best_mk, phi; then replays the
+ * selected plan into ev_start/ev_end and ar_start/ar_end when ev_start != NULL. */
+int pp_select(const pp_batch *b, void *stream);
+
+/* phi(profile, cluster) per instance into phi[] (cost.py:126-142). */
+int pp_phi(const pp_batch *b, void *stream);
+
+/* The whole spp(): pp_phi, pp_rdo, pp_prm, pp_pe_sweep, pp_select. */
+int pp_spp(const pp_batch *b, void *stream);
+
+/* DP table access for PartitionSolver.solve(l, xi, r, i) (partition.py:95-142):
+ * for each query q (device arrays, 1-based arguments already range-checked by
+ * the caller) write W to w[q] and the realizing fragments (ls, le, dlo, dhi)
+ * to frag[q*4*max_xi ...]; feasible[q] = 1/0.  Requires a prior pp_prm on the
+ * same batch and workspace. */
+int pp_prm_query(const pp_batch *b, int32_t n_query, const int32_t *q_inst, const int32_t *q_l,
+                 const int32_t *q_xi, const int32_t *q_r, const int32_t *q_i, int32_t max_xi,
+                 double *w, int32_t *frag, int32_t *feasible, void *stream);
+
+/* ---- simulation of caller plans (simulate_with_order / simulate_pe) -----
+ * One pp_plan per plan; resources are numbered in chain order
+ * (0 = stage1, 1 = chan1, 2 = stage2, ...), R = 2N-1 of them. */
+#define PP_SIM_FORWARD_BARRIER 1   /* simulate_with_order(forward_barrier=True)          */
+#define PP_SIM_PE_ORDER 2          /* queues = compute_execution_order(plan) (closed form) */
+
+typedef struct {
+    int32_t inst;        /* instance (profile + bw) in the pp_batch            */
+    int32_t N, M, flags;
+    int64_t stage_off;   /* ls/le[stage_off + n-1]                              */
+    int64_t devoff_off;  /* dev_off[devoff_off + 0..N] into devs                */
+    int64_t queue_off;   /* q_off[queue_off + 0..R] into q_items pairs          */
+    int64_t lane_off;    /* head[lane_off + 0..R-1]                             */
+    int64_t ev_off;      /* ev_start, ev_end, scratch [ev_off + (m-1)*(4N-3) + pos-1]         */
+    int64_t ar_off;      /* ar_*[ar_off + n-1]                                  */
+} pp_plan;
+
+typedef struct {
+    int32_t n_plan, max_N;
+    const pp_plan *plan;              /* device [n_plan]                        */
+    const int32_t *ls, *le;           /* stage layer intervals (1-based)         */
+    const int32_t *dev_off;           /* per plan N+1 offsets into devs          */
+    const int32_t *devs;              /* device indices                          */
+    const int32_t *q_off;             /* per plan R+1 offsets (pairs)            */
+    const int32_t *q_items;           /* (m, pos) pairs                          */
+    double *makespan, *bound;         /* [n_plan]                                */
+    int32_t *status;                  /* [n_plan] 0 ok, 1 stalled                */
+    int64_t *n_done;                  /* [n_plan] executions finished            */
+    int32_t *head;                    /* per resource: next unserved queue index */
+    double *ev_start, *ev_end;        /* per (m,pos); NULL skips event capture   */
+    double *ar_start, *ar_end;        /* per stage                               */
+    double *scratch;                  /* per (m,pos) completion times (generic queues) */
+} pp_sim_batch;
+
+/* simulate_with_order / simulate_pe (scheduler.py:121-231) + lemma1_bound
+ * (scheduler.py:234-238) for every plan.  Queue items must be unique, with
+ * 1 <= m <= M and 1 <= pos <= 4N-3, each on its own block's resource (the
+ * Python layer checks this). */
+int pp_simulate(const pp_batch *inst_batch, const pp_sim_batch *s, void *stream);
+
+/* Kernel launches issued by this library since load (evidence counter). */
+int64_t pp_launch_count(void);
+
+/* Measurement only (bench.py roofline denominator): launch a kernel that
+ * saturates the fp64 min/max pipe; *n_ops receives the DMNMX count it
+ * issues.  d_out: one device double (never written in practice). */
+int pp_peak_minmax(double *d_out, int32_t iters, int64_t *n_ops, void *stream);
+
+/* ---- ordering primitives ------------------------------------------------ */
+/* global_min_cut (ordering.py:30-91) over a vertex subset of instance `k`:
+ * verts (device, ascending, n of them); in_a[v] = 1 for side_a; weight[0]. */
+int pp_min_cut(const pp_batch *b, int32_t k, const int32_t *verts, int32_t n, uint8_t *in_a,
+               double *weight, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIPEPLAN_B200_H */

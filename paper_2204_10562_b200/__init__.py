@@ -1,0 +1,29 @@
+"""B200-native planning path of arXiv 2204.10562 ("pipeplan" drop-in).
+
+Same public names and semantics as the reference package's planning path
+(pipeplan/__init__.py:96-174): domain types, spp, PartitionSolver,
+simulate_pe / simulate_with_order, RDO.  Planning arithmetic runs only in
+libpipeplan_b200.so (sm_100a CUDA) — there is no CPU fallback; without a GPU
+the planning calls raise _lib.BackendUnavailable.
+"""
+
+from .model import (AllReduceWindow, Block, ClusterGraph, InterLayerEdge, LayerProfile, ModelProfile, Plan,
+                    Schedule, ScheduleEvent, Stage, ValidationError, check_numeric_range, make_cluster,
+                    plan_uses_all_gpus, validate_cluster, validate_plan, validate_profile)
+from .ordering import DeviceOrdering, global_min_cut, rdo
+from .partition import PartitionSolver, PrmResult, best_partition, prm
+from .planner import BoundReport, SppResult, SweepEntry, bound_factor, phi, spp, spp_many, theorem1_report
+from .scheduler import (ExecutionOrder, SchedulingError, build_block_list, compute_execution_order, lemma1_bound,
+                        simulate_pe, simulate_with_order)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "AllReduceWindow", "Block", "BoundReport", "ClusterGraph", "DeviceOrdering", "ExecutionOrder",
+    "InterLayerEdge", "LayerProfile", "ModelProfile", "Plan", "PartitionSolver", "PrmResult", "Schedule",
+    "ScheduleEvent", "SchedulingError", "SppResult", "Stage", "SweepEntry", "ValidationError",
+    "best_partition", "bound_factor", "build_block_list", "check_numeric_range", "compute_execution_order",
+    "global_min_cut", "lemma1_bound", "make_cluster", "phi", "plan_uses_all_gpus", "prm", "rdo",
+    "simulate_pe", "simulate_with_order", "spp", "spp_many", "theorem1_report", "validate_cluster",
+    "validate_plan", "validate_profile",
+]

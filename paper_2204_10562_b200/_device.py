@@ -1,0 +1,304 @@
+"""Host <-> device marshalling for the planning C-ABI.
+
+Instances are packed with numpy into two flat host buffers (fp64 inputs and
+int32 descriptors), moved with ONE pinned host-to-device copy each, and the
+pp_batch descriptor is filled with raw device pointers (torch tensors are only
+used as device allocations and for the current CUDA stream).  Outputs come
+back with one device-to-host copy per dtype.
+"""
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import PPBatch, PPInstance, PPPlan, PPSimBatch
+
+F64 = torch.float64
+I32 = torch.int32
+
+
+@dataclass
+class Packed:
+    """One instance as flat arrays (device indices = positions in sorted ids)."""
+    ids: Sequence[int]
+    fwd: np.ndarray
+    bwd: np.ndarray
+    param: np.ndarray
+    efwd: np.ndarray   # length L (last entry unused)
+    ebwd: np.ndarray
+    bw: np.ndarray     # V x V
+
+    @property
+    def L(self):
+        return int(self.fwd.shape[0])
+
+    @property
+    def V(self):
+        return int(self.bw.shape[0])
+
+
+def pack(profile, cluster) -> Packed:
+    L = profile.num_layers
+    fwd = np.fromiter((lp.fwd_time for lp in profile.layers), dtype=np.float64, count=L)
+    bwd = np.fromiter((lp.bwd_time for lp in profile.layers), dtype=np.float64, count=L)
+    par = np.fromiter((lp.param_bytes for lp in profile.layers), dtype=np.float64, count=L)
+    efwd = np.zeros(L)
+    ebwd = np.zeros(L)
+    if L > 1:
+        efwd[:L - 1] = [e.fwd_bytes for e in profile.edges]
+        ebwd[:L - 1] = [e.bwd_bytes for e in profile.edges]
+    ids = tuple(sorted(cluster.gpu_ids))
+    pos = {g: k for k, g in enumerate(ids)}
+    V = len(ids)
+    bw = np.zeros((V, V))
+    for (a, b), w in cluster.bandwidth.items():
+        pa, pb = pos[a], pos[b]
+        bw[pa, pb] = w
+        bw[pb, pa] = w
+    return Packed(ids, fwd, bwd, par, efwd, ebwd, bw)
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def device():
+    _lib.load(require_device=True)
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+class DeviceBatch:
+    """A batch of planning instances resident on the GPU with all outputs.
+
+    items: list of (Packed, M, flags, order_positions or None).
+    """
+
+    def __init__(self, items, capture_events=True):
+        lib = _lib.load()
+        dev = device()
+        self.items = items
+        n = len(items)
+        self.n = n
+        Ls = np.array([p.L for p, _, _, _ in items], dtype=np.int32)
+        Vs = np.array([p.V for p, _, _, _ in items], dtype=np.int32)
+        Ms = np.array([m for _, m, _, _ in items], dtype=np.int32)
+        fl = np.array([f for _, _, f, _ in items], dtype=np.int32)
+        inst = (PPInstance * n)()
+        tot = [C.c_int64() for _ in range(8)]
+        _lib.check(lib.pp_layout(n, Ls.ctypes.data, Vs.ctypes.data, Ms.ctypes.data, fl.ctypes.data,
+                                 C.cast(inst, C.c_void_p), *[C.byref(t) for t in tot]))
+        n_layer, n_bw, n_order, n_sweep, n_stage, n_ev, n_ar, n_ws = (t.value for t in tot)
+        self.inst_host = inst
+        self.sizes = dict(layer=n_layer, bw=n_bw, order=n_order, sweep=n_sweep, stage=n_stage,
+                          ev=n_ev, ar=n_ar, ws=n_ws)
+        # ---- fp64 input buffer: fwd | bwd | param | efwd | ebwd | bw
+        fin = np.empty(5 * n_layer + n_bw)
+        for k, (p, _, _, _) in enumerate(items):
+            lo, L = inst[k].layer_off, p.L
+            for s, arr in enumerate((p.fwd, p.bwd, p.param, p.efwd, p.ebwd)):
+                fin[s * n_layer + lo: s * n_layer + lo + L] = arr
+            fin[5 * n_layer + inst[k].bw_off: 5 * n_layer + inst[k].bw_off + p.V * p.V] = p.bw.reshape(-1)
+        # ---- int32 buffer: instance descriptors (as raw int32 words) | order
+        ib = np.frombuffer(bytes(inst), dtype=np.int32)
+        order = np.zeros(n_order, dtype=np.int32)
+        for k, (p, _, _, o) in enumerate(items):
+            if o is not None:
+                order[inst[k].order_off: inst[k].order_off + p.V] = o
+        iin = np.concatenate([ib, order])
+        self.max_L = int(Ls.max())
+        self.max_V = int(Vs.max())
+        # ---- device allocations
+        self.d_fin = torch.from_numpy(fin).pin_memory().to(dev, non_blocking=True)
+        self.d_iin = torch.from_numpy(iin).pin_memory().to(dev, non_blocking=True)
+        # outputs: fp64 [sweep_w | sweep_mk | sweep_bound | best_mk | phi | ar_s | ar_e | ev_s | ev_e]
+        ev = n_ev if capture_events else 0
+        self.f_off = np.cumsum([0, n_sweep, n_sweep, n_sweep, n, n, n_ar, n_ar, ev, ev])
+        self.d_fout = torch.empty(int(self.f_off[-1]), dtype=F64, device=dev)
+        # int32 outputs: [sweep_r | ls | le | dlo | dhi | best_xi]
+        self.i_off = np.cumsum([0, n_sweep, n_stage, n_stage, n_stage, n_stage, n])
+        self.d_iout = torch.empty(int(self.i_off[-1]), dtype=I32, device=dev)
+        self.d_ws = torch.empty(max(n_ws, 1), dtype=F64, device=dev)
+        self.capture_events = capture_events
+        self.n_ib = ib.size
+        b = PPBatch()
+        b.n_inst = n
+        b.max_L = self.max_L
+        b.max_V = self.max_V
+        fp = self.d_fin.data_ptr()
+        b.inst = self.d_iin.data_ptr()
+        b.fwd = fp
+        b.bwd = fp + 8 * n_layer
+        b.param = fp + 16 * n_layer
+        b.efwd = fp + 24 * n_layer
+        b.ebwd = fp + 32 * n_layer
+        b.bw = fp + 40 * n_layer
+        b.order = self.d_iin.data_ptr() + 4 * ib.size
+        fo = self.d_fout.data_ptr()
+        fo_ = [fo + 8 * int(x) for x in self.f_off]
+        b.sweep_w, b.sweep_mk, b.sweep_bound, b.best_mk, b.phi = fo_[0], fo_[1], fo_[2], fo_[3], fo_[4]
+        b.ar_start, b.ar_end = fo_[5], fo_[6]
+        b.ev_start = fo_[7] if capture_events else None
+        b.ev_end = fo_[8] if capture_events else None
+        io = self.d_iout.data_ptr()
+        io_ = [io + 4 * int(x) for x in self.i_off]
+        b.sweep_r, b.stage_ls, b.stage_le, b.stage_dlo, b.stage_dhi, b.best_xi = io_[:6]
+        b.ws = self.d_ws.data_ptr()
+        self.batch = b
+        self.lib = lib
+
+    # -- launches -------------------------------------------------------------
+    def run(self, what="spp"):
+        fn = {"spp": self.lib.pp_spp, "rdo": self.lib.pp_rdo, "prm": self.lib.pp_prm,
+              "phi": self.lib.pp_phi, "sweep": self.lib.pp_pe_sweep, "select": self.lib.pp_select}[what]
+        _lib.check(fn(C.byref(self.batch), _stream()))
+
+    # -- results --------------------------------------------------------------
+    def fetch(self):
+        """Copy all outputs to host numpy (one D2H per dtype)."""
+        fo = self.d_fout.cpu().numpy()
+        io = self.d_iout.cpu().numpy()
+        order = self.d_iin[self.n_ib:].cpu().numpy()
+        f = {k: fo[int(self.f_off[i]):int(self.f_off[i + 1])]
+             for i, k in enumerate(("sweep_w", "sweep_mk", "sweep_bound", "best_mk", "phi",
+                                    "ar_start", "ar_end", "ev_start", "ev_end"))}
+        g = {k: io[int(self.i_off[i]):int(self.i_off[i + 1])]
+             for i, k in enumerate(("sweep_r", "ls", "le", "dlo", "dhi", "best_xi"))}
+        f.update(g)
+        f["order"] = order
+        return f
+
+    def d2h_bytes(self):
+        return (self.d_fout.numel() * 8 + self.d_iout.numel() * 4 + (self.d_iin.numel() - self.n_ib) * 4)
+
+    def h2d_bytes(self):
+        return self.d_fin.numel() * 8 + self.d_iin.numel() * 4
+
+    def query(self, cells, max_xi):
+        """PartitionSolver.solve cells: list of (inst, l, xi, r, i) (valid ranges)."""
+        dev = self.d_fin.device
+        q = np.asarray(cells, dtype=np.int32).reshape(-1, 5)
+        nq = q.shape[0]
+        d_q = torch.from_numpy(np.ascontiguousarray(q.T)).to(dev)
+        w = torch.empty(nq, dtype=F64, device=dev)
+        frag = torch.zeros(nq * 4 * max_xi, dtype=I32, device=dev)
+        feas = torch.empty(nq, dtype=I32, device=dev)
+        p = d_q.data_ptr()
+        _lib.check(self.lib.pp_prm_query(C.byref(self.batch), nq, p, p + 4 * nq, p + 8 * nq, p + 12 * nq,
+                                         p + 16 * nq, max_xi, w.data_ptr(), frag.data_ptr(), feas.data_ptr(),
+                                         _stream()))
+        return w.cpu().numpy(), frag.cpu().numpy().reshape(nq, max_xi, 4), feas.cpu().numpy()
+
+    def min_cut(self, k, verts):
+        dev = self.d_fin.device
+        v = torch.tensor(list(verts), dtype=I32, device=dev)
+        in_a = torch.zeros(len(verts), dtype=torch.uint8, device=dev)
+        w = torch.empty(1, dtype=F64, device=dev)
+        _lib.check(self.lib.pp_min_cut(C.byref(self.batch), k, v.data_ptr(), len(verts), in_a.data_ptr(),
+                                       w.data_ptr(), _stream()))
+        return in_a.cpu().numpy(), float(w.cpu().item())
+
+
+@dataclass
+class SimPlan:
+    """A caller plan: stages (ls, le, device positions) + queues in chain order."""
+    inst: int
+    M: int
+    stages: List[tuple]
+    flags: int
+    queues: Optional[List[List[tuple]]] = None   # per resource (chain order): [(m, pos), ...]
+
+
+class SimRun:
+    """Run pp_simulate for plans over a DeviceBatch's instances."""
+
+    def __init__(self, db: DeviceBatch, plans: Sequence[SimPlan], capture_events=True):
+        lib = db.lib
+        dev = db.d_fin.device
+        n = len(plans)
+        P = (PPPlan * n)()
+        ls, le, doff, devs, qoff, qitems = [], [], [], [], [], []
+        lane = ev = ar = 0
+        max_N = 1
+        self.meta = []
+        for k, sp in enumerate(plans):
+            N = len(sp.stages)
+            J = 4 * N - 3
+            R = 2 * N - 1
+            max_N = max(max_N, N)
+            p = P[k]
+            p.inst, p.N, p.M, p.flags = sp.inst, N, sp.M, sp.flags
+            p.stage_off = len(ls)
+            p.devoff_off = len(doff)
+            for a, b_, d in sp.stages:
+                ls.append(a); le.append(b_)
+                doff.append(len(devs))
+                devs.extend(d)
+            doff.append(len(devs))
+            p.queue_off = len(qoff)
+            qbase = len(qitems) // 2
+            if sp.queues is not None:
+                cnt = 0
+                for q in sp.queues:
+                    qoff.append(qbase + cnt)
+                    for m, pos in q:
+                        qitems.extend((m, pos))
+                    cnt += len(q)
+                qoff.append(qbase + cnt)
+            else:
+                qoff.extend([qbase] * (R + 1))
+            p.lane_off = lane; lane += R
+            p.ev_off = ev; ev += sp.M * J
+            p.ar_off = ar; ar += N
+            self.meta.append((N, sp.M, J, R, p.lane_off, p.ev_off, p.ar_off))
+        ib = np.frombuffer(bytes(P), dtype=np.int32)
+        ints = [ib, np.array(ls, np.int32), np.array(le, np.int32), np.array(doff, np.int32),
+                np.array(devs if devs else [0], np.int32), np.array(qoff, np.int32),
+                np.array(qitems if qitems else [0, 0], np.int32)]
+        offs = np.cumsum([0] + [a.size for a in ints])
+        d_in = torch.from_numpy(np.concatenate(ints)).pin_memory().to(dev, non_blocking=True)
+        # fp64 outputs: makespan | bound | ar_s | ar_e | ev_s | ev_e | scratch
+        evn = ev if capture_events else 0
+        self.f_off = np.cumsum([0, n, n, ar, ar, evn, evn, ev])
+        self.d_f = torch.empty(int(self.f_off[-1]), dtype=F64, device=dev)
+        self.i_off = np.cumsum([0, n, lane])
+        self.d_i = torch.empty(int(self.i_off[-1]), dtype=I32, device=dev)
+        self.d_done = torch.empty(n, dtype=torch.int64, device=dev)
+        s = PPSimBatch()
+        s.n_plan, s.max_N = n, max_N
+        ip = d_in.data_ptr()
+        s.plan, s.ls, s.le, s.dev_off, s.devs, s.q_off, s.q_items = (ip + 4 * int(o) for o in offs[:7])
+        fp = self.d_f.data_ptr()
+        fo = [fp + 8 * int(x) for x in self.f_off]
+        s.makespan, s.bound, s.ar_start, s.ar_end = fo[0], fo[1], fo[2], fo[3]
+        s.ev_start = fo[4] if capture_events else None
+        s.ev_end = fo[5] if capture_events else None
+        s.scratch = fo[6]
+        io = self.d_i.data_ptr()
+        s.status, s.head = io, io + 4 * n
+        s.n_done = self.d_done.data_ptr()
+        self._keep = d_in
+        self.sim = s
+        self.n = n
+        self.capture_events = capture_events
+        _lib.check(lib.pp_simulate(C.byref(db.batch), C.byref(s), _stream()))
+
+    def fetch(self):
+        f = self.d_f.cpu().numpy()
+        i = self.d_i.cpu().numpy()
+        done = self.d_done.cpu().numpy()
+        out = []
+        for k, (N, M, J, R, lane, ev, ar) in enumerate(self.meta):
+            rec = dict(makespan=float(f[self.f_off[0] + k]), bound=float(f[self.f_off[1] + k]),
+                       status=int(i[k]), n_done=int(done[k]),
+                       head=i[self.i_off[1] + lane: self.i_off[1] + lane + R],
+                       ar_start=f[self.f_off[2] + ar: self.f_off[2] + ar + N],
+                       ar_end=f[self.f_off[3] + ar: self.f_off[3] + ar + N])
+            if self.capture_events:
+                rec["ev_start"] = f[self.f_off[4] + ev: self.f_off[4] + ev + M * J]
+                rec["ev_end"] = f[self.f_off[5] + ev: self.f_off[5] + ev + M * J]
+            out.append(rec)
+        return out

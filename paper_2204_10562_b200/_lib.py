@@ -1,0 +1,134 @@
+"""ctypes binding of libpipeplan_b200.so (include/pipeplan_b200.h).
+
+The planning path has no CPU fallback: importing the planning modules is
+cheap, but the first planning call loads the library and requires a CUDA
+device; if either is missing it raises :class:`BackendUnavailable` loudly.
+"""
+
+import ctypes as C
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpipeplan_b200.so")
+CSRC = os.path.join(HERE, "csrc")
+REPO = os.path.dirname(HERE)
+
+NVCC_FLAGS = ["-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-fmad=false",
+              "-std=c++17", "-Xcompiler", "-fPIC", "-shared"]
+
+PP_ALLOW_REPLICATION = 1
+PP_SUM_NAIVE = 2
+PP_GIVEN_ORDER = 4
+PP_SIM_FORWARD_BARRIER = 1
+PP_SIM_PE_ORDER = 2
+PP_MAX_LAYERS = 4096
+PP_MAX_GPUS = 512
+
+
+class BackendUnavailable(RuntimeError):
+    """The CUDA planning backend (libpipeplan_b200.so + a CUDA device) is missing."""
+
+
+def build(verbose=False):
+    """Compile the CUDA library in-tree for sm_100a."""
+    nvcc = os.environ.get("NVCC", "nvcc")
+    cmd = [nvcc] + NVCC_FLAGS + ["-o", LIB_PATH, os.path.join(CSRC, "unity.cu")]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.run(cmd, check=True)
+    return LIB_PATH
+
+
+class PPInstance(C.Structure):
+    _fields_ = [("L", C.c_int32), ("V", C.c_int32), ("M", C.c_int32), ("flags", C.c_int32),
+                ("layer_off", C.c_int64), ("bw_off", C.c_int64), ("order_off", C.c_int64),
+                ("sweep_off", C.c_int64), ("stage_off", C.c_int64), ("ws_off", C.c_int64),
+                ("ev_off", C.c_int64), ("ar_off", C.c_int64)]
+
+
+class PPBatch(C.Structure):
+    _fields_ = [("n_inst", C.c_int32), ("max_L", C.c_int32), ("max_V", C.c_int32),
+                ("inst", C.c_void_p),
+                ("fwd", C.c_void_p), ("bwd", C.c_void_p), ("param", C.c_void_p),
+                ("efwd", C.c_void_p), ("ebwd", C.c_void_p), ("bw", C.c_void_p),
+                ("order", C.c_void_p),
+                ("sweep_w", C.c_void_p), ("sweep_mk", C.c_void_p), ("sweep_bound", C.c_void_p),
+                ("sweep_r", C.c_void_p),
+                ("stage_ls", C.c_void_p), ("stage_le", C.c_void_p), ("stage_dlo", C.c_void_p),
+                ("stage_dhi", C.c_void_p),
+                ("best_xi", C.c_void_p), ("best_mk", C.c_void_p), ("phi", C.c_void_p),
+                ("ev_start", C.c_void_p), ("ev_end", C.c_void_p),
+                ("ar_start", C.c_void_p), ("ar_end", C.c_void_p),
+                ("ws", C.c_void_p)]
+
+
+class PPPlan(C.Structure):
+    _fields_ = [("inst", C.c_int32), ("N", C.c_int32), ("M", C.c_int32), ("flags", C.c_int32),
+                ("stage_off", C.c_int64), ("devoff_off", C.c_int64), ("queue_off", C.c_int64),
+                ("lane_off", C.c_int64), ("ev_off", C.c_int64), ("ar_off", C.c_int64)]
+
+
+class PPSimBatch(C.Structure):
+    _fields_ = [("n_plan", C.c_int32), ("max_N", C.c_int32), ("plan", C.c_void_p),
+                ("ls", C.c_void_p), ("le", C.c_void_p), ("dev_off", C.c_void_p), ("devs", C.c_void_p),
+                ("q_off", C.c_void_p), ("q_items", C.c_void_p),
+                ("makespan", C.c_void_p), ("bound", C.c_void_p), ("status", C.c_void_p),
+                ("n_done", C.c_void_p), ("head", C.c_void_p),
+                ("ev_start", C.c_void_p), ("ev_end", C.c_void_p),
+                ("ar_start", C.c_void_p), ("ar_end", C.c_void_p), ("scratch", C.c_void_p)]
+
+
+EXPORTS = ("pp_version", "pp_last_error", "pp_device_count", "pp_layout", "pp_rdo", "pp_prm",
+           "pp_pe_sweep", "pp_select", "pp_spp", "pp_prm_query", "pp_simulate", "pp_min_cut",
+           "pp_launch_count", "pp_phi", "pp_peak_minmax")
+
+_lib = None
+
+
+def load(require_device=True):
+    """Load the library (building it first only if the source tree is present
+    and the .so is missing); with require_device, insist on a CUDA device."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise BackendUnavailable(
+                f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc, sm_100a) first")
+        lib = C.CDLL(LIB_PATH)
+        _declare(lib)
+        _lib = lib
+    if require_device and _lib.pp_device_count() < 1:
+        raise BackendUnavailable("no CUDA device visible: the planning path runs only on the GPU")
+    return _lib
+
+
+def _declare(L):
+    vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+    L.pp_version.restype = C.c_char_p
+    L.pp_last_error.restype = C.c_char_p
+    L.pp_device_count.restype = C.c_int
+    L.pp_launch_count.restype = i64
+    L.pp_layout.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.pp_layout.restype = C.c_int
+    for name in ("pp_rdo", "pp_prm", "pp_pe_sweep", "pp_select", "pp_spp", "pp_phi"):
+        fn = getattr(L, name)
+        fn.argtypes = [vp, vp]
+        fn.restype = C.c_int
+    L.pp_prm_query.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp]
+    L.pp_prm_query.restype = C.c_int
+    L.pp_simulate.argtypes = [vp, vp, vp]
+    L.pp_simulate.restype = C.c_int
+    L.pp_min_cut.argtypes = [vp, i32, vp, i32, vp, vp, vp]
+    L.pp_min_cut.restype = C.c_int
+    L.pp_peak_minmax.argtypes = [vp, i32, vp, vp]
+    L.pp_peak_minmax.restype = C.c_int
+
+
+def check(rc):
+    if rc != 0:
+        msg = _lib.pp_last_error().decode() if _lib is not None else "library not loaded"
+        raise RuntimeError(f"libpipeplan_b200 error {rc}: {msg}")
+
+
+def launch_count():
+    return int(load(require_device=False).pp_launch_count())

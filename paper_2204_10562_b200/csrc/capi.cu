@@ -1,0 +1,215 @@
+// capi.cu — extern "C" entry points of libpipeplan_b200.so (include/pipeplan_b200.h).
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "common.cuh"
+
+namespace pp {
+__global__ void k_prep(pp_batch b);
+__global__ void k_phi(pp_batch b);
+__global__ void k_expand(pp_batch b, int j, int tiles_r);
+__global__ void k_combine(pp_batch b, int i, int tiles_x);
+__global__ void k_backtrack(pp_batch b);
+__global__ void k_query(pp_batch b, int n, const int* qi, const int* ql, const int* qx, const int* qr,
+                        const int* qd, int max_xi, double* w, int* frag, int* feas);
+__global__ void k_rdo(pp_batch b, int w_in_smem);
+__global__ void k_min_cut(pp_batch b, int k, const int* verts, int n, unsigned char* in_a, double* weight,
+                          int w_in_smem);
+__global__ void k_pe_sweep(pp_batch b);
+__global__ void k_select(pp_batch b);
+__global__ void k_replay(pp_batch b);
+__global__ void k_sim_plans(pp_batch b, pp_sim_batch s);
+__global__ void k_peak_minmax(double* out, int iters, double seed);
+}  // namespace pp
+
+using namespace pp;
+
+static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+static int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define PP_CHECK_LAUNCH(name)                                                                        \
+    do {                                                                                             \
+        g_launches.fetch_add(1, std::memory_order_relaxed);                                          \
+        cudaError_t e_ = cudaGetLastError();                                                         \
+        if (e_ != cudaSuccess) return fail(PP_ECUDA, "%s launch: %s", name, cudaGetErrorString(e_)); \
+    } while (0)
+
+static inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+static inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+extern "C" {
+
+const char* pp_version(void) { return "pipeplan_b200 0.1.0 (sm_100a, fp64 bit-exact)"; }
+const char* pp_last_error(void) { return g_err.c_str(); }
+int64_t pp_launch_count(void) { return g_launches.load(); }
+
+int pp_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) { cudaGetLastError(); return 0; }
+    return n;
+}
+
+int pp_layout(int32_t n, const int32_t* L, const int32_t* V, const int32_t* M, const int32_t* flags,
+              pp_instance* inst, int64_t* n_layer, int64_t* n_bw, int64_t* n_order, int64_t* n_sweep,
+              int64_t* n_stage, int64_t* n_ev, int64_t* n_ar, int64_t* n_ws) {
+    int64_t lo = 0, bo = 0, oo = 0, so = 0, sto = 0, wo = 0, eo = 0, ao = 0;
+    for (int k = 0; k < n; ++k) {
+        if (L[k] < 1 || L[k] > PP_MAX_LAYERS) return fail(PP_EINVAL, "instance %d: L=%d outside 1..%d", k, L[k], PP_MAX_LAYERS);
+        if (V[k] < 1 || V[k] > PP_MAX_GPUS) return fail(PP_EINVAL, "instance %d: V=%d outside 1..%d", k, V[k], PP_MAX_GPUS);
+        if (M[k] < 1) return fail(PP_EINVAL, "instance %d: microbatch count must be positive", k);
+        pp_instance& I = inst[k];
+        I.L = L[k]; I.V = V[k]; I.M = M[k]; I.flags = flags[k];
+        I.layer_off = lo; lo += L[k];
+        I.bw_off = bo; bo += (int64_t)V[k] * V[k];
+        I.order_off = oo; oo += V[k];
+        I.sweep_off = so; so += V[k];
+        I.stage_off = sto; sto += (int64_t)V[k] * (V[k] + 1) / 2;
+        I.ws_off = wo; wo += ws_layout(L[k], V[k]).total;
+        I.ev_off = eo; eo += (int64_t)M[k] * (4 * V[k] - 3);
+        I.ar_off = ao; ao += V[k];
+    }
+    *n_layer = lo; *n_bw = bo; *n_order = oo; *n_sweep = so; *n_stage = sto; *n_ev = eo; *n_ar = ao; *n_ws = wo;
+    return PP_OK;
+}
+
+int pp_rdo(const pp_batch* b, void* stream) {
+    if (b->n_inst <= 0) return PP_OK;
+    const int V = b->max_V;
+    const int in_smem = V <= 128;
+    const size_t smem = (in_smem ? sizeof(double) * V * V : 0) + rdo_state_bytes(V);
+    cudaFuncSetAttribute(k_rdo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_rdo<<<b->n_inst, 128, smem, S(stream)>>>(*b, in_smem);
+    PP_CHECK_LAUNCH("k_rdo");
+    return PP_OK;
+}
+
+int pp_prm(const pp_batch* b, void* stream) {
+    if (b->n_inst <= 0) return PP_OK;
+    const int maxL = b->max_L, maxV = b->max_V;
+    dim3 gp(b->n_inst, maxL > maxV ? maxL : maxV);
+    k_prep<<<gp, 128, 0, S(stream)>>>(*b);
+    PP_CHECK_LAUNCH("k_prep");
+    const int tiles_l = ceil_div(maxL, 32);
+    for (int i = 1; i <= maxV; ++i) {
+        const int tiles_x = ceil_div(i, 32);
+        dim3 gc(b->n_inst, i, tiles_l * tiles_x);
+        k_combine<<<gc, 128, 0, S(stream)>>>(*b, i, tiles_x);
+        PP_CHECK_LAUNCH("k_combine");
+        if (i < maxV && maxL > 1) {
+            const int tiles_xi = ceil_div(i, 32), tiles_r = ceil_div(maxV - i, 32);
+            dim3 ge(b->n_inst, maxL - 1, tiles_xi * tiles_r);
+            k_expand<<<ge, 128, 0, S(stream)>>>(*b, i, tiles_r);
+            PP_CHECK_LAUNCH("k_expand");
+        }
+    }
+    dim3 gb(b->n_inst, maxV);
+    k_backtrack<<<gb, 32, 0, S(stream)>>>(*b);
+    PP_CHECK_LAUNCH("k_backtrack");
+    return PP_OK;
+}
+
+static size_t sim_smem(int maxN) {
+    const int R = 2 * maxN - 1;
+    return sizeof(double) * (4 * R + 64);
+}
+
+static int sim_block(int maxN) {
+    const int R = 2 * maxN - 1;
+    int t = (R + 31) / 32 * 32;
+    return t < 32 ? 32 : t;
+}
+
+int pp_pe_sweep(const pp_batch* b, void* stream) {
+    if (b->n_inst <= 0) return PP_OK;
+    const size_t smem = sim_smem(b->max_V);
+    cudaFuncSetAttribute(k_pe_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dim3 g(b->n_inst, b->max_V);
+    k_pe_sweep<<<g, sim_block(b->max_V), smem, S(stream)>>>(*b);
+    PP_CHECK_LAUNCH("k_pe_sweep");
+    return PP_OK;
+}
+
+int pp_select(const pp_batch* b, void* stream) {
+    if (b->n_inst <= 0) return PP_OK;
+    k_select<<<b->n_inst, 32, 0, S(stream)>>>(*b);
+    PP_CHECK_LAUNCH("k_select");
+    if (b->ev_start) {
+        const size_t smem = sim_smem(b->max_V);
+        cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_replay<<<b->n_inst, sim_block(b->max_V), smem, S(stream)>>>(*b);
+        PP_CHECK_LAUNCH("k_replay");
+    }
+    return PP_OK;
+}
+
+int pp_phi(const pp_batch* b, void* stream) {
+    if (b->n_inst <= 0) return PP_OK;
+    k_phi<<<b->n_inst, 128, 0, S(stream)>>>(*b);
+    PP_CHECK_LAUNCH("k_phi");
+    return PP_OK;
+}
+
+int pp_spp(const pp_batch* b, void* stream) {
+    int rc;
+    if ((rc = pp_phi(b, stream))) return rc;
+    if ((rc = pp_rdo(b, stream))) return rc;
+    if ((rc = pp_prm(b, stream))) return rc;
+    if ((rc = pp_pe_sweep(b, stream))) return rc;
+    return pp_select(b, stream);
+}
+
+int pp_prm_query(const pp_batch* b, int32_t n_query, const int32_t* q_inst, const int32_t* q_l,
+                 const int32_t* q_xi, const int32_t* q_r, const int32_t* q_i, int32_t max_xi, double* w,
+                 int32_t* frag, int32_t* feasible, void* stream) {
+    if (n_query <= 0) return PP_OK;
+    k_query<<<n_query, 32, 0, S(stream)>>>(*b, n_query, q_inst, q_l, q_xi, q_r, q_i, max_xi, w, frag, feasible);
+    PP_CHECK_LAUNCH("k_query");
+    return PP_OK;
+}
+
+int pp_simulate(const pp_batch* ib, const pp_sim_batch* s, void* stream) {
+    if (s->n_plan <= 0) return PP_OK;
+    if (s->max_N < 1 || s->max_N > PP_MAX_GPUS) return fail(PP_EINVAL, "max_N=%d outside 1..%d", s->max_N, PP_MAX_GPUS);
+    const size_t smem = sim_smem(s->max_N);
+    cudaFuncSetAttribute(k_sim_plans, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_sim_plans<<<s->n_plan, sim_block(s->max_N), smem, S(stream)>>>(*ib, *s);
+    PP_CHECK_LAUNCH("k_sim_plans");
+    return PP_OK;
+}
+
+int pp_peak_minmax(double* d_out, int32_t iters, int64_t* n_ops, void* stream) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int blocks = sms * 8, threads = 256;
+    k_peak_minmax<<<blocks, threads, 0, S(stream)>>>(d_out, iters, 0.5);
+    PP_CHECK_LAUNCH("k_peak_minmax");
+    *n_ops = (int64_t)blocks * threads * iters * 16;
+    return PP_OK;
+}
+
+int pp_min_cut(const pp_batch* b, int32_t k, const int32_t* verts, int32_t n, uint8_t* in_a, double* weight,
+               void* stream) {
+    if (n < 2) return fail(PP_EINVAL, "min cut needs at least 2 vertices");
+    const int V = b->max_V;
+    const int in_smem = V <= 128;
+    const size_t smem = (in_smem ? sizeof(double) * V * V : 0) + rdo_state_bytes(V);
+    cudaFuncSetAttribute(k_min_cut, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_min_cut<<<1, 32, smem, S(stream)>>>(*b, k, verts, n, in_a, weight, in_smem);
+    PP_CHECK_LAUNCH("k_min_cut");
+    return PP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,595 @@
+// prm.cu — device ordering (RDO), DP tables and the PRM dynamic program.
+//
+// Reference: ordering.py:30-113 (Stoer-Wagner RDO), partition.py:41-162
+// (W(l, xi, r, i) recursion), cost.py:64-99 (bandwidth minima, AllReduce).
+//
+// The DP runs as a wavefront over the device prefix i (W(., ., ., i) needs
+// only slices j < i, partition.py:133).  The reference's candidate
+//     w(l', r') = max(W(l', xi-1, r', j), chan(l', r'), stage(l'))
+// is evaluated in factored form (bit-exact: max/min are exact and monotone):
+//   expand(j):  X(l', xi, r, j+r) = min_{r'} max(W_j(l', xi-1, r'), chan(l', r', r, j+r))
+//   combine(i): W_i(l, r, xi)     = min_{l'} max(X(l', xi, r, i), stage(l', l, r, i))
+// Both are (min, max)-semiring matrix products; each CTA computes a 32x32
+// output tile from smem-staged 32x32 operand tiles, 4x2 / 2x4 register
+// micro-tiles per thread.  Arg-mins are not stored: the backtrack re-derives
+// the reference's first-found (l', r') for the few cells on each chosen path.
+#include "common.cuh"
+
+namespace pp {
+
+// ----------------------------------------------------------------------------
+// k_prep: per instance tables (partition.py:59-93, cost.py:64-99, cost.py:126-142)
+//   prefix[l] = (prefix[l-1] + fwd_l) + bwd_l                     partition.py:62
+//   psum[ls][le] = sum(param[ls..le])  (CPython sum)              cost.py:98
+//   minpair[lo][hi] = min pairwise bw over order[lo..hi]          cost.py:64-71
+//   cross(rp, r, i) = min bw between order[i-r-rp+1..i-r] and order[i-r+1..i]
+//                                                                  partition.py:82-93
+// grid (n_inst, max(maxL, maxV)); row y handles psum row ls=y+1, minpair row
+// lo=y+1 and the cross table of i=y+1.  Row 0 also computes prefix and phi.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_prep(pp_batch b) {
+    const pp_instance I = b.inst[blockIdx.x];
+    const int L = I.L, V = I.V;
+    const bool naive = I.flags & PP_SUM_NAIVE;
+    const WsLayout lay = ws_layout(L, V);
+    double* ws = b.ws + I.ws_off;
+    const double* fwd = b.fwd + I.layer_off;
+    const double* bwd = b.bwd + I.layer_off;
+    const double* par = b.param + I.layer_off;
+    const double* bw = b.bw + I.bw_off;
+    const int* order = b.order + I.order_off;
+    const int row = blockIdx.y + 1;
+    const int t = threadIdx.x;
+
+    if (row == 1 && t == 0) {
+        double p = 0.0;
+        ws[lay.prefix] = 0.0;
+        for (int l = 1; l <= L; ++l) {
+            p = p + fwd[l - 1] + bwd[l - 1];
+            ws[lay.prefix + l] = p;
+        }
+    }
+    // psum row ls = row: running CPython sum over le = ls..L
+    if (row <= L && t == 0) {
+        PySum s(naive);
+        for (int le = row; le <= L; ++le) {
+            s.add(par[le - 1]);
+            ws[lay.psum + (int64_t)(row - 1) * L + (le - 1)] = s.value();
+        }
+    }
+    if (row > V) return;
+    // minpair row lo = row: colmin(hi) = min_{a in [lo, hi-1]} bw(order a, order hi); prefix-min over hi
+    __shared__ double s_col[PP_MAX_GPUS];
+    for (int hi = row + 1 + t; hi <= V; hi += blockDim.x) {
+        double m = PP_INF;
+        const double* bwr = bw + (int64_t)order[hi - 1] * V;
+        for (int a = row; a < hi; ++a) m = fmin(m, bwr[order[a - 1]]);
+        s_col[hi - 1] = m;
+    }
+    __syncthreads();
+    if (t == 0) {
+        double m = PP_INF;
+        ws[lay.minpair + (int64_t)(row - 1) * V + (row - 1)] = m;
+        for (int hi = row + 1; hi <= V; ++hi) {
+            m = fmin(m, s_col[hi - 1]);
+            ws[lay.minpair + (int64_t)(row - 1) * V + (hi - 1)] = m;
+        }
+    }
+    // cross table for i = row: thread per r in [1, i-1], sequential over rp
+    const int i = row;
+    for (int r = 1 + t; r < i; r += blockDim.x) {
+        const int lo = i - r + 1;
+        double m = PP_INF;
+        for (int rp = 1; rp <= i - r; ++rp) {
+            const double* bwr = bw + (int64_t)order[lo - 1 - rp] * V;   // new left device, rank lo - rp
+            for (int c = lo; c <= i; ++c) m = fmin(m, bwr[order[c - 1]]);
+            ws[lay.cross + cross_idx(V, i, r, rp)] = m;
+        }
+    }
+}
+
+// phi (cost.py:126-142): max(p_max * b_max, d_max) / Gamma * (1/b_min - 1/b_max),
+// 0 on single-GPU or uniform clusters.  One CTA (128 threads) per instance.
+__global__ void __launch_bounds__(128) k_phi(pp_batch b) {
+    const pp_instance I = b.inst[blockIdx.x];
+    const int L = I.L, V = I.V;
+    const double* fwd = b.fwd + I.layer_off;
+    const double* bwd = b.bwd + I.layer_off;
+    const double* bw = b.bw + I.bw_off;
+    const int t = threadIdx.x;
+    __shared__ double s_red[2][128];
+    double mn = PP_INF, mx = -PP_INF;
+    for (int e = t; e < V * V; e += blockDim.x) {
+        const int a = e / V, c = e % V;
+        if (a < c) { const double x = bw[e]; mn = fmin(mn, x); mx = fmax(mx, x); }
+    }
+    s_red[0][t] = mn; s_red[1][t] = mx;
+    __syncthreads();
+    if (t != 0) return;
+    for (int k = 1; k < blockDim.x; ++k) { mn = fmin(mn, s_red[0][k]); mx = fmax(mx, s_red[1][k]); }
+    double pmax = 0.0, dmax = 0.0;
+    PySum g(I.flags & PP_SUM_NAIVE);
+    for (int l = 0; l < L; ++l) {
+        const double tot = fwd[l] + bwd[l];
+        g.add(tot);
+        if (l == 0 || tot > pmax) pmax = tot;
+    }
+    for (int e = 0; e < L - 1; ++e) {
+        const double d = b.efwd[I.layer_off + e] + b.ebwd[I.layer_off + e];
+        if (e == 0 || d > dmax) dmax = d;
+    }
+    const double gamma = g.value() / (double)V;   // cost.py:128
+    double phi = 0.0;
+    if (!(V == 1 || mn == mx)) {
+        const double num = (dmax > pmax * mx) ? dmax : pmax * mx;
+        phi = num / gamma * (1.0 / mn - 1.0 / mx);
+    }
+    b.phi[blockIdx.x] = phi;
+}
+
+// ----------------------------------------------------------------------------
+// k_expand(j): after slice j is final, X for every target (r, i = j + r).
+// grid (n_inst, maxL-1, tiles_xi * tiles_r); CTA tile = 32 xi x 32 r for one l'.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_expand(pp_batch b, int j, int tiles_r) {
+    const pp_instance I = b.inst[blockIdx.x];
+    const int L = I.L, V = I.V;
+    const int lp = blockIdx.y + 1;
+    if (j >= V || lp > L - 1) return;
+    const int txi = blockIdx.z / tiles_r, tr = blockIdx.z % tiles_r;
+    const int xi0 = 2 + 32 * txi, r0 = 1 + 32 * tr;
+    if (xi0 > j + 1 || r0 > V - j) return;
+    const WsLayout lay = ws_layout(L, V);
+    double* ws = b.ws + I.ws_off;
+    const double* Wj = ws + lay.W;
+    const double* cross = ws + lay.cross;
+    const double Mp = (double)I.M * (b.efwd[I.layer_off + lp - 1] + b.ebwd[I.layer_off + lp - 1]);   // partition.py:131,137
+
+    __shared__ double As[32][33];   // [r'][xi]   W_j(l', xi-1, r')
+    __shared__ double Bs[32][33];   // [r'][r]    chan(l', r', r, j+r)
+    const int t = threadIdx.x, cx = t & 7, cr = t >> 3;
+    double acc[4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) { acc[a][0] = PP_INF; acc[a][1] = PP_INF; }
+
+    for (int rp0 = 1; rp0 <= j; rp0 += 32) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int e = t + 128 * q, rr = e >> 5, cc = e & 31;
+            const int rp = rp0 + rr;
+            const int xip = xi0 + cc - 1;   // W_j's xi index = xi - 1
+            As[rr][cc] = (rp <= j && xip <= j) ? Wj[W_idx(L, j, lp, rp, xip)] : PP_INF;
+            const int r = r0 + cc;
+            double c = PP_INF;
+            if (rp <= j && r <= V - j) {
+                const int i = j + r;
+                c = Mp / ((double)(rp * r) * cross[cross_idx(V, i, r, rp)]);
+            }
+            Bs[rr][cc] = c;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) {
+            double a0 = As[k][cx * 4 + 0], a1 = As[k][cx * 4 + 1], a2 = As[k][cx * 4 + 2], a3 = As[k][cx * 4 + 3];
+            double b0 = Bs[k][cr * 2 + 0], b1 = Bs[k][cr * 2 + 1];
+            acc[0][0] = fmin(acc[0][0], fmax(a0, b0)); acc[0][1] = fmin(acc[0][1], fmax(a0, b1));
+            acc[1][0] = fmin(acc[1][0], fmax(a1, b0)); acc[1][1] = fmin(acc[1][1], fmax(a1, b1));
+            acc[2][0] = fmin(acc[2][0], fmax(a2, b0)); acc[2][1] = fmin(acc[2][1], fmax(a2, b1));
+            acc[3][0] = fmin(acc[3][0], fmax(a3, b0)); acc[3][1] = fmin(acc[3][1], fmax(a3, b1));
+        }
+        __syncthreads();
+    }
+    double* X = ws + lay.X;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int xi = xi0 + cx * 4 + a;
+        if (xi > j + 1) continue;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int r = r0 + cr * 2 + c;
+            if (r > V - j) continue;
+            X[X_base(L, j + r, r) + (int64_t)(lp - 1) * j + (xi - 2)] = acc[a][c];
+        }
+    }
+}
+
+// stage(l', l, r, i) = (M * span(l'+1, l)) / r (+ sync(l'+1, l, i-r+1, i) if r > 1)
+// partition.py:127-129, cost.py:99.
+__device__ __forceinline__ double stage_term(int M, int L, int V, const double* prefix, const double* psum,
+                                             const double* minpair, int lp, int l, int r, int i) {
+    double s = (double)M * (prefix[l] - prefix[lp]) / (double)r;
+    if (r > 1) {
+        double total = psum[(int64_t)lp * L + (l - 1)];
+        s += 2.0 * (double)(r - 1) * total / ((double)r * minpair[(int64_t)(i - r) * V + (i - 1)]);
+    }
+    return s;
+}
+
+// ----------------------------------------------------------------------------
+// k_combine(i): slice W_i for every (r, l, xi).  grid (n_inst, i, tiles_l * tiles_x).
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_combine(pp_batch b, int i, int tiles_x) {
+    const pp_instance I = b.inst[blockIdx.x];
+    const int L = I.L, V = I.V, M = I.M;
+    const int r = blockIdx.y + 1;
+    if (i > V || r > i) return;
+    const int tl = blockIdx.z / tiles_x, tx = blockIdx.z % tiles_x;
+    const int l0 = 1 + 32 * tl, x0 = 1 + 32 * tx;
+    if (l0 > L || x0 > i) return;
+    const bool allow = I.flags & PP_ALLOW_REPLICATION;
+    const WsLayout lay = ws_layout(L, V);
+    double* ws = b.ws + I.ws_off;
+    const double* prefix = ws + lay.prefix;
+    const double* psum = ws + lay.psum;
+    const double* minpair = ws + lay.minpair;
+    double* Wi = ws + lay.W + W_base(L, i);
+    const int t = threadIdx.x;
+
+    if (r == i || (!allow && r != 1)) {
+        // partition.py:103-104 (no replication) and :115-121 (base / INF rules)
+        for (int e = t; e < 32 * 32; e += 128) {
+            const int l = l0 + (e >> 5), xi = x0 + (e & 31);
+            if (l > L || xi > i) continue;
+            double v = PP_INF;
+            if (r == i && xi == 1 && (allow || i == 1)) {
+                // partition.py:117-119: M * span(1, l) / i + sync(1, l, 1, i)
+                double sync = 0.0;
+                if (i > 1) sync = 2.0 * (double)(i - 1) * psum[l - 1] / ((double)i * minpair[i - 1]);
+                v = (double)M * (prefix[l] - prefix[0]) / (double)i + sync;
+            }
+            Wi[((int64_t)(l - 1) * i + (r - 1)) * i + (xi - 1)] = v;
+        }
+        return;
+    }
+    const int j = i - r;
+    const double* X = ws + lay.X + X_base(L, i, r);
+    __shared__ double Xs[32][33];   // [l'][xi]
+    __shared__ double Ss[32][33];   // [l'][l]
+    const int cx = t & 15, cl = t >> 4;
+    double acc[4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) { acc[a][0] = PP_INF; acc[a][1] = PP_INF; }
+    const int kmin = max(1, x0 - 1);
+    const int kmax = min(L - 1, l0 + 30);
+    for (int lp0 = kmin; lp0 <= kmax; lp0 += 32) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int e = t + 128 * q, rr = e >> 5, cc = e & 31;
+            const int lp = lp0 + rr;
+            const int xi = x0 + cc;
+            Xs[rr][cc] = (lp <= kmax && xi >= 2 && xi <= j + 1) ? X[(int64_t)(lp - 1) * j + (xi - 2)] : PP_INF;
+            const int l = l0 + cc;
+            Ss[rr][cc] = (lp < l && l <= L) ? stage_term(M, L, V, prefix, psum, minpair, lp, l, r, i) : PP_INF;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) {
+            double x0v = Xs[k][cx * 2 + 0], x1v = Xs[k][cx * 2 + 1];
+            double s0 = Ss[k][cl * 4 + 0], s1 = Ss[k][cl * 4 + 1], s2 = Ss[k][cl * 4 + 2], s3 = Ss[k][cl * 4 + 3];
+            acc[0][0] = fmin(acc[0][0], fmax(x0v, s0)); acc[0][1] = fmin(acc[0][1], fmax(x1v, s0));
+            acc[1][0] = fmin(acc[1][0], fmax(x0v, s1)); acc[1][1] = fmin(acc[1][1], fmax(x1v, s1));
+            acc[2][0] = fmin(acc[2][0], fmax(x0v, s2)); acc[2][1] = fmin(acc[2][1], fmax(x1v, s2));
+            acc[3][0] = fmin(acc[3][0], fmax(x0v, s3)); acc[3][1] = fmin(acc[3][1], fmax(x1v, s3));
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int l = l0 + cl * 4 + a;
+        if (l > L) continue;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int xi = x0 + cx * 2 + c;
+            if (xi > i) continue;
+            Wi[((int64_t)(l - 1) * i + (r - 1)) * i + (xi - 1)] = acc[a][c];
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------
+// Backtrack: re-derive the reference's first-found realizing (l', r') of a
+// cell (partition.py:126-141 loop order, strict `best > w`) by scanning the
+// candidates in lexicographic order for the first whose value equals W.
+// Warp-cooperative; writes stage n (1-based) via the callback arrays.
+// ----------------------------------------------------------------------------
+__device__ void dp_walk(const pp_batch& b, const pp_instance& I, int l, int x, int r, int i, double w,
+                        int* o_ls, int* o_le, int* o_dlo, int* o_dhi) {
+    const int L = I.L, V = I.V, M = I.M;
+    const WsLayout lay = ws_layout(L, V);
+    const double* ws = b.ws + I.ws_off;
+    const double* prefix = ws + lay.prefix;
+    const double* psum = ws + lay.psum;
+    const double* minpair = ws + lay.minpair;
+    const double* cross = ws + lay.cross;
+    const double* W = ws + lay.W;
+    const int lane = threadIdx.x & 31;
+    while (x >= 2) {
+        const int j = i - r;
+        const int nl = l - (x - 1);
+        const int total = nl * j;
+        int found = -1;
+        for (int base = 0; base < total && found < 0; base += 32) {
+            const int k = base + lane;
+            bool match = false;
+            if (k < total) {
+                const int lp = x - 1 + k / j, rp = 1 + k % j;
+                const double sub = W[W_idx(L, j, lp, rp, x - 1)];
+                const double Mp = (double)M * (b.efwd[I.layer_off + lp - 1] + b.ebwd[I.layer_off + lp - 1]);
+                const double chan = Mp / ((double)(rp * r) * cross[cross_idx(V, i, r, rp)]);
+                const double st = stage_term(M, L, V, prefix, psum, minpair, lp, l, r, i);
+                const double v = fmax(fmax(sub, chan), st);
+                match = (v == w);
+            }
+            const unsigned mask = __ballot_sync(0xffffffffu, match);
+            if (mask) found = base + __ffs(mask) - 1;
+        }
+        if (found < 0) {   // cannot happen for a consistent table; leave a detectable hole
+            if (lane == 0) { o_ls[x - 1] = 0; o_le[x - 1] = 0; o_dlo[x - 1] = 0; o_dhi[x - 1] = 0; }
+            return;
+        }
+        const int lp = x - 1 + found / j, rp = 1 + found % j;
+        if (lane == 0) { o_ls[x - 1] = lp + 1; o_le[x - 1] = l; o_dlo[x - 1] = i - r + 1; o_dhi[x - 1] = i; }
+        w = W[W_idx(L, j, lp, rp, x - 1)];
+        l = lp; i = j; r = rp; --x;
+    }
+    if (lane == 0) { o_ls[0] = 1; o_le[0] = l; o_dlo[0] = 1; o_dhi[0] = i; }
+}
+
+// best_partition(xi) for every xi (partition.py:144-162).  grid (n_inst, maxV), block 32.
+__global__ void __launch_bounds__(32) k_backtrack(pp_batch b) {
+    const pp_instance I = b.inst[blockIdx.x];
+    const int xi = blockIdx.y + 1;
+    const int L = I.L, V = I.V;
+    if (xi > V) return;
+    const WsLayout lay = ws_layout(L, V);
+    const double* W = b.ws + I.ws_off + lay.W;
+    const int lane = threadIdx.x;
+    double best = PP_INF;
+    int br = 0;
+    for (int r = 1 + lane; r <= V; r += 32) {
+        const double v = (xi <= L) ? W[W_idx(L, V, L, r, xi)] : PP_INF;
+        if (v < best) { best = v; br = r; }   // ascending r per lane: first r on ties
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, off);
+        const int orr = __shfl_xor_sync(0xffffffffu, br, off);
+        if (ov < best || (ov == best && orr != 0 && (br == 0 || orr < br))) { best = ov; br = orr; }
+    }
+    const int64_t so = I.sweep_off + xi - 1;
+    if (lane == 0) { b.sweep_w[so] = best; b.sweep_r[so] = br; }
+    if (br == 0) return;
+    const int64_t st = I.stage_off + (int64_t)xi * (xi - 1) / 2;
+    dp_walk(b, I, L, xi, br, V, best, b.stage_ls + st, b.stage_le + st, b.stage_dlo + st, b.stage_dhi + st);
+}
+
+// PartitionSolver.solve queries (partition.py:95-142).  One warp per query.
+__global__ void __launch_bounds__(32) k_query(pp_batch b, int n, const int* qi, const int* ql, const int* qx,
+                                              const int* qr, const int* qd, int max_xi, double* w, int* frag,
+                                              int* feas) {
+    const int q = blockIdx.x;
+    if (q >= n) return;
+    const pp_instance I = b.inst[qi[q]];
+    const int l = ql[q], x = qx[q], r = qr[q], i = qd[q];
+    const WsLayout lay = ws_layout(I.L, I.V);
+    const double* W = b.ws + I.ws_off + lay.W;
+    double v = PP_INF;
+    if (x <= i && r <= i) v = W[W_idx(I.L, i, l, r, x)];
+    const int lane = threadIdx.x;
+    // Base cells (xi = 1, r = i) are feasible with any value; others iff finite
+    // (an infinite candidate never passes `best > w`, partition.py:139).
+    const bool f = (x == 1 && r == i && x <= i) ? (v == v && (I.flags & PP_ALLOW_REPLICATION || i == 1)) : (v < PP_INF);
+    if (lane == 0) { w[q] = v; feas[q] = f ? 1 : 0; }
+    if (!f) return;
+    int* fr = frag + (int64_t)q * 4 * max_xi;
+    // fragments stored interleaved (ls, le, dlo, dhi) per stage: use strided views
+    __shared__ int s_ls[PP_MAX_GPUS], s_le[PP_MAX_GPUS], s_dlo[PP_MAX_GPUS], s_dhi[PP_MAX_GPUS];
+    dp_walk(b, I, l, x, r, i, v, s_ls, s_le, s_dlo, s_dhi);
+    __syncwarp();
+    for (int n2 = lane; n2 < x; n2 += 32) {
+        fr[4 * n2 + 0] = s_ls[n2]; fr[4 * n2 + 1] = s_le[n2]; fr[4 * n2 + 2] = s_dlo[n2]; fr[4 * n2 + 3] = s_dhi[n2];
+    }
+}
+
+// ----------------------------------------------------------------------------
+// RDO (ordering.py:30-113).  One CTA per instance; each warp runs the
+// Stoer-Wagner min cut of one vertex group (a node of the recursion tree);
+// groups of one recursion level are cut concurrently by different warps.
+// A group is identified by its lowest rank `lo`; every vertex stores the lo
+// of its current group, so the final rank of vertex v is lo[v].
+// Per-vertex state is indexed by the global vertex index (groups are
+// disjoint, so warps never touch the same entries).
+// ----------------------------------------------------------------------------
+
+struct RdoSmem {
+    double* w;       // V*V contracted weights (smem or global scratch)
+    double* adj;     // [V]
+    int* lo;         // [V]
+    int* grp;        // [V] supernode of each vertex
+    int* cnt;        // [V] group sizes by lo-1
+    int* first;      // [V] smallest member by lo-1
+    int* glist;      // [V] groups to cut this level
+    int* mem;        // [RDO_WARPS][V] member lists
+    unsigned char* alive;
+    unsigned char* inadj;
+    unsigned char* side;
+};
+
+// Cut the group whose members are mem[0..n) (ascending); returns weight and
+// leaves side flags (1 = side_a, the side holding mem[0]) in S.side.
+__device__ double warp_min_cut(const RdoSmem& S, const double* bw, int V, const int* mem, int n) {
+    const int lane = threadIdx.x & 31;
+    double* w = S.w;
+    // every cut starts from the cluster's own weights (ordering.py:50-54)
+    for (int e = lane; e < n * n; e += 32) {
+        const int a = mem[e / n], c = mem[e % n];
+        w[(int64_t)a * V + c] = (a == c) ? 0.0 : bw[(int64_t)a * V + c];
+    }
+    for (int k = lane; k < n; k += 32) { const int v = mem[k]; S.alive[v] = 1; S.grp[v] = v; S.side[v] = 0; }
+    __syncwarp();
+    double best_weight = PP_INF;
+    int n_alive = n;
+    const int start = mem[0];   // the smallest id never merges away (merged = min(s, t))
+    while (n_alive > 1) {
+        for (int k = lane; k < n; k += 32) {
+            const int v = mem[k];
+            const unsigned char in = S.alive[v] && v != start;
+            S.inadj[v] = in;
+            if (in) S.adj[v] = w[(int64_t)start * V + v];
+        }
+        __syncwarp();
+        int s = start, t = start;
+        double cut = 0.0;
+        for (int step = 0; step < n_alive - 1; ++step) {
+            double bv = -PP_INF;
+            int bi = 0x7fffffff;
+            for (int k = lane; k < n; k += 32) {
+                const int v = mem[k];
+                if (S.inadj[v]) {
+                    const double a = S.adj[v];
+                    if (a > bv || (a == bv && v < bi)) { bv = a; bi = v; }
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+                if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+            }
+            const int nv = bi;
+            cut = bv;
+            s = t; t = nv;
+            __syncwarp();
+            if (lane == 0) S.inadj[nv] = 0;
+            __syncwarp();
+            const double* row = w + (int64_t)nv * V;
+            for (int k = lane; k < n; k += 32) {   // adj[u] += wt(next_v, u)  (ordering.py:69-70)
+                const int v = mem[k];
+                if (S.inadj[v]) S.adj[v] = S.adj[v] + row[v];
+            }
+            __syncwarp();
+        }
+        if (cut < best_weight) {   // ordering.py:73-75
+            best_weight = cut;
+            for (int k = lane; k < n; k += 32) { const int v = mem[k]; S.side[v] = (S.grp[v] == t); }
+        }
+        const int merged = min(s, t), other = max(s, t);   // ordering.py:77-85
+        for (int k = lane; k < n; k += 32) {
+            const int u = mem[k];
+            if (S.alive[u] && u != s && u != t) {
+                const double x = w[(int64_t)s * V + u] + w[(int64_t)t * V + u];
+                w[(int64_t)merged * V + u] = x;
+                w[(int64_t)u * V + merged] = x;
+            }
+        }
+        __syncwarp();
+        for (int k = lane; k < n; k += 32) { const int v = mem[k]; if (S.grp[v] == other) S.grp[v] = merged; }
+        __syncwarp();
+        if (lane == 0) S.alive[other] = 0;
+        __syncwarp();
+        --n_alive;
+    }
+    // side holding the smallest id becomes side_a (ordering.py:87-91)
+    const unsigned char low = S.side[mem[0]];
+    __syncwarp();
+    for (int k = lane; k < n; k += 32) { const int v = mem[k]; S.side[v] = low ? S.side[v] : !S.side[v]; }
+    __syncwarp();
+    return best_weight;
+}
+
+__device__ RdoSmem rdo_carve(char* base, double* w, int V) {
+    RdoSmem S;
+    char* p = base;
+    S.w = w;
+    S.adj = (double*)p; p += sizeof(double) * V;
+    S.lo = (int*)p; p += sizeof(int) * V;
+    S.grp = (int*)p; p += sizeof(int) * V;
+    S.cnt = (int*)p; p += sizeof(int) * V;
+    S.first = (int*)p; p += sizeof(int) * V;
+    S.glist = (int*)p; p += sizeof(int) * V;
+    S.mem = (int*)p; p += sizeof(int) * V * RDO_WARPS;
+    S.alive = (unsigned char*)p; p += V;
+    S.inadj = (unsigned char*)p; p += V;
+    S.side = (unsigned char*)p; p += V;
+    return S;
+}
+
+
+__global__ void __launch_bounds__(32 * RDO_WARPS) k_rdo(pp_batch b, int w_in_smem) {
+    const pp_instance I = b.inst[blockIdx.x];
+    if (I.flags & PP_GIVEN_ORDER) return;
+    const int V = I.V;
+    extern __shared__ double smem_d[];
+    char* sm = (char*)smem_d;
+    double* w;
+    if (w_in_smem) { w = (double*)sm; sm += sizeof(double) * V * V; }
+    else w = b.ws + I.ws_off + ws_layout(I.L, V).rdo_w;
+    const RdoSmem S = rdo_carve(sm, w, V);
+    const double* bw = b.bw + I.bw_off;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    for (int e = t; e < V * V; e += blockDim.x) w[e] = (e / V == e % V) ? 0.0 : bw[e];
+    for (int v = t; v < V; v += blockDim.x) S.lo[v] = 1;
+    __syncthreads();
+    __shared__ int s_ngroups;
+    for (;;) {
+        for (int v = t; v < V; v += blockDim.x) { S.cnt[v] = 0; S.first[v] = 0x7fffffff; }
+        if (t == 0) s_ngroups = 0;
+        __syncthreads();
+        for (int v = t; v < V; v += blockDim.x) { atomicAdd(&S.cnt[S.lo[v] - 1], 1); atomicMin(&S.first[S.lo[v] - 1], v); }
+        __syncthreads();
+        for (int v = t; v < V; v += blockDim.x) {
+            const int g = S.lo[v];
+            if (S.cnt[g - 1] >= 2 && S.first[g - 1] == v) S.glist[atomicAdd(&s_ngroups, 1)] = g;
+        }
+        __syncthreads();
+        const int ng = s_ngroups;
+        if (ng == 0) break;
+        for (int gi = warp; gi < ng; gi += RDO_WARPS) {
+            const int g = S.glist[gi];
+            int* mem = S.mem + warp * V;
+            int n = 0;
+            for (int v0 = 0; v0 < V; v0 += 32) {   // ascending member list
+                const int v = v0 + lane;
+                const bool in = v < V && S.lo[v] == g;
+                const unsigned m = __ballot_sync(0xffffffffu, in);
+                if (in) mem[n + __popc(m & ((1u << lane) - 1))] = v;
+                n += __popc(m);
+            }
+            __syncwarp();
+            warp_min_cut(S, bw, V, mem, n);
+            int na = 0;
+            for (int k0 = 0; k0 < n; k0 += 32) {
+                const int k = k0 + lane;
+                const bool in = k < n && S.side[mem[k]];
+                na += __popc(__ballot_sync(0xffffffffu, in));
+            }
+            for (int k = lane; k < n; k += 32) { const int v = mem[k]; S.lo[v] = S.side[v] ? g : g + na; }
+            __syncwarp();
+        }
+        __syncthreads();
+    }
+    int* order = b.order + I.order_off;
+    for (int v = t; v < V; v += blockDim.x) order[S.lo[v] - 1] = v;
+}
+
+// global_min_cut on a vertex subset (ordering.py:30-91): one warp.
+__global__ void __launch_bounds__(32) k_min_cut(pp_batch b, int k, const int* verts, int n, unsigned char* in_a,
+                                                double* weight, int w_in_smem) {
+    const pp_instance I = b.inst[k];
+    const int V = I.V;
+    extern __shared__ double smem_d[];
+    char* sm = (char*)smem_d;
+    double* w;
+    if (w_in_smem) { w = (double*)sm; sm += sizeof(double) * V * V; }
+    else w = b.ws + I.ws_off + ws_layout(I.L, V).rdo_w;
+    const RdoSmem S = rdo_carve(sm, w, V);
+    const double* bw = b.bw + I.bw_off;
+    for (int e = threadIdx.x; e < V * V; e += 32) w[e] = (e / V == e % V) ? 0.0 : bw[e];
+    for (int q = threadIdx.x; q < n; q += 32) S.mem[q] = verts[q];
+    __syncwarp();
+    const double cw = warp_min_cut(S, bw, V, S.mem, n);
+    for (int q = threadIdx.x; q < n; q += 32) in_a[q] = S.side[S.mem[q]];
+    if (threadIdx.x == 0) weight[0] = cw;
+}
+
+}  // namespace pp

@@ -1,0 +1,4 @@
+// Single translation unit for libpipeplan_b200.so.
+#include "prm.cu"
+#include "sim.cu"
+#include "capi.cu"

@@ -1,0 +1,113 @@
+"""CPU-only checks: the C-ABI library loads and exports every declared symbol,
+host-side layout/ordering logic, validators, and the loud no-GPU failure."""
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import block_labels
+
+import paper_2204_10562_b200 as P
+from paper_2204_10562_b200 import _lib
+from paper_2204_10562_b200 import workloads as W
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    text = open(os.path.join(REPO, "include", "pipeplan_b200.h")).read()
+    return sorted(set(re.findall(r"\b(pp_[a-z_0-9]+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(_lib.LIB_PATH):
+        _lib.build()
+    return _lib.load(require_device=False)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    syms = header_symbols()
+    assert len(syms) >= 14
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_lib.EXPORTS)
+    assert b"sm_100a" in lib.pp_version()
+
+
+def test_layout_offsets(lib):
+    L = np.array([3, 96, 1], np.int32)
+    V = np.array([2, 64, 5], np.int32)
+    M = np.array([2, 8, 1], np.int32)
+    f = np.zeros(3, np.int32)
+    inst = (_lib.PPInstance * 3)()
+    tot = [C.c_int64() for _ in range(8)]
+    rc = lib.pp_layout(3, L.ctypes.data, V.ctypes.data, M.ctypes.data, f.ctypes.data, C.cast(inst, C.c_void_p),
+                       *[C.byref(t) for t in tot])
+    assert rc == 0
+    assert [inst[k].layer_off for k in range(3)] == [0, 3, 99]
+    assert [inst[k].bw_off for k in range(3)] == [0, 4, 4 + 64 * 64]
+    assert [inst[k].stage_off for k in range(3)] == [0, 3, 3 + 64 * 65 // 2]
+    assert tot[0].value == 100 and tot[4].value == 3 + 2080 + 15
+    assert inst[1].ws_off > inst[0].ws_off and tot[7].value > inst[2].ws_off
+    bad = np.array([0], np.int32)
+    assert lib.pp_layout(1, bad.ctypes.data, V.ctypes.data, M.ctypes.data, f.ctypes.data,
+                         C.cast(inst, C.c_void_p), *[C.byref(t) for t in tot]) == -1
+    assert b"outside" in lib.pp_last_error()
+
+
+def test_block_list_matches_reference_layout():
+    for N in range(1, 12):
+        plan = P.Plan(stages=tuple(P.Stage(n + 1, n + 1, n + 1, (n + 1,)) for n in range(N)), microbatch_count=1)
+        got = {b.position: (b.resource, b.label) for b in P.build_block_list(plan)}
+        assert got == block_labels(N)
+
+
+def test_execution_order_closed_form_matches_pass_loop():
+    for N in range(1, 9):
+        for M in (1, 2, 3, 7, 16):
+            plan = P.Plan(stages=tuple(P.Stage(n + 1, n + 1, n + 1, (n + 1,)) for n in range(N)),
+                          microbatch_count=M)
+            got = P.compute_execution_order(plan).queues
+            q_off, items = O.pe_queues(N, M)
+            names = [f"stage{r // 2 + 1}" if r % 2 == 0 else f"chan{r // 2 + 1}" for r in range(2 * N - 1)]
+            want = {names[r]: tuple(map(tuple, items[q_off[r]:q_off[r + 1]].tolist())) for r in range(2 * N - 1)}
+            assert got == want
+
+
+def test_validators_and_numeric_guard():
+    with pytest.raises(P.ValidationError, match="no layers"):
+        P.validate_profile(P.ModelProfile("x", 1, (), ()))
+    with pytest.raises(P.ValidationError, match="missing pair"):
+        P.validate_cluster(P.ClusterGraph((1, 2, 3), {(1, 2): 1.0}))
+    with pytest.raises(P.ValidationError, match="asymmetric"):
+        P.make_cluster([1, 2], [(1, 2, 1.0), (2, 1, 2.0)])
+    prof = P.ModelProfile("x", 1, (P.LayerProfile(1, 1e101, 1.0, 0.0),), ())
+    with pytest.raises(P.ValidationError, match="supported range"):
+        P.check_numeric_range(prof, P.make_cluster([1], []))
+
+
+def test_workload_generators_are_deterministic():
+    a, b = W.c4_instance(5), W.c4_instance(5)
+    assert a.fwd == b.fwd and a.links == b.links
+    assert W.c1_vgg19().L == 19 and W.c2_bert24().V == 8
+    c3 = W.c3_gpt96()
+    assert (c3.L, c3.V) == (96, 64)
+    assert len(W.c3_sweep()) == 12
+    c5 = W.c5_instance()
+    assert (c5.L, c5.V, c5.M) == (1024, 256, 512)
+    plan = W.even_split_plan(10, list(range(7)), 3)
+    assert plan == [(1, 4, (0, 1, 2)), (5, 7, (3, 4)), (8, 10, (5, 6))]
+
+
+def test_no_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    prof, clu, M = W.c2_bert24().to_model()
+    with pytest.raises(_lib.BackendUnavailable):
+        P.spp(prof, clu, M)
