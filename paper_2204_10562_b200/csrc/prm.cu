@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(128) k_prep(pp_batch b) {
     for (int hi = row + 1 + t; hi <= V; hi += blockDim.x) {
         double m = PP_INF;
         const double* bwr = bw + (int64_t)order[hi - 1] * V;
-        for (int a = row; a < hi; ++a) m = fmin(m, bwr[order[a - 1]]);
+        for (int a = row; a < hi; ++a) m = dmin(m, bwr[order[a - 1]]);
         s_col[hi - 1] = m;
     }
     __syncthreads();
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(128) k_prep(pp_batch b) {
         double m = PP_INF;
         ws[lay.minpair + (int64_t)(row - 1) * V + (row - 1)] = m;
         for (int hi = row + 1; hi <= V; ++hi) {
-            m = fmin(m, s_col[hi - 1]);
+            m = dmin(m, s_col[hi - 1]);
             ws[lay.minpair + (int64_t)(row - 1) * V + (hi - 1)] = m;
         }
     }
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(128) k_prep(pp_batch b) {
         double m = PP_INF;
         for (int rp = 1; rp <= i - r; ++rp) {
             const double* bwr = bw + (int64_t)order[lo - 1 - rp] * V;   // new left device, rank lo - rp
-            for (int c = lo; c <= i; ++c) m = fmin(m, bwr[order[c - 1]]);
+            for (int c = lo; c <= i; ++c) m = dmin(m, bwr[order[c - 1]]);
             ws[lay.cross + cross_idx(V, i, r, rp)] = m;
         }
     }
@@ -101,12 +101,12 @@ __global__ void __launch_bounds__(128) k_phi(pp_batch b) {
     double mn = PP_INF, mx = -PP_INF;
     for (int e = t; e < V * V; e += blockDim.x) {
         const int a = e / V, c = e % V;
-        if (a < c) { const double x = bw[e]; mn = fmin(mn, x); mx = fmax(mx, x); }
+        if (a < c) { const double x = bw[e]; mn = dmin(mn, x); mx = dmax(mx, x); }
     }
     s_red[0][t] = mn; s_red[1][t] = mx;
     __syncthreads();
     if (t != 0) return;
-    for (int k = 1; k < blockDim.x; ++k) { mn = fmin(mn, s_red[0][k]); mx = fmax(mx, s_red[1][k]); }
+    for (int k = 1; k < blockDim.x; ++k) { mn = dmin(mn, s_red[0][k]); mx = dmax(mx, s_red[1][k]); }
     double pmax = 0.0, dmax = 0.0;
     PySum g(I.flags & PP_SUM_NAIVE);
     for (int l = 0; l < L; ++l) {
@@ -172,10 +172,10 @@ __global__ void __launch_bounds__(128) k_expand(pp_batch b, int j, int tiles_r) 
         for (int k = 0; k < 32; ++k) {
             double a0 = As[k][cx * 4 + 0], a1 = As[k][cx * 4 + 1], a2 = As[k][cx * 4 + 2], a3 = As[k][cx * 4 + 3];
             double b0 = Bs[k][cr * 2 + 0], b1 = Bs[k][cr * 2 + 1];
-            acc[0][0] = fmin(acc[0][0], fmax(a0, b0)); acc[0][1] = fmin(acc[0][1], fmax(a0, b1));
-            acc[1][0] = fmin(acc[1][0], fmax(a1, b0)); acc[1][1] = fmin(acc[1][1], fmax(a1, b1));
-            acc[2][0] = fmin(acc[2][0], fmax(a2, b0)); acc[2][1] = fmin(acc[2][1], fmax(a2, b1));
-            acc[3][0] = fmin(acc[3][0], fmax(a3, b0)); acc[3][1] = fmin(acc[3][1], fmax(a3, b1));
+            acc[0][0] = dmin(acc[0][0], dmax(a0, b0)); acc[0][1] = dmin(acc[0][1], dmax(a0, b1));
+            acc[1][0] = dmin(acc[1][0], dmax(a1, b0)); acc[1][1] = dmin(acc[1][1], dmax(a1, b1));
+            acc[2][0] = dmin(acc[2][0], dmax(a2, b0)); acc[2][1] = dmin(acc[2][1], dmax(a2, b1));
+            acc[3][0] = dmin(acc[3][0], dmax(a3, b0)); acc[3][1] = dmin(acc[3][1], dmax(a3, b1));
         }
         __syncthreads();
     }
@@ -225,8 +225,9 @@ __global__ void __launch_bounds__(128) k_combine(pp_batch b, int i, int tiles_x)
     double* Wi = ws + lay.W + W_base(L, i);
     const int t = threadIdx.x;
 
-    if (r == i || (!allow && r != 1)) {
-        // partition.py:103-104 (no replication) and :115-121 (base / INF rules)
+    if (r == i || (!allow && r != 1) || x0 > i - r + 1) {
+        // partition.py:103-104 (no replication) and :115-121 (base / INF rules);
+        // tiles whose every xi exceeds i-r+1 are infeasible (earlier stages need xi-1 devices)
         for (int e = t; e < 32 * 32; e += 128) {
             const int l = l0 + (e >> 5), xi = x0 + (e & 31);
             if (l > L || xi > i) continue;
@@ -266,10 +267,10 @@ __global__ void __launch_bounds__(128) k_combine(pp_batch b, int i, int tiles_x)
         for (int k = 0; k < 32; ++k) {
             double x0v = Xs[k][cx * 2 + 0], x1v = Xs[k][cx * 2 + 1];
             double s0 = Ss[k][cl * 4 + 0], s1 = Ss[k][cl * 4 + 1], s2 = Ss[k][cl * 4 + 2], s3 = Ss[k][cl * 4 + 3];
-            acc[0][0] = fmin(acc[0][0], fmax(x0v, s0)); acc[0][1] = fmin(acc[0][1], fmax(x1v, s0));
-            acc[1][0] = fmin(acc[1][0], fmax(x0v, s1)); acc[1][1] = fmin(acc[1][1], fmax(x1v, s1));
-            acc[2][0] = fmin(acc[2][0], fmax(x0v, s2)); acc[2][1] = fmin(acc[2][1], fmax(x1v, s2));
-            acc[3][0] = fmin(acc[3][0], fmax(x0v, s3)); acc[3][1] = fmin(acc[3][1], fmax(x1v, s3));
+            acc[0][0] = dmin(acc[0][0], dmax(x0v, s0)); acc[0][1] = dmin(acc[0][1], dmax(x1v, s0));
+            acc[1][0] = dmin(acc[1][0], dmax(x0v, s1)); acc[1][1] = dmin(acc[1][1], dmax(x1v, s1));
+            acc[2][0] = dmin(acc[2][0], dmax(x0v, s2)); acc[2][1] = dmin(acc[2][1], dmax(x1v, s2));
+            acc[3][0] = dmin(acc[3][0], dmax(x0v, s3)); acc[3][1] = dmin(acc[3][1], dmax(x1v, s3));
         }
         __syncthreads();
     }
@@ -288,10 +289,18 @@ __global__ void __launch_bounds__(128) k_combine(pp_batch b, int i, int tiles_x)
 
 // ----------------------------------------------------------------------------
 // Backtrack: re-derive the reference's first-found realizing (l', r') of a
-// cell (partition.py:126-141 loop order, strict `best > w`) by scanning the
-// candidates in lexicographic order for the first whose value equals W.
-// Warp-cooperative; writes stage n (1-based) via the callback arrays.
+// cell (partition.py:126-141 loop order, strict `best > w`).  The candidate
+// values are w(l', r') = max(W_j(l', xi-1, r'), chan(l', r'), stage(l')) and
+// min over r' of w(l', .) = max(X(l', xi), stage(l')) exactly, so the
+// lexicographically first (l', r') achieving the cell value is: the first
+// l' with max(X(l'), stage(l')) == W (X is the stored expansion the DP
+// used), then the first r' with w(l', r') == W.  Warp-cooperative.
 // ----------------------------------------------------------------------------
+__device__ __forceinline__ int warp_first(bool match) {
+    const unsigned mask = __ballot_sync(0xffffffffu, match);
+    return mask ? __ffs(mask) - 1 : -1;
+}
+
 __device__ void dp_walk(const pp_batch& b, const pp_instance& I, int l, int x, int r, int i, double w,
                         int* o_ls, int* o_le, int* o_dlo, int* o_dhi) {
     const int L = I.L, V = I.V, M = I.M;
@@ -305,29 +314,37 @@ __device__ void dp_walk(const pp_batch& b, const pp_instance& I, int l, int x, i
     const int lane = threadIdx.x & 31;
     while (x >= 2) {
         const int j = i - r;
-        const int nl = l - (x - 1);
-        const int total = nl * j;
-        int found = -1;
-        for (int base = 0; base < total && found < 0; base += 32) {
-            const int k = base + lane;
+        const double* X = ws + lay.X + X_base(L, i, r);
+        int lp = -1;
+        for (int base = x - 1; base <= l - 1 && lp < 0; base += 32) {
+            const int c = base + lane;
             bool match = false;
-            if (k < total) {
-                const int lp = x - 1 + k / j, rp = 1 + k % j;
-                const double sub = W[W_idx(L, j, lp, rp, x - 1)];
-                const double Mp = (double)M * (b.efwd[I.layer_off + lp - 1] + b.ebwd[I.layer_off + lp - 1]);
-                const double chan = Mp / ((double)(rp * r) * cross[cross_idx(V, i, r, rp)]);
-                const double st = stage_term(M, L, V, prefix, psum, minpair, lp, l, r, i);
-                const double v = fmax(fmax(sub, chan), st);
-                match = (v == w);
-            }
-            const unsigned mask = __ballot_sync(0xffffffffu, match);
-            if (mask) found = base + __ffs(mask) - 1;
+            if (c <= l - 1)
+                match = dmax(X[(int64_t)(c - 1) * j + (x - 2)],
+                             stage_term(M, L, V, prefix, psum, minpair, c, l, r, i)) == w;
+            const int f = warp_first(match);
+            if (f >= 0) lp = base + f;
         }
-        if (found < 0) {   // cannot happen for a consistent table; leave a detectable hole
+        int rp = -1;
+        if (lp > 0) {
+            const double st = stage_term(M, L, V, prefix, psum, minpair, lp, l, r, i);
+            const double Mp = (double)M * (b.efwd[I.layer_off + lp - 1] + b.ebwd[I.layer_off + lp - 1]);
+            for (int base = 1; base <= j && rp < 0; base += 32) {
+                const int c = base + lane;
+                bool match = false;
+                if (c <= j) {
+                    const double sub = W[W_idx(L, j, lp, c, x - 1)];
+                    const double chan = Mp / ((double)(c * r) * cross[cross_idx(V, i, r, c)]);
+                    match = dmax(dmax(sub, chan), st) == w;
+                }
+                const int f = warp_first(match);
+                if (f >= 0) rp = base + f;
+            }
+        }
+        if (rp < 0) {   // cannot happen for a consistent table; leave a detectable hole
             if (lane == 0) { o_ls[x - 1] = 0; o_le[x - 1] = 0; o_dlo[x - 1] = 0; o_dhi[x - 1] = 0; }
             return;
         }
-        const int lp = x - 1 + found / j, rp = 1 + found % j;
         if (lane == 0) { o_ls[x - 1] = lp + 1; o_le[x - 1] = l; o_dlo[x - 1] = i - r + 1; o_dhi[x - 1] = i; }
         w = W[W_idx(L, j, lp, rp, x - 1)];
         l = lp; i = j; r = rp; --x;
@@ -397,123 +414,109 @@ __global__ void __launch_bounds__(32) k_query(pp_batch b, int n, const int* qi, 
 // groups of one recursion level are cut concurrently by different warps.
 // A group is identified by its lowest rank `lo`; every vertex stores the lo
 // of its current group, so the final rank of vertex v is lo[v].
-// Per-vertex state is indexed by the global vertex index (groups are
-// disjoint, so warps never touch the same entries).
+//
+// Inside a cut, vertex k of the group (k = position in the ascending member
+// list, so local order == GPU-id order) lives on lane k % 32, register slot
+// k / 32: adjacency, supernode and flags never touch memory.  The group's
+// weights are a local n x n matrix (shared memory when the instance fits,
+// else the instance's global scratch), rebuilt from the cluster for every
+// cut as the reference does (ordering.py:50-54).  Arg-max per step: the
+// adjacencies are positive doubles, which order like their uint64 bit
+// patterns, so the max is two 32-bit __reduce_max_sync (high word, then low
+// word among high-word winners) and the reference's smallest-id tie rule
+// (ordering.py:66) is a __reduce_min_sync over the tied local indices.
 // ----------------------------------------------------------------------------
-
-struct RdoSmem {
-    double* w;       // V*V contracted weights (smem or global scratch)
-    double* adj;     // [V]
-    int* lo;         // [V]
-    int* grp;        // [V] supernode of each vertex
-    int* cnt;        // [V] group sizes by lo-1
-    int* first;      // [V] smallest member by lo-1
-    int* glist;      // [V] groups to cut this level
-    int* mem;        // [RDO_WARPS][V] member lists
-    unsigned char* alive;
-    unsigned char* inadj;
-    unsigned char* side;
-};
-
-// Cut the group whose members are mem[0..n) (ascending); returns weight and
-// leaves side flags (1 = side_a, the side holding mem[0]) in S.side.
-__device__ double warp_min_cut(const RdoSmem& S, const double* bw, int V, const int* mem, int n) {
+template <int SLOTS>
+__device__ double warp_min_cut_t(double* wl, const double* bw, int V, const int* mem, int n,
+                                 unsigned char* side_out) {
+    const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    double* w = S.w;
-    // every cut starts from the cluster's own weights (ordering.py:50-54)
     for (int e = lane; e < n * n; e += 32) {
-        const int a = mem[e / n], c = mem[e % n];
-        w[(int64_t)a * V + c] = (a == c) ? 0.0 : bw[(int64_t)a * V + c];
+        const int a = e / n, c = e - a * n;
+        wl[e] = (a == c) ? 0.0 : bw[(int64_t)mem[a] * V + mem[c]];
     }
-    for (int k = lane; k < n; k += 32) { const int v = mem[k]; S.alive[v] = 1; S.grp[v] = v; S.side[v] = 0; }
     __syncwarp();
+    double adj[SLOTS];
+    int grp[SLOTS];
+    bool alive[SLOTS], inadj[SLOTS], side[SLOTS];
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+        const int k = lane + 32 * s;
+        alive[s] = k < n; grp[s] = k; side[s] = false; inadj[s] = false; adj[s] = 0.0;
+    }
     double best_weight = PP_INF;
-    int n_alive = n;
-    const int start = mem[0];   // the smallest id never merges away (merged = min(s, t))
-    while (n_alive > 1) {
-        for (int k = lane; k < n; k += 32) {
-            const int v = mem[k];
-            const unsigned char in = S.alive[v] && v != start;
-            S.inadj[v] = in;
-            if (in) S.adj[v] = w[(int64_t)start * V + v];
+    for (int n_alive = n; n_alive > 1; --n_alive) {
+#pragma unroll
+        for (int s = 0; s < SLOTS; ++s) {   // phase starts at the smallest id (ordering.py:61-64)
+            const int k = lane + 32 * s;
+            inadj[s] = alive[s] && k != 0;
+            if (inadj[s]) adj[s] = wl[k];
         }
-        __syncwarp();
-        int s = start, t = start;
+        int sv = 0, tv = 0;
         double cut = 0.0;
         for (int step = 0; step < n_alive - 1; ++step) {
-            double bv = -PP_INF;
-            int bi = 0x7fffffff;
-            for (int k = lane; k < n; k += 32) {
-                const int v = mem[k];
-                if (S.inadj[v]) {
-                    const double a = S.adj[v];
-                    if (a > bv || (a == bv && v < bi)) { bv = a; bi = v; }
-                }
-            }
+            unsigned long long bu = 0ull;
+            int bk = 0x7fffffff;
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-                if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+            for (int s = 0; s < SLOTS; ++s) {
+                const unsigned long long u = (unsigned long long)__double_as_longlong(adj[s]);
+                if (inadj[s] && u > bu) { bu = u; bk = lane + 32 * s; }
             }
-            const int nv = bi;
-            cut = bv;
-            s = t; t = nv;
-            __syncwarp();
-            if (lane == 0) S.inadj[nv] = 0;
-            __syncwarp();
-            const double* row = w + (int64_t)nv * V;
-            for (int k = lane; k < n; k += 32) {   // adj[u] += wt(next_v, u)  (ordering.py:69-70)
-                const int v = mem[k];
-                if (S.inadj[v]) S.adj[v] = S.adj[v] + row[v];
+            const unsigned hi = (unsigned)(bu >> 32), lo = (unsigned)bu;
+            const unsigned mhi = __reduce_max_sync(FULL, hi);
+            const unsigned mlo = __reduce_max_sync(FULL, hi == mhi ? lo : 0u);
+            const bool win = bk != 0x7fffffff && hi == mhi && lo == mlo;
+            const int nk = (int)__reduce_min_sync(FULL, win ? (unsigned)bk : 0x7fffffffu);
+            cut = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+            sv = tv; tv = nk;
+            const double* row = wl + nk * n;
+#pragma unroll
+            for (int s = 0; s < SLOTS; ++s) {   // adj[u] += wt(next_v, u)  (ordering.py:69-70)
+                const int k = lane + 32 * s;
+                if (k == nk) inadj[s] = false;
+                if (inadj[s]) adj[s] = adj[s] + row[k];
             }
-            __syncwarp();
         }
-        if (cut < best_weight) {   // ordering.py:73-75
+        if (cut < best_weight) {   // first minimum cut-of-phase (ordering.py:73-75)
             best_weight = cut;
-            for (int k = lane; k < n; k += 32) { const int v = mem[k]; S.side[v] = (S.grp[v] == t); }
+#pragma unroll
+            for (int s = 0; s < SLOTS; ++s) side[s] = (grp[s] == tv);
         }
-        const int merged = min(s, t), other = max(s, t);   // ordering.py:77-85
-        for (int k = lane; k < n; k += 32) {
-            const int u = mem[k];
-            if (S.alive[u] && u != s && u != t) {
-                const double x = w[(int64_t)s * V + u] + w[(int64_t)t * V + u];
-                w[(int64_t)merged * V + u] = x;
-                w[(int64_t)u * V + merged] = x;
+        const int merged = min(sv, tv), other = max(sv, tv);   // ordering.py:77-85
+#pragma unroll
+        for (int s = 0; s < SLOTS; ++s) {
+            const int u = lane + 32 * s;
+            if (alive[s] && u != sv && u != tv) {
+                const double x = wl[sv * n + u] + wl[tv * n + u];
+                wl[merged * n + u] = x;
+                wl[u * n + merged] = x;
             }
         }
         __syncwarp();
-        for (int k = lane; k < n; k += 32) { const int v = mem[k]; if (S.grp[v] == other) S.grp[v] = merged; }
-        __syncwarp();
-        if (lane == 0) S.alive[other] = 0;
-        __syncwarp();
-        --n_alive;
+#pragma unroll
+        for (int s = 0; s < SLOTS; ++s) {
+            if (grp[s] == other) grp[s] = merged;
+            if (lane + 32 * s == other) alive[s] = false;
+        }
     }
-    // side holding the smallest id becomes side_a (ordering.py:87-91)
-    const unsigned char low = S.side[mem[0]];
-    __syncwarp();
-    for (int k = lane; k < n; k += 32) { const int v = mem[k]; S.side[v] = low ? S.side[v] : !S.side[v]; }
+    // the side holding the smallest id becomes side_a (ordering.py:87-91)
+    const bool low = __shfl_sync(FULL, side[0], 0);
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+        const int k = lane + 32 * s;
+        if (k < n) side_out[k] = low ? side[s] : !side[s];
+    }
     __syncwarp();
     return best_weight;
 }
 
-__device__ RdoSmem rdo_carve(char* base, double* w, int V) {
-    RdoSmem S;
-    char* p = base;
-    S.w = w;
-    S.adj = (double*)p; p += sizeof(double) * V;
-    S.lo = (int*)p; p += sizeof(int) * V;
-    S.grp = (int*)p; p += sizeof(int) * V;
-    S.cnt = (int*)p; p += sizeof(int) * V;
-    S.first = (int*)p; p += sizeof(int) * V;
-    S.glist = (int*)p; p += sizeof(int) * V;
-    S.mem = (int*)p; p += sizeof(int) * V * RDO_WARPS;
-    S.alive = (unsigned char*)p; p += V;
-    S.inadj = (unsigned char*)p; p += V;
-    S.side = (unsigned char*)p; p += V;
-    return S;
+__device__ double warp_min_cut(double* wl, const double* bw, int V, const int* mem, int n, unsigned char* side) {
+    if (n <= 32) return warp_min_cut_t<1>(wl, bw, V, mem, n, side);
+    if (n <= 64) return warp_min_cut_t<2>(wl, bw, V, mem, n, side);
+    if (n <= 128) return warp_min_cut_t<4>(wl, bw, V, mem, n, side);
+    if (n <= 256) return warp_min_cut_t<8>(wl, bw, V, mem, n, side);
+    return warp_min_cut_t<16>(wl, bw, V, mem, n, side);
 }
-
 
 __global__ void __launch_bounds__(32 * RDO_WARPS) k_rdo(pp_batch b, int w_in_smem) {
     const pp_instance I = b.inst[blockIdx.x];
@@ -521,55 +524,65 @@ __global__ void __launch_bounds__(32 * RDO_WARPS) k_rdo(pp_batch b, int w_in_sme
     const int V = I.V;
     extern __shared__ double smem_d[];
     char* sm = (char*)smem_d;
-    double* w;
-    if (w_in_smem) { w = (double*)sm; sm += sizeof(double) * V * V; }
-    else w = b.ws + I.ws_off + ws_layout(I.L, V).rdo_w;
-    const RdoSmem S = rdo_carve(sm, w, V);
+    double* W;
+    if (w_in_smem) { W = (double*)sm; sm += sizeof(double) * V * V; }
+    else W = b.ws + I.ws_off + ws_layout(I.L, V).rdo_w;
+    int* lo = (int*)sm;      sm += sizeof(int) * V;
+    int* cnt = (int*)sm;     sm += sizeof(int) * V;
+    int* first = (int*)sm;   sm += sizeof(int) * V;
+    int* glist = (int*)sm;   sm += sizeof(int) * V;
+    int* goff = (int*)sm;    sm += sizeof(int) * V;
+    int* memall = (int*)sm;  sm += sizeof(int) * V * RDO_WARPS;
+    unsigned char* sideall = (unsigned char*)sm;
     const double* bw = b.bw + I.bw_off;
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-    for (int e = t; e < V * V; e += blockDim.x) w[e] = (e / V == e % V) ? 0.0 : bw[e];
-    for (int v = t; v < V; v += blockDim.x) S.lo[v] = 1;
+    for (int v = t; v < V; v += blockDim.x) lo[v] = 1;
     __syncthreads();
     __shared__ int s_ngroups;
     for (;;) {
-        for (int v = t; v < V; v += blockDim.x) { S.cnt[v] = 0; S.first[v] = 0x7fffffff; }
+        for (int v = t; v < V; v += blockDim.x) { cnt[v] = 0; first[v] = 0x7fffffff; }
         if (t == 0) s_ngroups = 0;
         __syncthreads();
-        for (int v = t; v < V; v += blockDim.x) { atomicAdd(&S.cnt[S.lo[v] - 1], 1); atomicMin(&S.first[S.lo[v] - 1], v); }
+        for (int v = t; v < V; v += blockDim.x) { atomicAdd(&cnt[lo[v] - 1], 1); atomicMin(&first[lo[v] - 1], v); }
         __syncthreads();
         for (int v = t; v < V; v += blockDim.x) {
-            const int g = S.lo[v];
-            if (S.cnt[g - 1] >= 2 && S.first[g - 1] == v) S.glist[atomicAdd(&s_ngroups, 1)] = g;
+            const int g = lo[v];
+            if (cnt[g - 1] >= 2 && first[g - 1] == v) glist[atomicAdd(&s_ngroups, 1)] = g;
         }
         __syncthreads();
         const int ng = s_ngroups;
         if (ng == 0) break;
+        if (t == 0) {   // disjoint groups: sum of n^2 <= V^2 fits the V x V region
+            int o = 0;
+            for (int gi = 0; gi < ng; ++gi) { goff[gi] = o; const int c = cnt[glist[gi] - 1]; o += c * c; }
+        }
+        __syncthreads();
         for (int gi = warp; gi < ng; gi += RDO_WARPS) {
-            const int g = S.glist[gi];
-            int* mem = S.mem + warp * V;
+            const int g = glist[gi];
+            int* mem = memall + warp * V;
+            unsigned char* side = sideall + warp * V;
             int n = 0;
             for (int v0 = 0; v0 < V; v0 += 32) {   // ascending member list
                 const int v = v0 + lane;
-                const bool in = v < V && S.lo[v] == g;
+                const bool in = v < V && lo[v] == g;
                 const unsigned m = __ballot_sync(0xffffffffu, in);
                 if (in) mem[n + __popc(m & ((1u << lane) - 1))] = v;
                 n += __popc(m);
             }
             __syncwarp();
-            warp_min_cut(S, bw, V, mem, n);
+            warp_min_cut(W + goff[gi], bw, V, mem, n, side);
             int na = 0;
             for (int k0 = 0; k0 < n; k0 += 32) {
                 const int k = k0 + lane;
-                const bool in = k < n && S.side[mem[k]];
-                na += __popc(__ballot_sync(0xffffffffu, in));
+                na += __popc(__ballot_sync(0xffffffffu, k < n && side[k]));
             }
-            for (int k = lane; k < n; k += 32) { const int v = mem[k]; S.lo[v] = S.side[v] ? g : g + na; }
+            for (int k = lane; k < n; k += 32) lo[mem[k]] = side[k] ? g : g + na;
             __syncwarp();
         }
         __syncthreads();
     }
     int* order = b.order + I.order_off;
-    for (int v = t; v < V; v += blockDim.x) order[S.lo[v] - 1] = v;
+    for (int v = t; v < V; v += blockDim.x) order[lo[v] - 1] = v;
 }
 
 // global_min_cut on a vertex subset (ordering.py:30-91): one warp.
@@ -579,16 +592,13 @@ __global__ void __launch_bounds__(32) k_min_cut(pp_batch b, int k, const int* ve
     const int V = I.V;
     extern __shared__ double smem_d[];
     char* sm = (char*)smem_d;
-    double* w;
-    if (w_in_smem) { w = (double*)sm; sm += sizeof(double) * V * V; }
-    else w = b.ws + I.ws_off + ws_layout(I.L, V).rdo_w;
-    const RdoSmem S = rdo_carve(sm, w, V);
-    const double* bw = b.bw + I.bw_off;
-    for (int e = threadIdx.x; e < V * V; e += 32) w[e] = (e / V == e % V) ? 0.0 : bw[e];
-    for (int q = threadIdx.x; q < n; q += 32) S.mem[q] = verts[q];
+    double* W;
+    if (w_in_smem) { W = (double*)sm; sm += sizeof(double) * V * V; }
+    else W = b.ws + I.ws_off + ws_layout(I.L, V).rdo_w;
+    int* mem = (int*)sm;
+    for (int q = threadIdx.x; q < n; q += 32) mem[q] = verts[q];
     __syncwarp();
-    const double cw = warp_min_cut(S, bw, V, S.mem, n);
-    for (int q = threadIdx.x; q < n; q += 32) in_a[q] = S.side[S.mem[q]];
+    const double cw = warp_min_cut(W, b.bw + I.bw_off, V, mem, n, in_a);
     if (threadIdx.x == 0) weight[0] = cw;
 }
 

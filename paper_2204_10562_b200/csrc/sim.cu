@@ -74,7 +74,7 @@ __device__ LaneCost lane_cost(const P& p, const InstView& I, int N, int lane) {
             const double total = pysum(I.par + a - 1, e - a + 1, I.naive);
             double mp = PP_INF;
             for (int x = 0; x < k; ++x)
-                for (int y = x + 1; y < k; ++y) mp = fmin(mp, I.w(p.dev(n, x), p.dev(n, y)));
+                for (int y = x + 1; y < k; ++y) mp = dmin(mp, I.w(p.dev(n, x), p.dev(n, y)));
             c.ar = 2.0 * (double)(k - 1) * total / ((double)k * mp);              // cost.py:99
             c.has_ar = true;
         }
@@ -82,7 +82,7 @@ __device__ LaneCost lane_cost(const P& p, const InstView& I, int N, int lane) {
         const int kl = p.k(n), kr = p.k(n + 1);
         double mc = PP_INF;
         for (int x = 0; x < kl; ++x)
-            for (int y = 0; y < kr; ++y) mc = fmin(mc, I.w(p.dev(n, x), p.dev(n + 1, y)));   // cost.py:74-80
+            for (int y = 0; y < kr; ++y) mc = dmin(mc, I.w(p.dev(n, x), p.dev(n + 1, y)));   // cost.py:74-80
         const double denom = (double)(kl * kr) * mc;                              // cost.py:121-122
         const int edge = p.stage_le(n);
         c.dA = I.efwd[edge - 1] / denom;
@@ -99,15 +99,15 @@ __device__ void reduce_costs(const LaneCost& c, int lane, int R, int nthr, doubl
     double ar = (lane < R && c.has_ar) ? c.ar : -PP_INF;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
-        cy = fmax(cy, __shfl_xor_sync(0xffffffffu, cy, off));
-        ar = fmax(ar, __shfl_xor_sync(0xffffffffu, ar, off));
+        cy = dmax(cy, __shfl_xor_sync(0xffffffffu, cy, off));
+        ar = dmax(ar, __shfl_xor_sync(0xffffffffu, ar, off));
     }
     const int warp = lane >> 5;
     if ((lane & 31) == 0) { red[2 * warp] = cy; red[2 * warp + 1] = ar; }
     bar_sync(nthr);
     if (lane == 0) {
         double a = -PP_INF, b = -PP_INF;
-        for (int w = 0; w < nthr / 32; ++w) { a = fmax(a, red[2 * w]); b = fmax(b, red[2 * w + 1]); }
+        for (int w = 0; w < nthr / 32; ++w) { a = dmax(a, red[2 * w]); b = dmax(b, red[2 * w + 1]); }
         *cyc_out = a;
         *ar_out = (b == -PP_INF) ? 0.0 : b;   // max(..., default=0.0)  scheduler.py:237
     }
@@ -151,7 +151,7 @@ __device__ void pe_simulate(const P& p, const InstView& I, int N, int M, int nth
                 double pred;
                 if (first_from_left) pred = has_left ? fe[prv * R + lane - 1] : 0.0;
                 else pred = has_right ? be[prv * R + lane + 1] : 0.0;
-                const double st = fmax(rfree, pred);
+                const double st = dmax(rfree, pred);
                 const double en = st + c.dB;   // B / FB / Y
                 rfree = en;
                 be[cur * R + lane] = en;
@@ -161,7 +161,7 @@ __device__ void pe_simulate(const P& p, const InstView& I, int N, int M, int nth
                 m = pass - p_second + 1;
                 if (m >= 1 && m <= M) {
                     const double pred = has_left ? fe[prv * R + lane - 1] : 0.0;
-                    const double st = fmax(rfree, pred);
+                    const double st = dmax(rfree, pred);
                     const double en = st + c.dA;   // F / X
                     rfree = en;
                     fe[cur * R + lane] = en;
@@ -179,13 +179,13 @@ __device__ void pe_simulate(const P& p, const InstView& I, int N, int M, int nth
     }
     // makespan = max(last B_1 / FB_1 end, AllReduce ends)   (scheduler.py:216-220)
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) arend = fmax(arend, __shfl_xor_sync(0xffffffffu, arend, off));
+    for (int off = 16; off > 0; off >>= 1) arend = dmax(arend, __shfl_xor_sync(0xffffffffu, arend, off));
     if ((lane & 31) == 0) red[lane >> 5] = arend;
     if (lane == 0) red[40] = rfree;   // stage1 lane: end of B_1(M) (or FB_1(M))
     bar_sync(nthr);
     if (lane == 0) {
         double mk = red[40];
-        for (int w = 0; w < nthr / 32; ++w) mk = fmax(mk, red[w]);
+        for (int w = 0; w < nthr / 32; ++w) mk = dmax(mk, red[w]);
         *o_mk = mk;
     }
 }
@@ -310,8 +310,8 @@ __global__ void __launch_bounds__(1024) k_sim_plans(pp_batch b, pp_sim_batch s) 
                 pred = comp[(int64_t)(m - 1) * J + pos - 2];
                 if (pred < 0.0) break;
             }
-            double st = fmax(rfree, pred);
-            if (fb && !fwd_side) st = fmax(st, T);
+            double st = dmax(rfree, pred);
+            if (fb && !fwd_side) st = dmax(st, T);
             const double en = st + (fwd_side ? c.dA : c.dB);
             rfree = en;
             const int64_t x = (int64_t)(m - 1) * J + pos - 1;
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(1024) k_sim_plans(pp_batch b, pp_sim_batch s) 
             __threadfence_block();
             comp[x] = en;
             ++head; ++prog;
-            if (fb && fwd_side) { ++my_fwd; my_fmax = fmax(my_fmax, en); }
+            if (fb && fwd_side) { ++my_fwd; my_fmax = dmax(my_fmax, en); }
         }
         // round barrier: progress and forward-completion reductions
         if (lane == 0) s_prog = 0;
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(1024) k_sim_plans(pp_batch b, pp_sim_batch s) 
         if (prog) atomicAdd((unsigned long long*)&s_prog, (unsigned long long)prog);
         double fm = my_fmax;
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) fm = fmax(fm, __shfl_xor_sync(0xffffffffu, fm, off));
+        for (int off = 16; off > 0; off >>= 1) fm = dmax(fm, __shfl_xor_sync(0xffffffffu, fm, off));
         if ((lane & 31) == 0) s_fmax[lane >> 5] = fm;
         if (my_fwd) { atomicAdd((unsigned long long*)&s_fwd, (unsigned long long)my_fwd); my_fwd = 0; }
         bar_sync(nthr);
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(1024) k_sim_plans(pp_batch b, pp_sim_batch s) 
         if (newly) {
             if (lane == 0) {
                 double T2 = -PP_INF;
-                for (int w = 0; w < nthr / 32; ++w) T2 = fmax(T2, s_fmax[w]);
+                for (int w = 0; w < nthr / 32; ++w) T2 = dmax(T2, s_fmax[w]);
                 s_T = T2;   // barrier opens when the last forward-side item ends (scheduler.py:190-194)
                 s_open = 1;
             }
@@ -366,15 +366,15 @@ __global__ void __launch_bounds__(1024) k_sim_plans(pp_batch b, pp_sim_batch s) 
     // finish = max over m of end(m, J)
     double fin = -PP_INF;
     if (ok)
-        for (int m = 1 + lane; m <= M; m += nthr) fin = fmax(fin, comp[(int64_t)(m - 1) * J + J - 1]);
-    double v = fmax(fin, arend);
+        for (int m = 1 + lane; m <= M; m += nthr) fin = dmax(fin, comp[(int64_t)(m - 1) * J + J - 1]);
+    double v = dmax(fin, arend);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
+    for (int off = 16; off > 0; off >>= 1) v = dmax(v, __shfl_xor_sync(0xffffffffu, v, off));
     if ((lane & 31) == 0) red[lane >> 5] = v;
     bar_sync(nthr);
     if (lane == 0) {
         double mk = -PP_INF;
-        for (int w = 0; w < nthr / 32; ++w) mk = fmax(mk, red[w]);
+        for (int w = 0; w < nthr / 32; ++w) mk = dmax(mk, red[w]);
         s.makespan[blockIdx.x] = ok ? mk : 0.0;
         s.status[blockIdx.x] = ok ? 0 : 1;
         s.n_done[blockIdx.x] = (int64_t)s_done;
@@ -396,8 +396,8 @@ __global__ void __launch_bounds__(256) k_peak_minmax(double* out, int iters, dou
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
         for (int k = 0; k < 8; k += 2) {
-            const double a = fmin(fmax(x[k], y), x[k + 1]);
-            const double c = fmax(fmin(x[k + 1], z), x[k]);
+            const double a = dmin(dmax(x[k], y), x[k + 1]);
+            const double c = dmax(dmin(x[k + 1], z), x[k]);
             x[k] = a;
             x[k + 1] = c;
         }
