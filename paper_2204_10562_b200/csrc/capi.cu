@@ -9,8 +9,8 @@
 namespace pp {
 __global__ void k_prep(pp_batch b);
 __global__ void k_phi(pp_batch b);
-__global__ void k_expand(pp_batch b, int j, int tiles_r);
-__global__ void k_combine(pp_batch b, int i, int tiles_x);
+__global__ void k_expand(pp_batch b, int j, int planes_r);
+__global__ void k_combine(pp_batch b, int i, int planes_x);
 __global__ void k_backtrack(pp_batch b);
 __global__ void k_query(pp_batch b, int n, const int* qi, const int* ql, const int* qx, const int* qr,
                         const int* qd, int max_xi, double* w, int* frag, int* feas);
@@ -101,16 +101,17 @@ int pp_prm(const pp_batch* b, void* stream) {
     dim3 gp(b->n_inst, maxL > maxV ? maxL : maxV);
     k_prep<<<gp, 128, 0, S(stream)>>>(*b);
     PP_CHECK_LAUNCH("k_prep");
-    const int tiles_l = ceil_div(maxL, 32);
+    const int planes_l = ceil_div(maxL, 128);   // k_combine plane: 128 l x 64 xi
+    cudaFuncSetAttribute(k_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CB_SMEM);
     for (int i = 1; i <= maxV; ++i) {
-        const int tiles_x = ceil_div(i, 32);
-        dim3 gc(b->n_inst, i, tiles_l * tiles_x);
-        k_combine<<<gc, 128, 0, S(stream)>>>(*b, i, tiles_x);
+        const int planes_x = ceil_div(i, 64);
+        dim3 gc(b->n_inst, i, planes_l * planes_x);
+        k_combine<<<gc, 256, CB_SMEM, S(stream)>>>(*b, i, planes_x);
         PP_CHECK_LAUNCH("k_combine");
-        if (i < maxV && maxL > 1) {
-            const int tiles_xi = ceil_div(i, 32), tiles_r = ceil_div(maxV - i, 32);
-            dim3 ge(b->n_inst, maxL - 1, tiles_xi * tiles_r);
-            k_expand<<<ge, 128, 0, S(stream)>>>(*b, i, tiles_r);
+        if (i < maxV && maxL > 1) {   // k_expand plane: 64 xi x 64 r per l'
+            const int planes_xi = ceil_div(i, 64), planes_r = ceil_div(maxV - i, 64);
+            dim3 ge(b->n_inst, maxL - 1, planes_xi * planes_r);
+            k_expand<<<ge, 128, 0, S(stream)>>>(*b, i, planes_r);
             PP_CHECK_LAUNCH("k_expand");
         }
     }

@@ -128,67 +128,106 @@ __global__ void __launch_bounds__(128) k_phi(pp_batch b) {
 }
 
 // ----------------------------------------------------------------------------
-// k_expand(j): after slice j is final, X for every target (r, i = j + r).
-// grid (n_inst, maxL-1, tiles_xi * tiles_r); CTA tile = 32 xi x 32 r for one l'.
+// (min, max) micro-kernel shared by expand and combine: a thread owns a 4x4
+// register tile of outputs and folds one K index per step,
+//     acc[a][c] = min(acc[a][c], max(p[a], q[c])),
+// p from a 4-wide slice of the "row" operand and q from the "column" operand,
+// both read from shared memory as two LDS.128 each.  Every output's K range
+// is trimmed to where its candidates can be finite (the triangular l' < l and
+// r' <= j - xi + 2 structure), so padded INF candidates are not evaluated.
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_expand(pp_batch b, int j, int tiles_r) {
+constexpr int KC = 32;   // K chunk staged per __syncthreads
+
+__device__ __forceinline__ void mm_step(double (&acc)[4][4], const double* prow, const double* qrow) {
+    const double2 p01 = *reinterpret_cast<const double2*>(prow);
+    const double2 p23 = *reinterpret_cast<const double2*>(prow + 2);
+    const double2 q01 = *reinterpret_cast<const double2*>(qrow);
+    const double2 q23 = *reinterpret_cast<const double2*>(qrow + 2);
+    const double p[4] = {p01.x, p01.y, p23.x, p23.y};
+    const double q[4] = {q01.x, q01.y, q23.x, q23.y};
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = dmin(acc[a][c], dmax(p[a], q[c]));
+}
+
+// ----------------------------------------------------------------------------
+// k_expand(j): once slice j is final, X(l', xi, r, i = j + r) for every target,
+//   X = min_{r' <= j} max(W_j(l', xi-1, r'), chan(l', r', r, i)),
+//   chan = (M * payload(l')) / ((r' * r) * cross(r', r, i))   (partition.py:130-138)
+// grid (n_inst, maxL-1, planes): one CTA per (instance, l', 64 xi x 64 r plane).
+// ----------------------------------------------------------------------------
+constexpr int EX_T = 128, EX_P = 64, EX_S = EX_P + 4;
+
+__global__ void __launch_bounds__(EX_T) k_expand(pp_batch b, int j, int planes_r) {
     const pp_instance I = b.inst[blockIdx.x];
     const int L = I.L, V = I.V;
     const int lp = blockIdx.y + 1;
     if (j >= V || lp > L - 1) return;
-    const int txi = blockIdx.z / tiles_r, tr = blockIdx.z % tiles_r;
-    const int xi0 = 2 + 32 * txi, r0 = 1 + 32 * tr;
-    if (xi0 > j + 1 || r0 > V - j) return;
+    const int xi0 = 2 + EX_P * (int)(blockIdx.z / planes_r), r0 = 1 + EX_P * (int)(blockIdx.z % planes_r);
+    const int nxi = min(EX_P, j + 2 - xi0), nr = min(EX_P, V - j + 1 - r0);
+    if (nxi <= 0 || nr <= 0) return;
     const WsLayout lay = ws_layout(L, V);
     double* ws = b.ws + I.ws_off;
     const double* Wj = ws + lay.W;
     const double* cross = ws + lay.cross;
     const double Mp = (double)I.M * (b.efwd[I.layer_off + lp - 1] + b.ebwd[I.layer_off + lp - 1]);   // partition.py:131,137
-
-    __shared__ double As[32][33];   // [r'][xi]   W_j(l', xi-1, r')
-    __shared__ double Bs[32][33];   // [r'][r]    chan(l', r', r, j+r)
-    const int t = threadIdx.x, cx = t & 7, cr = t >> 3;
-    double acc[4][2];
+    __shared__ __align__(16) double As[KC][EX_S];   // [r'][xi - xi0]  W_j(l', xi-1, r')
+    __shared__ __align__(16) double Bs[KC][EX_S];   // [r'][r - r0]    chan(l', r', r, j+r)
+    const int t = threadIdx.x;
+    const int ntx = (nxi + 3) >> 2, ntr = (nr + 3) >> 2, ntiles = ntx * ntr;
+    const int wx = ntx * 4, wr = ntr * 4;
+    // up to two 4x4 tiles per thread
+    int tx[2], tr[2], kend[2];
+    double acc[2][4][4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) { acc[a][0] = PP_INF; acc[a][1] = PP_INF; }
-
-    for (int rp0 = 1; rp0 <= j; rp0 += 32) {
+    for (int u = 0; u < 2; ++u) {
+        const int id = t + u * EX_T;
+        tx[u] = (id < ntiles) ? id % ntx : -1;
+        tr[u] = (id < ntiles) ? id / ntx : 0;
+        // candidates need r' <= j - xi + 2; the tile's smallest xi bounds its K range
+        kend[u] = (id < ntiles) ? j - (xi0 + 4 * tx[u]) + 2 : 0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int e = t + 128 * q, rr = e >> 5, cc = e & 31;
-            const int rp = rp0 + rr;
-            const int xip = xi0 + cc - 1;   // W_j's xi index = xi - 1
-            As[rr][cc] = (rp <= j && xip <= j) ? Wj[W_idx(L, j, lp, rp, xip)] : PP_INF;
-            const int r = r0 + cc;
-            double c = PP_INF;
-            if (rp <= j && r <= V - j) {
-                const int i = j + r;
-                c = Mp / ((double)(rp * r) * cross[cross_idx(V, i, r, rp)]);
-            }
-            Bs[rr][cc] = c;
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[u][a][c] = PP_INF;
+    }
+    const int kmax = j - xi0 + 2;   // largest r' any output of the plane needs
+    for (int rp0 = 1; rp0 <= kmax; rp0 += KC) {
+        const int kc = min(KC, kmax - rp0 + 1);
+        for (int e = t; e < kc * wx; e += EX_T) {
+            const int rr = e / wx, cc = e - rr * wx;
+            const int xi = xi0 + cc;
+            As[rr][cc] = (cc < nxi) ? Wj[W_idx(L, j, lp, rp0 + rr, xi - 1)] : PP_INF;
+        }
+        for (int e = t; e < kc * wr; e += EX_T) {
+            const int rr = e / wr, cc = e - rr * wr;
+            const int rp = rp0 + rr, r = r0 + cc;
+            Bs[rr][cc] = (cc < nr) ? Mp / ((double)(rp * r) * cross[cross_idx(V, j + r, r, rp)]) : PP_INF;
         }
         __syncthreads();
-#pragma unroll 8
-        for (int k = 0; k < 32; ++k) {
-            double a0 = As[k][cx * 4 + 0], a1 = As[k][cx * 4 + 1], a2 = As[k][cx * 4 + 2], a3 = As[k][cx * 4 + 3];
-            double b0 = Bs[k][cr * 2 + 0], b1 = Bs[k][cr * 2 + 1];
-            acc[0][0] = dmin(acc[0][0], dmax(a0, b0)); acc[0][1] = dmin(acc[0][1], dmax(a0, b1));
-            acc[1][0] = dmin(acc[1][0], dmax(a1, b0)); acc[1][1] = dmin(acc[1][1], dmax(a1, b1));
-            acc[2][0] = dmin(acc[2][0], dmax(a2, b0)); acc[2][1] = dmin(acc[2][1], dmax(a2, b1));
-            acc[3][0] = dmin(acc[3][0], dmax(a3, b0)); acc[3][1] = dmin(acc[3][1], dmax(a3, b1));
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (tx[u] < 0) continue;
+            const int kk_end = min(kc, kend[u] - rp0 + 1);
+            for (int kk = 0; kk < kk_end; ++kk) mm_step(acc[u], &As[kk][4 * tx[u]], &Bs[kk][4 * tr[u]]);
         }
         __syncthreads();
     }
     double* X = ws + lay.X;
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const int xi = xi0 + cx * 4 + a;
-        if (xi > j + 1) continue;
+    for (int u = 0; u < 2; ++u) {
+        if (tx[u] < 0) continue;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int r = r0 + cr * 2 + c;
+        for (int c = 0; c < 4; ++c) {
+            const int r = r0 + 4 * tr[u] + c;
             if (r > V - j) continue;
-            X[X_base(L, j + r, r) + (int64_t)(lp - 1) * j + (xi - 2)] = acc[a][c];
+            double* Xr = X + X_base(L, j + r, r) + (int64_t)(lp - 1) * j;
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int xi = xi0 + 4 * tx[u] + a;
+                if (xi <= j + 1) Xr[xi - 2] = acc[u][a][c];
+            }
         }
     }
 }
@@ -206,16 +245,21 @@ __device__ __forceinline__ double stage_term(int M, int L, int V, const double* 
 }
 
 // ----------------------------------------------------------------------------
-// k_combine(i): slice W_i for every (r, l, xi).  grid (n_inst, i, tiles_l * tiles_x).
+// k_combine(i): slice W_i(l, r, xi) = min_{l'} max(X(l', xi, r, i), stage(l', l, r, i)).
+// grid (n_inst, i, planes): one CTA per (instance, r, 128 l x 64 xi plane);
+// r = 1 (the largest j) comes first in launch order.
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_combine(pp_batch b, int i, int tiles_x) {
+constexpr int CB_T = 256, CB_L = 128, CB_X = 64;
+constexpr size_t CB_SMEM = sizeof(double) * KC * (CB_X + 4 + CB_L + 4);
+
+__global__ void __launch_bounds__(CB_T, 2) k_combine(pp_batch b, int i, int planes_x) {
     const pp_instance I = b.inst[blockIdx.x];
     const int L = I.L, V = I.V, M = I.M;
     const int r = blockIdx.y + 1;
     if (i > V || r > i) return;
-    const int tl = blockIdx.z / tiles_x, tx = blockIdx.z % tiles_x;
-    const int l0 = 1 + 32 * tl, x0 = 1 + 32 * tx;
+    const int l0 = 1 + CB_L * (int)(blockIdx.z / planes_x), x0 = 1 + CB_X * (int)(blockIdx.z % planes_x);
     if (l0 > L || x0 > i) return;
+    const int nl = min(CB_L, L - l0 + 1), nx = min(CB_X, i - x0 + 1);
     const bool allow = I.flags & PP_ALLOW_REPLICATION;
     const WsLayout lay = ws_layout(L, V);
     double* ws = b.ws + I.ws_off;
@@ -224,65 +268,87 @@ __global__ void __launch_bounds__(128) k_combine(pp_batch b, int i, int tiles_x)
     const double* minpair = ws + lay.minpair;
     double* Wi = ws + lay.W + W_base(L, i);
     const int t = threadIdx.x;
-
-    if (r == i || (!allow && r != 1) || x0 > i - r + 1) {
-        // partition.py:103-104 (no replication) and :115-121 (base / INF rules);
-        // tiles whose every xi exceeds i-r+1 are infeasible (earlier stages need xi-1 devices)
-        for (int e = t; e < 32 * 32; e += 128) {
-            const int l = l0 + (e >> 5), xi = x0 + (e & 31);
-            if (l > L || xi > i) continue;
-            double v = PP_INF;
-            if (r == i && xi == 1 && (allow || i == 1)) {
-                // partition.py:117-119: M * span(1, l) / i + sync(1, l, 1, i)
-                double sync = 0.0;
-                if (i > 1) sync = 2.0 * (double)(i - 1) * psum[l - 1] / ((double)i * minpair[i - 1]);
-                v = (double)M * (prefix[l] - prefix[0]) / (double)i + sync;
-            }
-            Wi[((int64_t)(l - 1) * i + (r - 1)) * i + (xi - 1)] = v;
-        }
-        return;
-    }
     const int j = i - r;
+    // computed columns: xi in [cA, cB]; every other cell of the block is +inf
+    const int cA = max(x0, 2), cB = min(x0 + nx - 1, j + 1);
+    const bool dp_cells = r < i && (allow || r == 1) && cA <= cB;
+    const int ncol = dp_cells ? cB - cA + 1 : 0;
+    const int ntx = (ncol + 3) >> 2, ntl = (nl + 3) >> 2, ntiles = dp_cells ? ntx * ntl : 0;
+    // fill the cells no tile writes: base row (r == i), xi = 1, xi > j + 1, disabled widths
+    for (int e = t; e < nl * nx; e += CB_T) {
+        const int l = l0 + e / nx, xi = x0 + e % nx;
+        if (dp_cells && xi >= cA && xi < cA + 4 * ntx) continue;
+        double v = PP_INF;
+        if (r == i && xi == 1 && (allow || i == 1)) {
+            // partition.py:117-119: M * span(1, l) / i + sync(1, l, 1, i)
+            double sync = 0.0;
+            if (i > 1) sync = 2.0 * (double)(i - 1) * psum[l - 1] / ((double)i * minpair[i - 1]);
+            v = (double)M * (prefix[l] - prefix[0]) / (double)i + sync;
+        }
+        Wi[((int64_t)(l - 1) * i + (r - 1)) * i + (xi - 1)] = v;
+    }
+    if (!dp_cells) return;
+
     const double* X = ws + lay.X + X_base(L, i, r);
-    __shared__ double Xs[32][33];   // [l'][xi]
-    __shared__ double Ss[32][33];   // [l'][l]
-    const int cx = t & 15, cl = t >> 4;
-    double acc[4][2];
+    extern __shared__ __align__(16) double cb_smem[];
+    double (*Xs)[CB_X + 4] = reinterpret_cast<double (*)[CB_X + 4]>(cb_smem);              // [l' - lp0][xi - cA]
+    double (*Ss)[CB_L + 4] = reinterpret_cast<double (*)[CB_L + 4]>(cb_smem + KC * (CB_X + 4));   // [l' - lp0][l - l0]
+    const int wx = ntx * 4, wl = ntl * 4;
+    int ti[2], tj[2], kbeg[2], kend[2];
+    double acc[2][4][4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) { acc[a][0] = PP_INF; acc[a][1] = PP_INF; }
-    const int kmin = max(1, x0 - 1);
-    const int kmax = min(L - 1, l0 + 30);
-    for (int lp0 = kmin; lp0 <= kmax; lp0 += 32) {
+    for (int u = 0; u < 2; ++u) {
+        const int id = t + u * CB_T;
+        ti[u] = (id < ntiles) ? id / ntx : -1;   // row tile (l)
+        tj[u] = (id < ntiles) ? id % ntx : 0;    // column tile (xi)
+        // candidates need l' >= xi - 1 (X is +inf below) and l' <= l - 1
+        kbeg[u] = max(1, cA + 4 * tj[u] - 1);
+        kend[u] = min(L - 1, l0 + 4 * ti[u] + 2);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int e = t + 128 * q, rr = e >> 5, cc = e & 31;
-            const int lp = lp0 + rr;
-            const int xi = x0 + cc;
-            Xs[rr][cc] = (lp <= kmax && xi >= 2 && xi <= j + 1) ? X[(int64_t)(lp - 1) * j + (xi - 2)] : PP_INF;
-            const int l = l0 + cc;
-            Ss[rr][cc] = (lp < l && l <= L) ? stage_term(M, L, V, prefix, psum, minpair, lp, l, r, i) : PP_INF;
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[u][a][c] = PP_INF;
+    }
+    const int kmin = max(1, cA - 1), kmax = min(L - 1, l0 + nl - 2);
+    const double mp = minpair[(int64_t)(i - r) * V + (i - 1)];
+    for (int lp0 = kmin; lp0 <= kmax; lp0 += KC) {
+        const int kc = min(KC, kmax - lp0 + 1);
+        for (int e = t; e < kc * wx; e += CB_T) {
+            const int rr = e / wx, cc = e - rr * wx;
+            Xs[rr][cc] = (cc < ncol) ? X[(int64_t)(lp0 + rr - 1) * j + (cA + cc - 2)] : PP_INF;
+        }
+        for (int e = t; e < kc * wl; e += CB_T) {
+            const int rr = e / wl, cc = e - rr * wl;
+            const int lp = lp0 + rr, l = l0 + cc;
+            double s = PP_INF;
+            if (cc < nl && lp < l) {
+                s = (double)M * (prefix[l] - prefix[lp]) / (double)r;
+                if (r > 1) s += 2.0 * (double)(r - 1) * psum[(int64_t)lp * L + (l - 1)] / ((double)r * mp);
+            }
+            Ss[rr][cc] = s;
         }
         __syncthreads();
-#pragma unroll 8
-        for (int k = 0; k < 32; ++k) {
-            double x0v = Xs[k][cx * 2 + 0], x1v = Xs[k][cx * 2 + 1];
-            double s0 = Ss[k][cl * 4 + 0], s1 = Ss[k][cl * 4 + 1], s2 = Ss[k][cl * 4 + 2], s3 = Ss[k][cl * 4 + 3];
-            acc[0][0] = dmin(acc[0][0], dmax(x0v, s0)); acc[0][1] = dmin(acc[0][1], dmax(x1v, s0));
-            acc[1][0] = dmin(acc[1][0], dmax(x0v, s1)); acc[1][1] = dmin(acc[1][1], dmax(x1v, s1));
-            acc[2][0] = dmin(acc[2][0], dmax(x0v, s2)); acc[2][1] = dmin(acc[2][1], dmax(x1v, s2));
-            acc[3][0] = dmin(acc[3][0], dmax(x0v, s3)); acc[3][1] = dmin(acc[3][1], dmax(x1v, s3));
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (ti[u] < 0) continue;
+            const int k0 = max(0, kbeg[u] - lp0), k1 = min(kc, kend[u] - lp0 + 1);
+            for (int kk = k0; kk < k1; ++kk) mm_step(acc[u], &Ss[kk][4 * ti[u]], &Xs[kk][4 * tj[u]]);
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const int l = l0 + cl * 4 + a;
-        if (l > L) continue;
+    for (int u = 0; u < 2; ++u) {
+        if (ti[u] < 0) continue;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int xi = x0 + cx * 2 + c;
-            if (xi > i) continue;
-            Wi[((int64_t)(l - 1) * i + (r - 1)) * i + (xi - 1)] = acc[a][c];
+        for (int a = 0; a < 4; ++a) {
+            const int l = l0 + 4 * ti[u] + a;
+            if (l > L) continue;
+            double* row = Wi + ((int64_t)(l - 1) * i + (r - 1)) * i;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int xi = cA + 4 * tj[u] + c;
+                if (xi < x0 + nx) row[xi - 1] = acc[u][a][c];
+            }
         }
     }
 }
