@@ -9,8 +9,13 @@
 namespace pp {
 __global__ void k_prep(pp_batch b);
 __global__ void k_phi(pp_batch b);
-__global__ void k_expand(pp_batch b, int j, int planes_r);
-__global__ void k_combine(pp_batch b, int i, int planes_x);
+__global__ void k_base(pp_batch b, int full_rows);
+__global__ void k_expand(pp_batch b, int j, int planes_r, int ybase);
+__global__ void k_combine_diag(pp_batch b, int j, int planes_x);
+__global__ void k_expand_s(pp_batch b, int j);
+__global__ void k_sdedup(pp_batch b);
+__global__ void k_stab(pp_batch b);
+__global__ void k_combine_s(pp_batch b, int j);
 __global__ void k_backtrack(pp_batch b);
 __global__ void k_query(pp_batch b, int n, const int* qi, const int* ql, const int* qx, const int* qr,
                         const int* qd, int max_xi, double* w, int* frag, int* feas);
@@ -101,19 +106,53 @@ int pp_prm(const pp_batch* b, void* stream) {
     dim3 gp(b->n_inst, maxL > maxV ? maxL : maxV);
     k_prep<<<gp, 128, 0, S(stream)>>>(*b);
     PP_CHECK_LAUNCH("k_prep");
-    const int planes_l = ceil_div(maxL, 128);   // k_combine plane: 128 l x 64 xi
-    cudaFuncSetAttribute(k_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CB_SMEM);
-    for (int i = 1; i <= maxV; ++i) {
-        const int planes_x = ceil_div(i, 64);
-        dim3 gc(b->n_inst, i, planes_l * planes_x);
-        k_combine<<<gc, 256, CB_SMEM, S(stream)>>>(*b, i, planes_x);
-        PP_CHECK_LAUNCH("k_combine");
-        if (i < maxV && maxL > 1) {   // k_expand plane: 64 xi x 64 r per l'
-            const int planes_xi = ceil_div(i, 64), planes_r = ceil_div(maxV - i, 64);
-            dim3 ge(b->n_inst, maxL - 1, planes_xi * planes_r);
-            k_expand<<<ge, 128, 0, S(stream)>>>(*b, i, planes_r);
-            PP_CHECK_LAUNCH("k_expand");
+    dim3 gbase(b->n_inst, maxL > maxV ? maxL : maxV);
+    k_base<<<gbase, 128, 0, S(stream)>>>(*b, !(maxL <= SR_MAX && maxV <= SR_MAX));
+    PP_CHECK_LAUNCH("k_base");
+    // wavefront: step j = expand(j) (X for every target (r, j+r) + their stage
+    // terms) then combine_diag(j) (W for every target (r, j+r)); afterwards
+    // slice j+1 is complete.
+    if (maxL <= SR_MAX && maxV <= SR_MAX) {
+        // shared-memory-resident path: one barrier per work item
+        k_sdedup<<<b->n_inst, 128, 0, S(stream)>>>(*b);
+        PP_CHECK_LAUNCH("k_sdedup");
+        if (maxV > 1 && maxL > 1) {
+            dim3 gs(b->n_inst, maxV - 1, maxV);
+            k_stab<<<gs, 128, 0, S(stream)>>>(*b);
+            PP_CHECK_LAUNCH("k_stab");
         }
+        const size_t ex_smem = sizeof(double) * (size_t)maxV * maxV;
+        const size_t cs_smem = sizeof(double) * ((maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 +
+                                                 (size_t)(maxL > 1 ? maxL - 1 : 0) * maxV);
+        cudaFuncSetAttribute(k_expand_s, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ex_smem);
+        cudaFuncSetAttribute(k_combine_s, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs_smem);
+        for (int j = 1; j < maxV; ++j) {
+            if (maxL > 1) {
+                dim3 ge(b->n_inst, maxL - 1);
+                k_expand_s<<<ge, 128, sizeof(double) * (size_t)j * maxV, S(stream)>>>(*b, j);
+                PP_CHECK_LAUNCH("k_expand_s");
+            }
+            dim3 gc(b->n_inst, maxV - j);
+            const size_t sm = sizeof(double) * ((maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 +
+                                                (size_t)(maxL > 1 ? maxL - 1 : 0) * j);
+            k_combine_s<<<gc, 256, sm, S(stream)>>>(*b, j);
+            PP_CHECK_LAUNCH("k_combine_s");
+        }
+        dim3 gb(b->n_inst, maxV);
+        k_backtrack<<<gb, 32, 0, S(stream)>>>(*b);
+        PP_CHECK_LAUNCH("k_backtrack");
+        return PP_OK;
+    }
+    const int rows_l = ceil_div(maxL, CD_L), planes_cx = ceil_div(maxV, CD_X);
+    cudaFuncSetAttribute(k_combine_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CD_SMEM);
+    for (int j = 1; j < maxV; ++j) {
+        const int planes_xi = ceil_div(j, EX_P), planes_r = ceil_div(maxV - j, EX_P);
+        dim3 ge(b->n_inst, (maxL - 1) + (maxV - j), planes_xi * planes_r);
+        k_expand<<<ge, EX_T, 0, S(stream)>>>(*b, j, planes_r, maxL - 1);
+        PP_CHECK_LAUNCH("k_expand");
+        dim3 gc(b->n_inst, maxV - j, rows_l * planes_cx);
+        k_combine_diag<<<gc, CD_T, CD_SMEM, S(stream)>>>(*b, j, planes_cx);
+        PP_CHECK_LAUNCH("k_combine_diag");
     }
     dim3 gb(b->n_inst, maxV);
     k_backtrack<<<gb, 32, 0, S(stream)>>>(*b);

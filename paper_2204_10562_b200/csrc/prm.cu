@@ -9,13 +9,26 @@
 // is evaluated in factored form (bit-exact: max/min are exact and monotone):
 //   expand(j):  X(l', xi, r, j+r) = min_{r'} max(W_j(l', xi-1, r'), chan(l', r', r, j+r))
 //   combine(i): W_i(l, r, xi)     = min_{l'} max(X(l', xi, r, i), stage(l', l, r, i))
-// Both are (min, max)-semiring matrix products; each CTA computes a 32x32
-// output tile from smem-staged 32x32 operand tiles, 4x2 / 2x4 register
-// micro-tiles per thread.  Arg-mins are not stored: the backtrack re-derives
+// Both are (min, max)-semiring matrix products computed with register
+// micro-tiles from shared-memory operand chunks.  Schedule ("diagonal"): step j
+// runs expand(j) and then combine for every target (r, j + r) — after step j
+// slice j + 1 is complete.  Arg-mins are not stored: the backtrack re-derives
 // the reference's first-found (l', r') for the few cells on each chosen path.
 #include "common.cuh"
 
 namespace pp {
+
+// W(l, xi, r, i) with the structural +inf rules of partition.py:103-121 applied
+// by index (those cells are never materialised by the shared-memory path):
+// base cells (r = i) hold a value only at xi = 1; other cells need
+// 2 <= xi <= i - r + 1; without replication only r = 1 (or the 1-GPU base).
+__device__ __forceinline__ bool W_structural(int i, int r, int xi, bool allow) {
+    if (r == i) return xi == 1 && (allow || i == 1);
+    return xi >= 2 && xi <= i - r + 1 && (allow || r == 1);
+}
+__device__ __forceinline__ double W_at(const double* W, int L, int i, int l, int r, int xi, bool allow) {
+    return W_structural(i, r, xi, allow) ? W[W_idx(L, i, l, r, xi)] : PP_INF;
+}
 
 // ----------------------------------------------------------------------------
 // k_prep: per instance tables (partition.py:59-93, cost.py:64-99, cost.py:126-142)
@@ -128,56 +141,224 @@ __global__ void __launch_bounds__(128) k_phi(pp_batch b) {
 }
 
 // ----------------------------------------------------------------------------
-// (min, max) micro-kernel shared by expand and combine: a thread owns a 4x4
-// register tile of outputs and folds one K index per step,
-//     acc[a][c] = min(acc[a][c], max(p[a], q[c])),
-// p from a 4-wide slice of the "row" operand and q from the "column" operand,
-// both read from shared memory as two LDS.128 each.  Every output's K range
-// is trimmed to where its candidates can be finite (the triangular l' < l and
-// r' <= j - xi + 2 structure), so padded INF candidates are not evaluated.
+// k_base (once, after k_prep): grid (n_inst, max(L, V)), row y.
+//   l = y + 1 <= L : the base row of every slice, W_i(l, r = i, xi) for i = 1..V
+//                    (partition.py:117-121: xi = 1 -> M*span(1,l)/i + sync(1,l,1,i), else inf)
+//   l' = y in [1, L): T1[r][l'][l] = (M * span(l'+1, l)) / r for r = 1..V-1, l > l'
+//                    (partition.py:127; the i-independent half of every stage term)
 // ----------------------------------------------------------------------------
-constexpr int KC = 32;   // K chunk staged per __syncthreads
-
-__device__ __forceinline__ void mm_step(double (&acc)[4][4], const double* prow, const double* qrow) {
-    const double2 p01 = *reinterpret_cast<const double2*>(prow);
-    const double2 p23 = *reinterpret_cast<const double2*>(prow + 2);
-    const double2 q01 = *reinterpret_cast<const double2*>(qrow);
-    const double2 q23 = *reinterpret_cast<const double2*>(qrow + 2);
-    const double p[4] = {p01.x, p01.y, p23.x, p23.y};
-    const double q[4] = {q01.x, q01.y, q23.x, q23.y};
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[a][c] = dmin(acc[a][c], dmax(p[a], q[c]));
+__global__ void __launch_bounds__(128) k_base(pp_batch b, int full_rows) {
+    const pp_instance I = b.inst[blockIdx.x];
+    const int L = I.L, V = I.V, M = I.M;
+    const bool allow = I.flags & PP_ALLOW_REPLICATION;
+    const WsLayout lay = ws_layout(L, V);
+    double* ws = b.ws + I.ws_off;
+    const double* prefix = ws + lay.prefix;
+    const double* psum = ws + lay.psum;
+    const double* minpair = ws + lay.minpair;
+    const int y = blockIdx.y, t = threadIdx.x;
+    if (y < L) {
+        const int l = y + 1;
+        // the chunked path (batch-wide choice) reads whole rows: give it explicit +inf cells
+        if (full_rows)
+            for (int i = 2; i <= V; ++i) {
+                double* row = ws + lay.W + W_base(L, i) + ((int64_t)(l - 1) * i + (i - 1)) * i;
+                for (int xi = 2 + t; xi <= i; xi += blockDim.x) row[xi - 1] = PP_INF;
+            }
+        for (int i = 1; i <= V; ++i) {
+            double* row = ws + lay.W + W_base(L, i) + ((int64_t)(l - 1) * i + (i - 1)) * i;
+            if (t == 0) {   // only xi = 1 is structural; the rest of the row reads as +inf (W_at)
+                double v = PP_INF;
+                if (allow || i == 1) {
+                    double sync = 0.0;
+                    if (i > 1) sync = 2.0 * (double)(i - 1) * psum[l - 1] / ((double)i * minpair[i - 1]);
+                    v = (double)M * (prefix[l] - prefix[0]) / (double)i + sync;
+                }
+                row[0] = v;
+            }
+        }
+    }
+    if (y >= 1 && y < L) {
+        const int lp = y, w = L - lp;
+        double* T1 = ws + lay.T1;
+        for (int e = t; e < (V - 1) * w; e += blockDim.x) {
+            const int r = 1 + e / w, l = lp + 1 + e % w;
+            T1[stage_idx(L, r, lp, l)] = (double)M * (prefix[l] - prefix[lp]) / (double)r;
+        }
+    }
 }
 
 // ----------------------------------------------------------------------------
-// k_expand(j): once slice j is final, X(l', xi, r, i = j + r) for every target,
-//   X = min_{r' <= j} max(W_j(l', xi-1, r'), chan(l', r', r, i)),
-//   chan = (M * payload(l')) / ((r' * r) * cross(r', r, i))   (partition.py:130-138)
-// grid (n_inst, maxL-1, planes): one CTA per (instance, l', 64 xi x 64 r plane).
+// Stage-term tables for the shared-memory path.  S(l', l, r, i) depends on the
+// item (r, i) only through r and mp = minpair(i-r+1, i) (cost.py:99), so items
+// whose last-stage slices have bitwise-equal min-pair bandwidth share one
+// table.  k_sdedup: one thread per r assigns every (r, i) the slot of the
+// first i' with the same mp (sidx), slots numbered densely per instance.
+// k_stab: one CTA per canonical item fills its packed triangle
+//   row l' (1..L-1): S(l', l) = T1[r][l'][l] (+ sync if r > 1), l = l'+1..L.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_sdedup(pp_batch b) {
+    const pp_instance I = b.inst[blockIdx.x];
+    const int L = I.L, V = I.V;
+    if (L > SR_MAX || V > SR_MAX) return;
+    const WsLayout lay = ws_layout(L, V);
+    double* ws = b.ws + I.ws_off;
+    const double* minpair = ws + lay.minpair;
+    int* sidx = reinterpret_cast<int*>(ws + lay.sidx);
+    __shared__ int s_cnt[SR_MAX + 1];
+    const int t = threadIdx.x;
+    for (int r = 1 + t; r < V; r += blockDim.x) {   // pass 1: distinct mp values per r
+        int nd = 0;
+        for (int i = r + 1; i <= V; ++i) {
+            const double m = minpair[(int64_t)(i - r) * V + (i - 1)];
+            int first = i;
+            for (int q = r + 1; q < i; ++q)
+                if (minpair[(int64_t)(q - r) * V + (q - 1)] == m) { first = q; break; }
+            sidx[(r - 1) * V + (i - 1)] = (first == i) ? nd++ : -(first);   // provisional
+        }
+        s_cnt[r] = nd;
+    }
+    __syncthreads();
+    if (t == 0) {
+        int o = 0;
+        for (int r = 1; r < V; ++r) { const int c = s_cnt[r]; s_cnt[r] = o; o += c; }
+    }
+    __syncthreads();
+    for (int r = 1 + t; r < V; r += blockDim.x) {   // pass 2: global slot ids
+        const int base = s_cnt[r];
+        for (int i = r + 1; i <= V; ++i) {
+            int* e = &sidx[(r - 1) * V + (i - 1)];
+            *e = (*e >= 0) ? base + *e : sidx[(r - 1) * V + (-*e - 1)];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(128) k_stab(pp_batch b) {
+    const pp_instance I = b.inst[blockIdx.x];
+    const int L = I.L, V = I.V;
+    const int r = blockIdx.y + 1, i = blockIdx.z + 1;
+    if (L > SR_MAX || V > SR_MAX || r >= V || i <= r || i > V) return;
+    const WsLayout lay = ws_layout(L, V);
+    double* ws = b.ws + I.ws_off;
+    const int* sidx = reinterpret_cast<const int*>(ws + lay.sidx);
+    const int slot = sidx[(r - 1) * V + (i - 1)];
+    // only the canonical item of its slot (the first i with this slot) fills it
+    for (int q = r + 1; q < i; ++q)
+        if (sidx[(r - 1) * V + (q - 1)] == slot) return;
+    const int64_t tri = (int64_t)(L - 1) * L / 2;
+    double* out = ws + lay.Stab + (int64_t)slot * tri;
+    const double* T1 = ws + lay.T1;
+    const double* psum = ws + lay.psum;
+    const double den = (double)r * ws[lay.minpair + (int64_t)(i - r) * V + (i - 1)];
+    const double num = 2.0 * (double)(r - 1);
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, nw = blockDim.x >> 5;
+    int off = 0;
+    for (int lp = 1; lp < L; ++lp) {
+        if ((lp - 1) % nw == warp) {
+            const double* t1 = T1 + stage_idx(L, r, lp, 1);
+            const double* ps = psum + (int64_t)lp * L;
+            double a[4], p[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int l = lp + 1 + lane + 32 * u;
+                a[u] = (l <= L) ? t1[l - 1] : 0.0;
+                p[u] = (l <= L && r > 1) ? ps[l - 1] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int l = lp + 1 + lane + 32 * u;
+                if (l > L) continue;
+                double sv = a[u];
+                if (r > 1) sv += num * p[u] / den;   // partition.py:128-129, cost.py:99
+                out[off + (l - lp - 1)] = sv;
+            }
+        }
+        off += L - lp;
+    }
+}
+
+// (min, max) micro-kernel: a thread owns a TA x TB register tile and folds one
+// K index per step, acc[a][c] = min(acc[a][c], max(p[a], q[c])).
+template <int TA, int TB>
+__device__ __forceinline__ void mm_step(double (&acc)[TA][TB], const double* prow, const double* qrow) {
+    double p[TA], q[TB];
+#pragma unroll
+    for (int a = 0; a < TA; a += 2) { const double2 v = *reinterpret_cast<const double2*>(prow + a); p[a] = v.x; p[a + 1] = v.y; }
+    if constexpr (TB == 1) {
+        q[0] = qrow[0];
+    } else {
+#pragma unroll
+        for (int c = 0; c < TB; c += 2) { const double2 v = *reinterpret_cast<const double2*>(qrow + c); q[c] = v.x; q[c + 1] = v.y; }
+    }
+#pragma unroll
+    for (int a = 0; a < TA; ++a)
+#pragma unroll
+        for (int c = 0; c < TB; ++c) acc[a][c] = dmin(acc[a][c], dmax(p[a], q[c]));
+}
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+constexpr int KC = 32;   // K chunk staged per __syncthreads
+
+// ----------------------------------------------------------------------------
+// k_expand(j), step j of the wavefront, once slice W_j is final:
+//  (a) y < ybase: X(l', xi, r, i = j + r) for every target r (l' = y + 1),
+//        X = min_{r' <= j} max(W_j(l', xi-1, r'), chan(l', r', r, i)),
+//        chan = (M * payload(l')) / ((r' * r) * cross(r', r, i))   (partition.py:130-138)
+//      one CTA per (instance, l', 64 xi x 64 r plane), 4x4 register tiles,
+//      K range per tile trimmed to r' <= j - xi + 2 (W_j is inf beyond).
+//  (b) y >= ybase: the full stage-term table of step j's combine targets,
+//        S[r][l'][l] = T1[r][l'][l] (+ sync(l'+1, l, j+1, j+r) if r > 1), inf for l <= l'
+//      (partition.py:127-129, cost.py:99), r = y - ybase + 1.
 // ----------------------------------------------------------------------------
 constexpr int EX_T = 128, EX_P = 64, EX_S = EX_P + 4;
 
-__global__ void __launch_bounds__(EX_T) k_expand(pp_batch b, int j, int planes_r) {
+__global__ void __launch_bounds__(EX_T) k_expand(pp_batch b, int j, int planes_r, int ybase) {
     const pp_instance I = b.inst[blockIdx.x];
-    const int L = I.L, V = I.V;
+    const int L = I.L, V = I.V, M = I.M;
+    if (j >= V) return;
+    const WsLayout lay = ws_layout(L, V);
+    double* ws = b.ws + I.ws_off;
+    const int t = threadIdx.x;
+    if ((int)blockIdx.y >= ybase) {
+        const int r = (int)blockIdx.y - ybase + 1;
+        if (blockIdx.z != 0 || r > V - j) return;
+        const int i = j + r;
+        const double* T1 = ws + lay.T1;
+        const double* psum = ws + lay.psum;
+        const double den = (double)r * ws[lay.minpair + (int64_t)(i - r) * V + (i - 1)];
+        const double num = 2.0 * (double)(r - 1);
+        double* S = ws + lay.S + stage_idx(L, r, 0, 1);
+#pragma unroll 4
+        for (int e = t; e < L * L; e += EX_T) {
+            const int lp = e / L, l = e - lp * L + 1;
+            double s = PP_INF;
+            if (lp >= 1 && l > lp) {
+                s = T1[stage_idx(L, r, lp, l)];
+                if (r > 1) s += num * psum[(int64_t)lp * L + (l - 1)] / den;
+            }
+            S[e] = s;
+        }
+        return;
+    }
     const int lp = blockIdx.y + 1;
-    if (j >= V || lp > L - 1) return;
+    if (lp > L - 1) return;
     const int xi0 = 2 + EX_P * (int)(blockIdx.z / planes_r), r0 = 1 + EX_P * (int)(blockIdx.z % planes_r);
     const int nxi = min(EX_P, j + 2 - xi0), nr = min(EX_P, V - j + 1 - r0);
     if (nxi <= 0 || nr <= 0) return;
-    const WsLayout lay = ws_layout(L, V);
-    double* ws = b.ws + I.ws_off;
     const double* Wj = ws + lay.W;
     const double* cross = ws + lay.cross;
-    const double Mp = (double)I.M * (b.efwd[I.layer_off + lp - 1] + b.ebwd[I.layer_off + lp - 1]);   // partition.py:131,137
+    const double Mp = (double)M * (b.efwd[I.layer_off + lp - 1] + b.ebwd[I.layer_off + lp - 1]);   // partition.py:131,137
     __shared__ __align__(16) double As[KC][EX_S];   // [r'][xi - xi0]  W_j(l', xi-1, r')
     __shared__ __align__(16) double Bs[KC][EX_S];   // [r'][r - r0]    chan(l', r', r, j+r)
-    const int t = threadIdx.x;
     const int ntx = (nxi + 3) >> 2, ntr = (nr + 3) >> 2, ntiles = ntx * ntr;
     const int wx = ntx * 4, wr = ntr * 4;
-    // up to two 4x4 tiles per thread
     int tx[2], tr[2], kend[2];
     double acc[2][4][4];
 #pragma unroll
@@ -185,20 +366,18 @@ __global__ void __launch_bounds__(EX_T) k_expand(pp_batch b, int j, int planes_r
         const int id = t + u * EX_T;
         tx[u] = (id < ntiles) ? id % ntx : -1;
         tr[u] = (id < ntiles) ? id / ntx : 0;
-        // candidates need r' <= j - xi + 2; the tile's smallest xi bounds its K range
         kend[u] = (id < ntiles) ? j - (xi0 + 4 * tx[u]) + 2 : 0;
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[u][a][c] = PP_INF;
     }
-    const int kmax = j - xi0 + 2;   // largest r' any output of the plane needs
+    const int kmax = j - xi0 + 2;
     for (int rp0 = 1; rp0 <= kmax; rp0 += KC) {
         const int kc = min(KC, kmax - rp0 + 1);
         for (int e = t; e < kc * wx; e += EX_T) {
             const int rr = e / wx, cc = e - rr * wx;
-            const int xi = xi0 + cc;
-            As[rr][cc] = (cc < nxi) ? Wj[W_idx(L, j, lp, rp0 + rr, xi - 1)] : PP_INF;
+            As[rr][cc] = (cc < nxi) ? Wj[W_idx(L, j, lp, rp0 + rr, xi0 + cc - 1)] : PP_INF;
         }
         for (int e = t; e < kc * wr; e += EX_T) {
             const int rr = e / wr, cc = e - rr * wr;
@@ -210,7 +389,7 @@ __global__ void __launch_bounds__(EX_T) k_expand(pp_batch b, int j, int planes_r
         for (int u = 0; u < 2; ++u) {
             if (tx[u] < 0) continue;
             const int kk_end = min(kc, kend[u] - rp0 + 1);
-            for (int kk = 0; kk < kk_end; ++kk) mm_step(acc[u], &As[kk][4 * tx[u]], &Bs[kk][4 * tr[u]]);
+            for (int kk = 0; kk < kk_end; ++kk) mm_step<4, 4>(acc[u], &As[kk][4 * tx[u]], &Bs[kk][4 * tr[u]]);
         }
         __syncthreads();
     }
@@ -233,7 +412,7 @@ __global__ void __launch_bounds__(EX_T) k_expand(pp_batch b, int j, int planes_r
 }
 
 // stage(l', l, r, i) = (M * span(l'+1, l)) / r (+ sync(l'+1, l, i-r+1, i) if r > 1)
-// partition.py:127-129, cost.py:99.
+// partition.py:127-129, cost.py:99 (scalar form, used by the backtrack).
 __device__ __forceinline__ double stage_term(int M, int L, int V, const double* prefix, const double* psum,
                                              const double* minpair, int lp, int l, int r, int i) {
     double s = (double)M * (prefix[l] - prefix[lp]) / (double)r;
@@ -245,112 +424,362 @@ __device__ __forceinline__ double stage_term(int M, int L, int V, const double* 
 }
 
 // ----------------------------------------------------------------------------
-// k_combine(i): slice W_i(l, r, xi) = min_{l'} max(X(l', xi, r, i), stage(l', l, r, i)).
-// grid (n_inst, i, planes): one CTA per (instance, r, 128 l x 64 xi plane);
-// r = 1 (the largest j) comes first in launch order.
+// k_combine_diag(j), step j: every target (r, i = j + r) of slice i,
+//   W_i(l, r, xi) = min_{l'} max(S[r][l'][l], X(l', xi, r, i)),  xi in 2..j+1,
+// every other cell of the row block is +inf.  All CTAs of a launch share j, so
+// their work is uniform.  grid (n_inst, maxV - j, row blocks x xi blocks); the
+// K loop streams 32-row chunks of S and X through a cp.async double buffer.
+// Register tile TL x TX with TX = 4, 2, 1 for j >= 4, 2..3, 1.
 // ----------------------------------------------------------------------------
-constexpr int CB_T = 256, CB_L = 128, CB_X = 64;
-constexpr size_t CB_SMEM = sizeof(double) * KC * (CB_X + 4 + CB_L + 4);
+constexpr int CD_T = 256, CD_L = 64, CD_X = 64, CD_W = 68;
+struct CDSmem {
+    double X[2][KC][CD_W];   // [l' - lp0][xi - cA]
+    double S[2][KC][CD_W];   // [l' - lp0][l - l0]
+};
+constexpr size_t CD_SMEM = sizeof(CDSmem);
 
-__global__ void __launch_bounds__(CB_T, 2) k_combine(pp_batch b, int i, int planes_x) {
-    const pp_instance I = b.inst[blockIdx.x];
-    const int L = I.L, V = I.V, M = I.M;
-    const int r = blockIdx.y + 1;
-    if (i > V || r > i) return;
-    const int l0 = 1 + CB_L * (int)(blockIdx.z / planes_x), x0 = 1 + CB_X * (int)(blockIdx.z % planes_x);
-    if (l0 > L || x0 > i) return;
-    const int nl = min(CB_L, L - l0 + 1), nx = min(CB_X, i - x0 + 1);
-    const bool allow = I.flags & PP_ALLOW_REPLICATION;
-    const WsLayout lay = ws_layout(L, V);
-    double* ws = b.ws + I.ws_off;
-    const double* prefix = ws + lay.prefix;
-    const double* psum = ws + lay.psum;
-    const double* minpair = ws + lay.minpair;
-    double* Wi = ws + lay.W + W_base(L, i);
+template <int TX>
+__device__ void combine_compute(double* Wi, int i, int r, int L, int l0, int nl, int cA, int ncol, int j,
+                                const double* __restrict__ X, const double* __restrict__ Srow, CDSmem& sm) {
+    constexpr int TL = 16 / TX;
     const int t = threadIdx.x;
-    const int j = i - r;
-    // computed columns: xi in [cA, cB]; every other cell of the block is +inf
-    const int cA = max(x0, 2), cB = min(x0 + nx - 1, j + 1);
-    const bool dp_cells = r < i && (allow || r == 1) && cA <= cB;
-    const int ncol = dp_cells ? cB - cA + 1 : 0;
-    const int ntx = (ncol + 3) >> 2, ntl = (nl + 3) >> 2, ntiles = dp_cells ? ntx * ntl : 0;
-    // fill the cells no tile writes: base row (r == i), xi = 1, xi > j + 1, disabled widths
-    for (int e = t; e < nl * nx; e += CB_T) {
-        const int l = l0 + e / nx, xi = x0 + e % nx;
-        if (dp_cells && xi >= cA && xi < cA + 4 * ntx) continue;
-        double v = PP_INF;
-        if (r == i && xi == 1 && (allow || i == 1)) {
-            // partition.py:117-119: M * span(1, l) / i + sync(1, l, 1, i)
-            double sync = 0.0;
-            if (i > 1) sync = 2.0 * (double)(i - 1) * psum[l - 1] / ((double)i * minpair[i - 1]);
-            v = (double)M * (prefix[l] - prefix[0]) / (double)i + sync;
-        }
-        Wi[((int64_t)(l - 1) * i + (r - 1)) * i + (xi - 1)] = v;
-    }
-    if (!dp_cells) return;
-
-    const double* X = ws + lay.X + X_base(L, i, r);
-    extern __shared__ __align__(16) double cb_smem[];
-    double (*Xs)[CB_X + 4] = reinterpret_cast<double (*)[CB_X + 4]>(cb_smem);              // [l' - lp0][xi - cA]
-    double (*Ss)[CB_L + 4] = reinterpret_cast<double (*)[CB_L + 4]>(cb_smem + KC * (CB_X + 4));   // [l' - lp0][l - l0]
-    const int wx = ntx * 4, wl = ntl * 4;
-    int ti[2], tj[2], kbeg[2], kend[2];
-    double acc[2][4][4];
+    const int ntl = (nl + TL - 1) / TL, ntx = (ncol + TX - 1) / TX, ntiles = ntl * ntx;
+    const int wl = ntl * TL, wx = ntx * TX;
+    int ti[2], tj[2], kb[2], ke[2];
+    double acc[2][TL][TX];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-        const int id = t + u * CB_T;
-        ti[u] = (id < ntiles) ? id / ntx : -1;   // row tile (l)
-        tj[u] = (id < ntiles) ? id % ntx : 0;    // column tile (xi)
-        // candidates need l' >= xi - 1 (X is +inf below) and l' <= l - 1
-        kbeg[u] = max(1, cA + 4 * tj[u] - 1);
-        kend[u] = min(L - 1, l0 + 4 * ti[u] + 2);
+        const int id = t + u * CD_T;
+        ti[u] = (id < ntiles) ? id / ntx : -1;
+        tj[u] = (id < ntiles) ? id % ntx : 0;
+        kb[u] = max(1, cA + TX * tj[u] - 1);          // X(l', xi) is inf for l' < xi - 1
+        ke[u] = min(L - 1, l0 + TL * ti[u] + TL - 2);  // S(l', l) is inf for l' >= l
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < TL; ++a)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) acc[u][a][c] = PP_INF;
+            for (int c = 0; c < TX; ++c) acc[u][a][c] = PP_INF;
     }
     const int kmin = max(1, cA - 1), kmax = min(L - 1, l0 + nl - 2);
-    const double mp = minpair[(int64_t)(i - r) * V + (i - 1)];
-    for (int lp0 = kmin; lp0 <= kmax; lp0 += KC) {
+    auto stage = [&](int buf, int lp0) {
         const int kc = min(KC, kmax - lp0 + 1);
-        for (int e = t; e < kc * wx; e += CB_T) {
+        for (int e = t; e < KC * wx; e += CD_T) {
             const int rr = e / wx, cc = e - rr * wx;
-            Xs[rr][cc] = (cc < ncol) ? X[(int64_t)(lp0 + rr - 1) * j + (cA + cc - 2)] : PP_INF;
+            double* d = &sm.X[buf][rr][cc];
+            if (rr < kc && cc < ncol) cp_async8(d, X + (int64_t)(lp0 + rr - 1) * j + (cA - 2 + cc));
+            else *d = PP_INF;
         }
-        for (int e = t; e < kc * wl; e += CB_T) {
+        for (int e = t; e < KC * wl; e += CD_T) {
             const int rr = e / wl, cc = e - rr * wl;
-            const int lp = lp0 + rr, l = l0 + cc;
-            double s = PP_INF;
-            if (cc < nl && lp < l) {
-                s = (double)M * (prefix[l] - prefix[lp]) / (double)r;
-                if (r > 1) s += 2.0 * (double)(r - 1) * psum[(int64_t)lp * L + (l - 1)] / ((double)r * mp);
-            }
-            Ss[rr][cc] = s;
+            double* d = &sm.S[buf][rr][cc];
+            if (rr < kc && cc < nl) cp_async8(d, Srow + (int64_t)(lp0 + rr) * L + (l0 - 1 + cc));
+            else *d = PP_INF;
         }
-        __syncthreads();
+        cp_async_commit();
+    };
+    if (kmin <= kmax) {
+        int buf = 0;
+        stage(0, kmin);
+        for (int lp0 = kmin; lp0 <= kmax; lp0 += KC) {
+            if (lp0 + KC <= kmax) { stage(buf ^ 1, lp0 + KC); cp_async_wait<1>(); }
+            else cp_async_wait<0>();
+            __syncthreads();
+            const int kc = min(KC, kmax - lp0 + 1);
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            if (ti[u] < 0) continue;
-            const int k0 = max(0, kbeg[u] - lp0), k1 = min(kc, kend[u] - lp0 + 1);
-            for (int kk = k0; kk < k1; ++kk) mm_step(acc[u], &Ss[kk][4 * ti[u]], &Xs[kk][4 * tj[u]]);
+            for (int u = 0; u < 2; ++u) {
+                if (ti[u] < 0) continue;
+                const int k0 = max(0, kb[u] - lp0), k1 = min(kc, ke[u] - lp0 + 1);
+                for (int kk = k0; kk < k1; ++kk)
+                    mm_step<TL, TX>(acc[u], &sm.S[buf][kk][TL * ti[u]], &sm.X[buf][kk][TX * tj[u]]);
+            }
+            __syncthreads();
+            buf ^= 1;
         }
-        __syncthreads();
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
         if (ti[u] < 0) continue;
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            const int l = l0 + 4 * ti[u] + a;
-            if (l > L) continue;
+        for (int a = 0; a < TL; ++a) {
+            const int l = l0 + TL * ti[u] + a;
+            if (l > L || l >= l0 + nl) continue;
             double* row = Wi + ((int64_t)(l - 1) * i + (r - 1)) * i;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int xi = cA + 4 * tj[u] + c;
-                if (xi < x0 + nx) row[xi - 1] = acc[u][a][c];
+            for (int c = 0; c < TX; ++c) {
+                const int xi = cA + TX * tj[u] + c;
+                if (xi - cA < wx && xi <= i) row[xi - 1] = acc[u][a][c];
             }
         }
     }
+}
+
+__global__ void __launch_bounds__(CD_T, 2) k_combine_diag(pp_batch b, int j, int planes_x) {
+    const pp_instance I = b.inst[blockIdx.x];
+    const int L = I.L, V = I.V;
+    const int r = blockIdx.y + 1;
+    if (j >= V || r > V - j) return;
+    const int i = j + r;
+    const int l0 = 1 + CD_L * (int)(blockIdx.z / planes_x), x0 = 1 + CD_X * (int)(blockIdx.z % planes_x);
+    if (l0 > L || x0 > i) return;
+    const int nl = min(CD_L, L - l0 + 1), nx = min(CD_X, i - x0 + 1);
+    const bool allow = I.flags & PP_ALLOW_REPLICATION;
+    const WsLayout lay = ws_layout(L, V);
+    double* ws = b.ws + I.ws_off;
+    double* Wi = ws + lay.W + W_base(L, i);
+    const int cA = max(x0, 2), cB = min(x0 + nx - 1, j + 1);
+    const bool dp_cells = (allow || r == 1) && cA <= cB;   // partition.py:103-104
+    const int ncol = dp_cells ? cB - cA + 1 : 0;
+    const int TX = ncol >= 4 ? 4 : (ncol >= 2 ? 2 : 1);
+    const int wx = dp_cells ? (ncol + TX - 1) / TX * TX : 0;
+    for (int e = threadIdx.x; e < nl * nx; e += CD_T) {   // xi = 1, xi > j + 1, disabled widths
+        const int l = l0 + e / nx, xi = x0 + e % nx;
+        if (dp_cells && xi >= cA && xi < cA + wx) continue;
+        Wi[((int64_t)(l - 1) * i + (r - 1)) * i + (xi - 1)] = PP_INF;
+    }
+    if (!dp_cells) return;
+    extern __shared__ __align__(16) double cd_smem[];
+    CDSmem& sm = *reinterpret_cast<CDSmem*>(cd_smem);
+    const double* X = ws + lay.X + X_base(L, i, r);
+    const double* Srow = ws + lay.S + stage_idx(L, r, 0, 1);
+    if (TX == 4) combine_compute<4>(Wi, i, r, L, l0, nl, cA, ncol, j, X, Srow, sm);
+    else if (TX == 2) combine_compute<2>(Wi, i, r, L, l0, nl, cA, ncol, j, X, Srow, sm);
+    else combine_compute<1>(Wi, i, r, L, l0, nl, cA, ncol, j, X, Srow, sm);
+}
+
+// ----------------------------------------------------------------------------
+// Shared-memory-resident fast path (L <= 128 and V <= 128, i.e. C1-C4):
+// every work item stages ALL of its operands in shared memory once, crosses a
+// single __syncthreads, and then every thread folds its register tiles over
+// its own trimmed K range with no further barriers (no barrier stalls, no
+// inter-thread imbalance inside a chunk).
+// ----------------------------------------------------------------------------
+
+// expand, step j: one CTA per (instance, l').  smem: A = W_j(l', ., .) block
+// [r'][xi'] (j x j, one contiguous copy), B = chan(l', r', r) [r'][r]
+// (j x (V-j) exact divisions).  Tiles 4 xi x 4 r; tile K range r' <= j - xi0 + 2.
+__global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
+    const pp_instance I = b.inst[blockIdx.x];
+    const int L = I.L, V = I.V, M = I.M;
+    const int lp = blockIdx.y + 1;
+    if (j >= V || lp > L - 1) return;
+    const int nr = V - j;
+    const WsLayout lay = ws_layout(L, V);
+    double* ws = b.ws + I.ws_off;
+    const double* Wsrc = ws + lay.W + W_idx(L, j, lp, 1, 1);
+    const double* cross = ws + lay.cross;
+    const double Mp = (double)M * (b.efwd[I.layer_off + lp - 1] + b.ebwd[I.layer_off + lp - 1]);   // partition.py:131,137
+    extern __shared__ __align__(16) double ex_smem[];
+    double* A = ex_smem;             // [r'-1][xi'-1], stride j
+    double* B = ex_smem + j * j;     // [r'-1][r-1],   stride nr
+    const int t = threadIdx.x;
+    const bool allow = I.flags & PP_ALLOW_REPLICATION;
+    for (int e = t; e < j * j; e += blockDim.x) {   // A[r'-1][xi'-1] = W_j(l', xi', r')
+        const int rp = 1 + e / j, xip = 1 + e % j;
+        A[e] = W_structural(j, rp, xip, allow) ? Wsrc[e] : PP_INF;
+    }
+    for (int e = t; e < j * nr; e += blockDim.x) {
+        const int rp = 1 + e / nr, r = 1 + e % nr;
+        B[e] = Mp / ((double)(rp * r) * cross[cross_idx(V, j + r, r, rp)]);
+    }
+    __syncthreads();
+    const int ntx = (j + 3) >> 2, ntr = (nr + 3) >> 2, ntiles = ntx * ntr;
+    // split-K when the plane has few tiles: ks consecutive lanes share a tile,
+    // fold interleaved r' subsets and min-reduce with shuffles
+    int ks = 1;
+    while (ks < 8 && ntiles * ks * 2 <= (int)blockDim.x) ks *= 2;
+    const int sub = t % ks, lane = t & 31;
+    const unsigned gmask = (ks == 32 ? 0xffffffffu : ((1u << ks) - 1u)) << (lane & ~(ks - 1));
+    double* X = ws + lay.X;
+    for (int id = t / ks; id < ntiles; id += blockDim.x / ks) {
+        const int tx = id % ntx, tr = id / ntx;
+        const int xi0 = 2 + 4 * tx, r0 = 1 + 4 * tr;
+        const int kend = j - xi0 + 2;   // W_j(l', xi-1, r') = inf for r' > j - xi + 2
+        double acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[a][c] = PP_INF;
+        // padded columns read in-range garbage-free copies: clamp and mask at the end
+        const int xa[4] = {min(xi0 - 1, j) - 1, min(xi0, j) - 1, min(xi0 + 1, j) - 1, min(xi0 + 2, j) - 1};
+        const int ra[4] = {min(r0, nr) - 1, min(r0 + 1, nr) - 1, min(r0 + 2, nr) - 1, min(r0 + 3, nr) - 1};
+        for (int rp = 1 + sub; rp <= kend; rp += ks) {
+            const double* Ar = A + (rp - 1) * j;
+            const double* Br = B + (rp - 1) * nr;
+            double p[4], q[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) { p[a] = Ar[xa[a]]; q[a] = Br[ra[a]]; }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[a][c] = dmin(acc[a][c], dmax(p[a], q[c]));
+        }
+        for (int off = 1; off < ks; off <<= 1)
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[a][c] = dmin(acc[a][c], __shfl_xor_sync(gmask, acc[a][c], off));
+        if (sub != 0) continue;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int r = r0 + c;
+            if (r > nr) continue;
+            double* Xr = X + X_base(L, j + r, r) + (int64_t)(lp - 1) * j;
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int xi = xi0 + a;
+                if (xi <= j + 1) Xr[xi - 2] = acc[a][c];
+            }
+        }
+    }
+}
+
+// combine, step j: one CTA per (instance, r), target i = j + r.  smem: the
+// stage terms of the item as a packed triangle (row l' holds l = l'+1..L,
+// S = T1 + sync, T1 from k_base) and X(., ., r, i) (rows l' = 1..L-1, stride j).
+template <int TX>
+__device__ __forceinline__ int tile_nfast(int L, int l0, int xi0) {
+    constexpr int TL = 16 / TX;
+    const int kb = max(1, xi0 - 1), ke = min(L - 1, l0 + TL - 2);
+    return max(0, min(ke, l0 - 1) - kb + 1);
+}
+
+// One TL x TX tile: fold l' in [kb, ke].  The lane walks its own l' sequence
+// (row pointers advance incrementally through the packed triangle), so lanes
+// whose tiles have equal trip counts run in lockstep even though they start
+// at different l'.
+template <int TX>
+__device__ __forceinline__ void combine_tile_s(const double* Stri, const int* trio, const double* Xs, int L, int j,
+                                               int l0, int xi0, double (&acc)[16 / TX][TX]) {
+    constexpr int TL = 16 / TX;
+#pragma unroll
+    for (int a = 0; a < TL; ++a)
+#pragma unroll
+        for (int c = 0; c < TX; ++c) acc[a][c] = PP_INF;
+    int xc[TX];
+#pragma unroll
+    for (int c = 0; c < TX; ++c) xc[c] = min(xi0 + c, j + 1) - 2;   // clamp padded columns; masked on write
+    const int kb = max(1, xi0 - 1);
+    const int ke = min(L - 1, l0 + TL - 2);
+    const int nfast = max(0, min(ke, l0 - 1) - kb + 1);   // l' < l0: every row of the tile has l > l'
+    const double* Sr = Stri + trio[kb] + (l0 - kb - 1);  // S(kb, l0)
+    const double* Xr = Xs + (kb - 1) * j;
+    for (int k = 0; k < nfast; ++k) {
+        double p[TL], q[TX];
+#pragma unroll
+        for (int a = 0; a < TL; ++a) p[a] = Sr[a];
+#pragma unroll
+        for (int c = 0; c < TX; ++c) q[c] = Xr[xc[c]];
+#pragma unroll
+        for (int a = 0; a < TL; ++a)
+#pragma unroll
+            for (int c = 0; c < TX; ++c) acc[a][c] = dmin(acc[a][c], dmax(p[a], q[c]));
+        Sr += L - (kb + k) - 1;   // S(l'+1, l0) = S(l', l0) + (L - l' - 1)
+        Xr += j;
+    }
+    for (int lp = max(kb, l0); lp <= ke; ++lp) {   // the tile's diagonal: rows l <= l' are +inf
+        const double* Xd = Xs + (lp - 1) * j;
+        double q[TX];
+#pragma unroll
+        for (int c = 0; c < TX; ++c) q[c] = Xd[xc[c]];
+#pragma unroll
+        for (int a = 0; a < TL; ++a) {
+            const int l = l0 + a;
+            if (l <= lp || l > L) continue;
+            const double pa = Stri[trio[lp] + (l - lp - 1)];
+#pragma unroll
+            for (int c = 0; c < TX; ++c) acc[a][c] = dmin(acc[a][c], dmax(pa, q[c]));
+        }
+    }
+}
+
+template <int TX>
+__device__ __forceinline__ void combine_tiles_s(double* Wi, int i, int r, int L, int j, const double* Stri,
+                                                const int* trio, const double* Xs, int* hist, int* order) {
+    constexpr int TL = 16 / TX;
+    const int t = threadIdx.x;
+    const int ntl = (L + TL - 1) / TL, ntx = (j + TX - 1) / TX, ntiles = ntl * ntx;
+    // order tiles by trip count (descending) so each warp's lanes run equal-length loops
+    for (int k = t; k < L + 2; k += blockDim.x) hist[k] = 0;
+    __syncthreads();
+    for (int id = t; id < ntiles; id += blockDim.x)
+        atomicAdd(&hist[L - tile_nfast<TX>(L, 1 + TL * (id / ntx), 2 + TX * (id % ntx))], 1);
+    __syncthreads();
+    if (t == 0) {
+        int o = 0;
+        for (int k = 0; k < L + 2; ++k) { const int c = hist[k]; hist[k] = o; o += c; }
+    }
+    __syncthreads();
+    for (int id = t; id < ntiles; id += blockDim.x)
+        order[atomicAdd(&hist[L - tile_nfast<TX>(L, 1 + TL * (id / ntx), 2 + TX * (id % ntx))], 1)] = id;
+    __syncthreads();
+    for (int q = t; q < ntiles; q += blockDim.x) {
+        const int id = order[q];
+        const int l0 = 1 + TL * (id / ntx), xi0 = 2 + TX * (id % ntx);
+        double acc[TL][TX];
+        combine_tile_s<TX>(Stri, trio, Xs, L, j, l0, xi0, acc);
+#pragma unroll
+        for (int a = 0; a < TL; ++a) {
+            const int l = l0 + a;
+            if (l > L) continue;
+            double* row = Wi + ((int64_t)(l - 1) * i + (r - 1)) * i;
+#pragma unroll
+            for (int c = 0; c < TX; ++c) if (xi0 + c <= j + 1) row[xi0 + c - 1] = acc[a][c];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256, 2) k_combine_s(pp_batch b, int j) {
+    const pp_instance I = b.inst[blockIdx.x];
+    const int L = I.L, V = I.V;
+    const int r = blockIdx.y + 1;
+    if (j >= V || r > V - j) return;
+    const int i = j + r;
+    const bool allow = I.flags & PP_ALLOW_REPLICATION;
+    const WsLayout lay = ws_layout(L, V);
+    double* ws = b.ws + I.ws_off;
+    double* Wi = ws + lay.W + W_base(L, i);
+    const int t = threadIdx.x;
+    // cells outside xi in [2, j+1] and disabled widths are structural +inf (W_at)
+    if (!(allow || r == 1)) return;   // partition.py:103-104
+    extern __shared__ __align__(16) double cs_smem[];
+    int* trio = reinterpret_cast<int*>(cs_smem);                 // [L] triangle row offsets
+    double* Stri = cs_smem + (L + 1) / 2 + 1;                    // (L-1)L/2
+    double* Xs = Stri + (L - 1) * L / 2;                         // (L-1) x j
+    __shared__ int s_hist[SR_MAX + 2];
+    __shared__ int s_order[1024];
+    if (t == 0) {
+        int o = 0;
+        for (int lp = 1; lp < L; ++lp) { trio[lp] = o; o += L - lp; }
+    }
+    // X(., ., r, i): rows l' = 1..L-1, one contiguous copy (4 loads in flight per thread)
+    const double* Xg = ws + lay.X + X_base(L, i, r);
+    {
+        const int n = (L - 1) * j;
+        for (int e0 = t; e0 < n; e0 += 4 * 256) {
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { const int e = e0 + 256 * u; v[u] = (e < n) ? Xg[e] : 0.0; }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { const int e = e0 + 256 * u; if (e < n) Xs[e] = v[u]; }
+        }
+    }
+    __syncthreads();
+    // stage terms S(l', l) of this item: the shared triangle of its slot (k_stab)
+    {
+        const int slot = reinterpret_cast<const int*>(ws + lay.sidx)[(r - 1) * V + (i - 1)];
+        const int n = (L - 1) * L / 2;
+        const double* Sg = ws + lay.Stab + (int64_t)slot * n;
+        for (int e0 = t; e0 < n; e0 += 4 * 256) {
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { const int e = e0 + 256 * u; v[u] = (e < n) ? Sg[e] : 0.0; }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { const int e = e0 + 256 * u; if (e < n) Stri[e] = v[u]; }
+        }
+    }
+    __syncthreads();
+    if (j >= 4) combine_tiles_s<4>(Wi, i, r, L, j, Stri, trio, Xs, s_hist, s_order);
+    else if (j >= 2) combine_tiles_s<2>(Wi, i, r, L, j, Stri, trio, Xs, s_hist, s_order);
+    else combine_tiles_s<1>(Wi, i, r, L, j, Stri, trio, Xs, s_hist, s_order);
 }
 
 // ----------------------------------------------------------------------------
@@ -377,6 +806,7 @@ __device__ void dp_walk(const pp_batch& b, const pp_instance& I, int l, int x, i
     const double* minpair = ws + lay.minpair;
     const double* cross = ws + lay.cross;
     const double* W = ws + lay.W;
+    const bool allow = I.flags & PP_ALLOW_REPLICATION;
     const int lane = threadIdx.x & 31;
     while (x >= 2) {
         const int j = i - r;
@@ -399,7 +829,7 @@ __device__ void dp_walk(const pp_batch& b, const pp_instance& I, int l, int x, i
                 const int c = base + lane;
                 bool match = false;
                 if (c <= j) {
-                    const double sub = W[W_idx(L, j, lp, c, x - 1)];
+                    const double sub = W_at(W, L, j, lp, c, x - 1, allow);
                     const double chan = Mp / ((double)(c * r) * cross[cross_idx(V, i, r, c)]);
                     match = dmax(dmax(sub, chan), st) == w;
                 }
@@ -412,7 +842,7 @@ __device__ void dp_walk(const pp_batch& b, const pp_instance& I, int l, int x, i
             return;
         }
         if (lane == 0) { o_ls[x - 1] = lp + 1; o_le[x - 1] = l; o_dlo[x - 1] = i - r + 1; o_dhi[x - 1] = i; }
-        w = W[W_idx(L, j, lp, rp, x - 1)];
+        w = W_at(W, L, j, lp, rp, x - 1, allow);
         l = lp; i = j; r = rp; --x;
     }
     if (lane == 0) { o_ls[0] = 1; o_le[0] = l; o_dlo[0] = 1; o_dhi[0] = i; }
@@ -430,7 +860,7 @@ __global__ void __launch_bounds__(32) k_backtrack(pp_batch b) {
     double best = PP_INF;
     int br = 0;
     for (int r = 1 + lane; r <= V; r += 32) {
-        const double v = (xi <= L) ? W[W_idx(L, V, L, r, xi)] : PP_INF;
+        const double v = (xi <= L) ? W_at(W, L, V, L, r, xi, I.flags & PP_ALLOW_REPLICATION) : PP_INF;
         if (v < best) { best = v; br = r; }   // ascending r per lane: first r on ties
     }
 #pragma unroll
@@ -457,7 +887,7 @@ __global__ void __launch_bounds__(32) k_query(pp_batch b, int n, const int* qi, 
     const WsLayout lay = ws_layout(I.L, I.V);
     const double* W = b.ws + I.ws_off + lay.W;
     double v = PP_INF;
-    if (x <= i && r <= i) v = W[W_idx(I.L, i, l, r, x)];
+    if (x <= i && r <= i) v = W_at(W, I.L, i, l, r, x, I.flags & PP_ALLOW_REPLICATION);
     const int lane = threadIdx.x;
     // Base cells (xi = 1, r = i) are feasible with any value; others iff finite
     // (an infinite candidate never passes `best > w`, partition.py:139).

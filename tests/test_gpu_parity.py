@@ -206,6 +206,21 @@ def test_named_configs_vs_oracle():
     _check_vs_oracle(specs, res)
 
 
+def test_large_shapes_use_the_chunked_dp_path():
+    """L or V above the shared-memory-resident limit (128) run the chunked kernels."""
+    rng = random.Random(9)
+    specs = []
+    lu = lambda lo, hi: math.exp(rng.uniform(math.log(lo), math.log(hi)))
+    for L, V, M in ((150, 5, 4), (140, 9, 8), (3, 136, 2)):
+        ids = rng.sample(range(1, 1000), V)
+        specs.append(_spec([lu(1e-3, 1.0) for _ in range(L)], [lu(1e-3, 2.0) for _ in range(L)],
+                           [lu(1e6, 1e10) for _ in range(L)], [lu(1e5, 1e9) for _ in range(L - 1)],
+                           [lu(1e5, 1e9) for _ in range(L - 1)], ids,
+                           [(a, b, lu(1e8, 1e11)) for k, a in enumerate(ids) for b in ids[k + 1:]], M))
+    res = P.spp_many([model_of(s) for s in specs])
+    _check_vs_oracle(specs, res)
+
+
 def test_c3_full_size_vs_oracle():
     """GPT-96 on the 64-GPU 8x8 two-tier topology, M = 8 and jittered M = 256."""
     from paper_2204_10562_b200 import workloads as W
