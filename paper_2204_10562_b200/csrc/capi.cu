@@ -19,9 +19,9 @@ __global__ void k_combine_s(pp_batch b, int j);
 __global__ void k_backtrack(pp_batch b);
 __global__ void k_query(pp_batch b, int n, const int* qi, const int* ql, const int* qx, const int* qr,
                         const int* qd, int max_xi, double* w, int* frag, int* feas);
-__global__ void k_rdo(pp_batch b, int w_in_smem);
-__global__ void k_min_cut(pp_batch b, int k, const int* verts, int n, unsigned char* in_a, double* weight,
-                          int w_in_smem);
+template <bool SMEM> __global__ void k_rdo(pp_batch b);
+template <bool SMEM>
+__global__ void k_min_cut(pp_batch b, int k, const int* verts, int n, unsigned char* in_a, double* weight);
 __global__ void k_pe_sweep(pp_batch b);
 __global__ void k_select(pp_batch b);
 __global__ void k_replay(pp_batch b);
@@ -94,8 +94,13 @@ int pp_rdo(const pp_batch* b, void* stream) {
     const int V = b->max_V;
     const int in_smem = V <= 128;
     const size_t smem = (in_smem ? sizeof(double) * V * V : 0) + rdo_state_bytes(V);
-    cudaFuncSetAttribute(k_rdo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_rdo<<<b->n_inst, 128, smem, S(stream)>>>(*b, in_smem);
+    if (in_smem) {
+        cudaFuncSetAttribute(k_rdo<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_rdo<true><<<b->n_inst, 128, smem, S(stream)>>>(*b);
+    } else {
+        cudaFuncSetAttribute(k_rdo<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_rdo<false><<<b->n_inst, 128, smem, S(stream)>>>(*b);
+    }
     PP_CHECK_LAUNCH("k_rdo");
     return PP_OK;
 }
@@ -246,8 +251,13 @@ int pp_min_cut(const pp_batch* b, int32_t k, const int32_t* verts, int32_t n, ui
     const int V = b->max_V;
     const int in_smem = V <= 128;
     const size_t smem = (in_smem ? sizeof(double) * V * V : 0) + rdo_state_bytes(V);
-    cudaFuncSetAttribute(k_min_cut, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_min_cut<<<1, 32, smem, S(stream)>>>(*b, k, verts, n, in_a, weight, in_smem);
+    if (in_smem) {
+        cudaFuncSetAttribute(k_min_cut<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_min_cut<true><<<1, 32, smem, S(stream)>>>(*b, k, verts, n, in_a, weight);
+    } else {
+        cudaFuncSetAttribute(k_min_cut<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_min_cut<false><<<1, 32, smem, S(stream)>>>(*b, k, verts, n, in_a, weight);
+    }
     PP_CHECK_LAUNCH("k_min_cut");
     return PP_OK;
 }

@@ -572,11 +572,12 @@ __global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
     double* B = ex_smem + j * j;     // [r'-1][r-1],   stride nr
     const int t = threadIdx.x;
     const bool allow = I.flags & PP_ALLOW_REPLICATION;
+    const int lane = t & 31;
     for (int e = t; e < j * j; e += blockDim.x) {   // A[r'-1][xi'-1] = W_j(l', xi', r')
         const int rp = 1 + e / j, xip = 1 + e % j;
         A[e] = W_structural(j, rp, xip, allow) ? Wsrc[e] : PP_INF;
     }
-    for (int e = t; e < j * nr; e += blockDim.x) {
+    for (int e = t; e < j * nr; e += blockDim.x) {   // B[r'-1][r-1] = chan(l', r', r, j + r)
         const int rp = 1 + e / nr, r = 1 + e % nr;
         B[e] = Mp / ((double)(rp * r) * cross[cross_idx(V, j + r, r, rp)]);
     }
@@ -586,7 +587,7 @@ __global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
     // fold interleaved r' subsets and min-reduce with shuffles
     int ks = 1;
     while (ks < 8 && ntiles * ks * 2 <= (int)blockDim.x) ks *= 2;
-    const int sub = t % ks, lane = t & 31;
+    const int sub = t % ks;
     const unsigned gmask = (ks == 32 ? 0xffffffffu : ((1u << ks) - 1u)) << (lane & ~(ks - 1));
     double* X = ws + lay.X;
     for (int id = t / ks; id < ntiles; id += blockDim.x / ks) {
@@ -923,8 +924,8 @@ __global__ void __launch_bounds__(32) k_query(pp_batch b, int n, const int* qi, 
 // (ordering.py:66) is a __reduce_min_sync over the tied local indices.
 // ----------------------------------------------------------------------------
 template <int SLOTS>
-__device__ double warp_min_cut_t(double* wl, const double* bw, int V, const int* mem, int n,
-                                 unsigned char* side_out) {
+__device__ __forceinline__ double warp_min_cut_t(double* wl, const double* bw, int V, const int* mem, int n,
+                                                 unsigned char* side_out) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     for (int e = lane; e < n * n; e += 32) {
@@ -958,6 +959,7 @@ __device__ double warp_min_cut_t(double* wl, const double* bw, int V, const int*
                 const unsigned long long u = (unsigned long long)__double_as_longlong(adj[s]);
                 if (inadj[s] && u > bu) { bu = u; bk = lane + 32 * s; }
             }
+            // (ties are the common case on structured clusters: three REDUX beat ballot fast paths)
             const unsigned hi = (unsigned)(bu >> 32), lo = (unsigned)bu;
             const unsigned mhi = __reduce_max_sync(FULL, hi);
             const unsigned mlo = __reduce_max_sync(FULL, hi == mhi ? lo : 0u);
@@ -1006,7 +1008,8 @@ __device__ double warp_min_cut_t(double* wl, const double* bw, int V, const int*
     return best_weight;
 }
 
-__device__ double warp_min_cut(double* wl, const double* bw, int V, const int* mem, int n, unsigned char* side) {
+__device__ __forceinline__ double warp_min_cut(double* wl, const double* bw, int V, const int* mem, int n,
+                                               unsigned char* side) {
     if (n <= 32) return warp_min_cut_t<1>(wl, bw, V, mem, n, side);
     if (n <= 64) return warp_min_cut_t<2>(wl, bw, V, mem, n, side);
     if (n <= 128) return warp_min_cut_t<4>(wl, bw, V, mem, n, side);
@@ -1014,14 +1017,17 @@ __device__ double warp_min_cut(double* wl, const double* bw, int V, const int* m
     return warp_min_cut_t<16>(wl, bw, V, mem, n, side);
 }
 
-__global__ void __launch_bounds__(32 * RDO_WARPS) k_rdo(pp_batch b, int w_in_smem) {
+// SMEM: the contracted weights live in shared memory (V <= 128); a template
+// parameter so the compiler sees the address space and emits LDS/STS.
+template <bool SMEM>
+__global__ void __launch_bounds__(32 * RDO_WARPS) k_rdo(pp_batch b) {
     const pp_instance I = b.inst[blockIdx.x];
     if (I.flags & PP_GIVEN_ORDER) return;
     const int V = I.V;
     extern __shared__ double smem_d[];
     char* sm = (char*)smem_d;
     double* W;
-    if (w_in_smem) { W = (double*)sm; sm += sizeof(double) * V * V; }
+    if constexpr (SMEM) { W = smem_d; sm += sizeof(double) * V * V; }
     else W = b.ws + I.ws_off + ws_layout(I.L, V).rdo_w;
     int* lo = (int*)sm;      sm += sizeof(int) * V;
     int* cnt = (int*)sm;     sm += sizeof(int) * V;
@@ -1082,14 +1088,15 @@ __global__ void __launch_bounds__(32 * RDO_WARPS) k_rdo(pp_batch b, int w_in_sme
 }
 
 // global_min_cut on a vertex subset (ordering.py:30-91): one warp.
+template <bool SMEM>
 __global__ void __launch_bounds__(32) k_min_cut(pp_batch b, int k, const int* verts, int n, unsigned char* in_a,
-                                                double* weight, int w_in_smem) {
+                                                double* weight) {
     const pp_instance I = b.inst[k];
     const int V = I.V;
     extern __shared__ double smem_d[];
     char* sm = (char*)smem_d;
     double* W;
-    if (w_in_smem) { W = (double*)sm; sm += sizeof(double) * V * V; }
+    if constexpr (SMEM) { W = smem_d; sm += sizeof(double) * V * V; }
     else W = b.ws + I.ws_off + ws_layout(I.L, V).rdo_w;
     int* mem = (int*)sm;
     for (int q = threadIdx.x; q < n; q += 32) mem[q] = verts[q];
@@ -1097,5 +1104,9 @@ __global__ void __launch_bounds__(32) k_min_cut(pp_batch b, int k, const int* ve
     const double cw = warp_min_cut(W, b.bw + I.bw_off, V, mem, n, in_a);
     if (threadIdx.x == 0) weight[0] = cw;
 }
+template __global__ void k_rdo<true>(pp_batch);
+template __global__ void k_rdo<false>(pp_batch);
+template __global__ void k_min_cut<true>(pp_batch, int, const int*, int, unsigned char*, double*);
+template __global__ void k_min_cut<false>(pp_batch, int, const int*, int, unsigned char*, double*);
 
 }  // namespace pp
