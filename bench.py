@@ -342,8 +342,9 @@ def _oracle_instances(specs):
 
 
 def host_threads(req=0):
+    """All host threads, capped at 64 (each C3 oracle DP holds a 0.33 GB dense table)."""
     n = len(os.sched_getaffinity(0))
-    return max(1, min(req or n, n))
+    return max(1, min(req or n, n, 64))
 
 
 def cpu_baseline(specs, threads=0):

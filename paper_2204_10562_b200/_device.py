@@ -52,18 +52,51 @@ def pack(profile, cluster) -> Packed:
         efwd[:L - 1] = [e.fwd_bytes for e in profile.edges]
         ebwd[:L - 1] = [e.bwd_bytes for e in profile.edges]
     ids = tuple(sorted(cluster.gpu_ids))
-    pos = {g: k for k, g in enumerate(ids)}
     V = len(ids)
     bw = np.zeros((V, V))
-    for (a, b), w in cluster.bandwidth.items():
-        pa, pb = pos[a], pos[b]
-        bw[pa, pb] = w
-        bw[pb, pa] = w
+    items = cluster.bandwidth
+    if items:
+        sid = np.array(ids)
+        keys = np.array(list(items.keys()))
+        vals = np.fromiter(items.values(), dtype=np.float64, count=len(items))
+        ia, ib = np.searchsorted(sid, keys[:, 0]), np.searchsorted(sid, keys[:, 1])
+        bw[ia, ib] = vals
+        bw[ib, ia] = vals
     return Packed(ids, fwd, bwd, par, efwd, ebwd, bw)
 
 
 def _stream():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class _Staging:
+    """Reusable pinned host buffers for the H2D copies (one per dtype).  Before
+    a buffer is refilled, the event recorded after its previous copy is waited
+    on, so an in-flight non_blocking copy is never overwritten."""
+
+    def __init__(self):
+        self.buf = {}
+        self.evt = {}
+
+    def to_device(self, arr: np.ndarray, dev):
+        key = arr.dtype.str
+        n = arr.size
+        buf = self.buf.get(key)
+        if key in self.evt:
+            self.evt[key].synchronize()
+        if buf is None or buf.numel() < n:
+            buf = torch.empty(max(n, 1 << 16), dtype=torch.from_numpy(arr[:0]).dtype).pin_memory()
+            self.buf[key] = buf
+        view = buf[:n]
+        view.numpy()[:] = arr.reshape(-1)
+        out = view.to(dev, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.evt[key] = ev
+        return out
+
+
+_staging = _Staging()
 
 
 def device():
@@ -112,8 +145,8 @@ class DeviceBatch:
         self.max_L = int(Ls.max())
         self.max_V = int(Vs.max())
         # ---- device allocations
-        self.d_fin = torch.from_numpy(fin).pin_memory().to(dev, non_blocking=True)
-        self.d_iin = torch.from_numpy(iin).pin_memory().to(dev, non_blocking=True)
+        self.d_fin = _staging.to_device(fin, dev)
+        self.d_iin = _staging.to_device(iin, dev)
         # outputs: fp64 [sweep_w | sweep_mk | sweep_bound | best_mk | phi | ar_s | ar_e | ev_s | ev_e]
         ev = n_ev if capture_events else 0
         self.f_off = np.cumsum([0, n_sweep, n_sweep, n_sweep, n, n, n_ar, n_ar, ev, ev])
@@ -259,7 +292,7 @@ class SimRun:
                 np.array(devs if devs else [0], np.int32), np.array(qoff, np.int32),
                 np.array(qitems if qitems else [0, 0], np.int32)]
         offs = np.cumsum([0] + [a.size for a in ints])
-        d_in = torch.from_numpy(np.concatenate(ints)).pin_memory().to(dev, non_blocking=True)
+        d_in = _staging.to_device(np.concatenate(ints), dev)
         # fp64 outputs: makespan | bound | ar_s | ar_e | ev_s | ev_e | scratch
         evn = ev if capture_events else 0
         self.f_off = np.cumsum([0, n, n, ar, ar, evn, evn, ev])

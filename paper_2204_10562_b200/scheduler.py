@@ -7,14 +7,15 @@ and stall detection.  build_block_list / compute_execution_order build the
 reference's Python structures from their closed forms.
 """
 
+import functools
 from dataclasses import dataclass
 from typing import Dict, List, Sequence, Tuple
 
 import numpy as np
 
 from . import _device, _lib
-from .model import (BWD, COMM_BWD, COMM_FWD, FWD, FWDBWD, AllReduceWindow, Block, ClusterGraph, ModelProfile,
-                    Plan, Schedule, ScheduleEvent, ValidationError, check_numeric_range)
+from .model import (BWD, COMM_BWD, COMM_FWD, FWD, FWDBWD, AllReduceWindow, Block, ClusterGraph, LazyEvents,
+                    ModelProfile, Plan, Schedule, ValidationError, check_numeric_range)
 from .partition import sum_flags
 
 
@@ -108,6 +109,7 @@ def _pos_lane(N: int, pos: int) -> int:
     return 2 * n - 1 if q % 2 else 2 * n - 2
 
 
+@functools.lru_cache(maxsize=1024)
 def _labels(N: int):
     """position -> (resource, label, resource sort key) (model.py:148-158, scheduler.py:115-118)."""
     res, lab, key = [None] * (4 * N - 2), [None] * (4 * N - 2), np.zeros(4 * N - 2, dtype=np.int64)
@@ -116,6 +118,18 @@ def _labels(N: int):
         lab[b.position] = b.label
         key[b.position] = (b.stage if b.is_compute else (1 << 20) + b.channel)
     return res, lab, key
+
+
+@functools.lru_cache(maxsize=256)
+def _pe_tiebreak_order(N: int, M: int):
+    """Permutation of the (m, pos) grid sorted by (resource key, microbatch, position): a
+    stable sort by start time on top of it yields the reference's event order."""
+    J = 4 * N - 3
+    _, _, key = _labels(N)
+    m = np.repeat(np.arange(1, M + 1), J)
+    p = np.tile(np.arange(1, J + 1), M)
+    order = np.lexsort((p, m, key[p]))
+    return order, m[order], p[order]
 
 
 def _check_plan(plan: Plan, profile: ModelProfile, cluster: ClusterGraph) -> None:
@@ -164,13 +178,18 @@ def _build_schedule(plan: Plan, rec, tiebreak=None) -> Schedule:
     res, lab, key = _labels(N)
     start = rec["ev_start"]
     end = rec["ev_end"]
-    m = np.repeat(np.arange(1, M + 1), J)
-    p = np.tile(np.arange(1, J + 1), M)
-    tb = p if tiebreak is None else tiebreak
     # stable order of the reference: (start, resource key, microbatch), ties in queue order
-    idx = np.lexsort((tb, m, key[p], start))
-    st, en, mm, pp = start[idx].tolist(), end[idx].tolist(), m[idx].tolist(), p[idx].tolist()
-    events = tuple(ScheduleEvent(res[q], a, lab[q], s, e) for s, e, a, q in zip(st, en, mm, pp))
+    if tiebreak is None:
+        # PE queues: same-resource, same-microbatch ties are in position order
+        order, mo, po = _pe_tiebreak_order(N, M)
+        so = start[order]
+        k = np.argsort(so, kind="stable")
+        events = LazyEvents(res, lab, mo[k], po[k], so[k], end[order][k])
+    else:
+        m = np.repeat(np.arange(1, M + 1), J)
+        p = np.tile(np.arange(1, J + 1), M)
+        idx = np.lexsort((tiebreak, m, key[p], start))
+        events = LazyEvents(res, lab, m[idx], p[idx], start[idx], end[idx])
     windows = tuple(AllReduceWindow(stage=s.index, start=float(rec["ar_start"][s.index - 1]),
                                     end=float(rec["ar_end"][s.index - 1]))
                     for s in plan.stages if s.replicated)
