@@ -105,8 +105,52 @@ int pp_rdo(const pp_batch* b, void* stream) {
     return PP_OK;
 }
 
+static int prm_chain(const pp_batch* b, void* stream);
+
+// The wavefront is a chain of ~2V dependent launches whose last wave is
+// partly empty.  Instance groups run their chains on separate streams so one
+// group's tail overlaps another group's kernels (fork/join with events on the
+// caller's stream; the side streams are created once per host thread+device).
+static constexpr int PP_DP_STREAMS = 4;
+struct SideStreams {
+    int dev = -1;
+    cudaStream_t s[PP_DP_STREAMS];
+    cudaEvent_t fork, join[PP_DP_STREAMS];
+};
+static thread_local SideStreams g_side;
+
 int pp_prm(const pp_batch* b, void* stream) {
     if (b->n_inst <= 0) return PP_OK;
+    const int G = b->n_inst < PP_DP_STREAMS ? b->n_inst : PP_DP_STREAMS;
+    if (G <= 1) return prm_chain(b, stream);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (g_side.dev != dev) {
+        for (int g = 0; g < PP_DP_STREAMS; ++g) {
+            if (cudaStreamCreateWithFlags(&g_side.s[g], cudaStreamNonBlocking) != cudaSuccess ||
+                cudaEventCreateWithFlags(&g_side.join[g], cudaEventDisableTiming) != cudaSuccess)
+                return fail(PP_ECUDA, "side stream creation: %s", cudaGetErrorString(cudaGetLastError()));
+        }
+        if (cudaEventCreateWithFlags(&g_side.fork, cudaEventDisableTiming) != cudaSuccess)
+            return fail(PP_ECUDA, "event creation: %s", cudaGetErrorString(cudaGetLastError()));
+        g_side.dev = dev;
+    }
+    cudaEventRecord(g_side.fork, S(stream));
+    for (int g = 0; g < G; ++g) {
+        const int lo = (int)((int64_t)g * b->n_inst / G), hi = (int)((int64_t)(g + 1) * b->n_inst / G);
+        pp_batch bg = *b;
+        bg.inst = b->inst + lo;
+        bg.n_inst = hi - lo;
+        cudaStreamWaitEvent(g_side.s[g], g_side.fork, 0);
+        const int rc = prm_chain(&bg, g_side.s[g]);
+        if (rc) return rc;
+        cudaEventRecord(g_side.join[g], g_side.s[g]);
+        cudaStreamWaitEvent(S(stream), g_side.join[g], 0);
+    }
+    return PP_OK;
+}
+
+static int prm_chain(const pp_batch* b, void* stream) {
     const int maxL = b->max_L, maxV = b->max_V;
     dim3 gp(b->n_inst, maxL > maxV ? maxL : maxV);
     k_prep<<<gp, 128, 0, S(stream)>>>(*b);
