@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--profile-steps", type=int, default=0, help="(for ncu) run N untimed steps and exit")
+    ap.add_argument("--workload", default="c3", choices=["c3", "c4", "c5"],
+                    help="c3 = the headline (BASELINE.json metric); c4/c5 = secondary configs, 1 GPU")
     return ap.parse_args()
 
 
@@ -395,10 +397,87 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_secondary(args):
+    """Secondary configs (single GPU, not the driver's headline):
+    c4 — 4096 random 32-layer profiles x random 16-GPU cliques, M = 32: spp instances/s;
+    c5 — 256 candidate plans (xi = 1..256, even split on the RDO order) of a 1024-layer
+         chain on a 256-GPU clique, M = 512: simulated block executions/s (RDO excluded,
+         as in SURVEY.md §8d)."""
+    import numpy as np
+    import torch
+    from paper_2204_10562_b200 import _device, _lib, rdo
+    from paper_2204_10562_b200 import workloads as W
+    from paper_2204_10562_b200.partition import sum_flags
+    torch.cuda.set_device(0)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def timed(fn):
+        for _ in range(max(args.warmup, 3)):
+            fn()
+        torch.cuda.synchronize()
+        ms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+            a.record(stream); fn(); b.record(stream)
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+        return ms
+
+    O, _ = _oracle_instances([])
+    if args.workload == "c4":
+        specs = W.c4_batch(4096)
+        models = [s.to_model() for s in specs]
+        items = [(_device.pack(p, c), M, _lib.PP_ALLOW_REPLICATION | sum_flags(), None) for p, c, M in models]
+        db = _device.DeviceBatch(items, capture_events=True)
+        ms = timed(lambda: db.run("spp"))
+        value = len(specs) * len(ms) / (sum(ms) / 1e3)
+        _, sample = _oracle_instances(specs[:64])
+        nt = host_threads(args.cpu_threads)
+        t0 = time.perf_counter(); O.spp_batch(sample, nt); dt = time.perf_counter() - t0
+        line = {"metric": "C4 batched planning throughput", "value": value, "unit": "instances/s",
+                "ms_per_step": sum(ms) / len(ms), "steps": args.steps, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "c4_4096x(L32,V16,M32)"},
+                "roofline": {"bound": "fp64_minmax", "algorithmic_ops_per_step": 2 * 4096 * t_fact(32, 16)},
+                "cpu_baseline": {"value": len(sample) / dt, "unit": "instances/s", "cores": nt, "kind": "port",
+                                 "sample": f"64 C4 instances on {nt} threads, {dt:.1f} s"}}
+    else:
+        spec = W.c5_instance()
+        profile, cluster, M = spec.to_model()
+        order = rdo(cluster).order
+        ids = sorted(spec.gpu_ids)
+        pos = {g: k for k, g in enumerate(ids)}
+        packed = _device.pack(profile, cluster)
+        db = _device.DeviceBatch([(packed, M, sum_flags(), None)], capture_events=False)
+        sps = [_device.SimPlan(inst=0, M=M, stages=[(a, b, [pos[g] for g in d]) for a, b, d in
+                                                    W.even_split_plan(spec.L, order, xi)],
+                               flags=_lib.PP_SIM_PE_ORDER) for xi in range(1, 257)]
+        ms = timed(lambda: _device.SimRun(db, sps, capture_events=False))
+        execs = sum(M * (4 * xi - 3) for xi in range(1, 257))
+        value = execs * len(ms) / (sum(ms) / 1e3)
+        _, (oi,) = _oracle_instances([spec])
+        nt = host_threads(args.cpu_threads)
+        oplans = [O.Plan([(a, b, tuple(pos[g] for g in d)) for a, b, d in W.even_split_plan(spec.L, order, xi)], M)
+                  for xi in range(1, 257, 8)]
+        t0 = time.perf_counter(); O.simulate_pe_batch(oi, oplans, nt); dt = time.perf_counter() - t0
+        cexec = sum(M * (4 * xi - 3) for xi in range(1, 257, 8))
+        line = {"metric": "C5 candidate-plan simulation throughput", "value": value,
+                "unit": "block executions/s", "ms_per_step": sum(ms) / len(ms), "steps": args.steps,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "c5_256plans_1024layers_256gpus_M512", "block_executions_per_step": execs,
+                           "note": "includes plan upload (SimRun) per step; RDO excluded"},
+                "cpu_baseline": {"value": cexec / dt, "unit": "block executions/s", "cores": nt, "kind": "port",
+                                 "sample": f"32 of the 256 plans (every 8th xi) on {nt} threads, {dt:.1f} s"}}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload != "c3":
+        run_secondary(args)
     else:
         run_ours(args)
 

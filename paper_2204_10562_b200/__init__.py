@@ -14,7 +14,7 @@ from .ordering import DeviceOrdering, global_min_cut, rdo
 from .partition import PartitionSolver, PrmResult, best_partition, prm
 from .planner import BoundReport, SppResult, SweepEntry, bound_factor, phi, spp, spp_many, theorem1_report
 from .scheduler import (ExecutionOrder, SchedulingError, build_block_list, compute_execution_order, lemma1_bound,
-                        simulate_pe, simulate_with_order)
+                        simulate_pe, simulate_pe_many, simulate_with_order)
 
 __version__ = "0.1.0"
 
@@ -24,6 +24,6 @@ __all__ = [
     "ScheduleEvent", "SchedulingError", "SppResult", "Stage", "SweepEntry", "ValidationError",
     "best_partition", "bound_factor", "build_block_list", "check_numeric_range", "compute_execution_order",
     "global_min_cut", "lemma1_bound", "make_cluster", "phi", "plan_uses_all_gpus", "prm", "rdo",
-    "simulate_pe", "simulate_with_order", "spp", "spp_many", "theorem1_report", "validate_cluster",
+    "simulate_pe", "simulate_pe_many", "simulate_with_order", "spp", "spp_many", "theorem1_report", "validate_cluster",
     "validate_plan", "validate_profile",
 ]

@@ -293,9 +293,10 @@ class SimRun:
                 np.array(qitems if qitems else [0, 0], np.int32)]
         offs = np.cumsum([0] + [a.size for a in ints])
         d_in = _staging.to_device(np.concatenate(ints), dev)
-        # fp64 outputs: makespan | bound | ar_s | ar_e | ev_s | ev_e | scratch
+        # fp64 outputs: makespan | bound | ar_s | ar_e | ev_s | ev_e | scratch (generic queues only)
         evn = ev if capture_events else 0
-        self.f_off = np.cumsum([0, n, n, ar, ar, evn, evn, ev])
+        scr = ev if any(sp.queues is not None for sp in plans) else 1
+        self.f_off = np.cumsum([0, n, n, ar, ar, evn, evn, scr])
         self.d_f = torch.empty(int(self.f_off[-1]), dtype=F64, device=dev)
         self.i_off = np.cumsum([0, n, lane])
         self.d_i = torch.empty(int(self.i_off[-1]), dtype=I32, device=dev)

@@ -239,6 +239,23 @@ def simulate_pe(plan: Plan, profile: ModelProfile, cluster: ClusterGraph) -> Sch
     return _build_schedule(plan, _sim(plan, profile, cluster))
 
 
+def simulate_pe_many(plans: Sequence[Plan], profile: ModelProfile, cluster: ClusterGraph):
+    """[(makespan, lemma1_bound)] of simulate_pe for many plans of one instance in ONE launch
+    (one CTA per plan; the C5 candidate sweep).  Schedules are not materialised."""
+    check_numeric_range(profile, cluster)
+    for p in plans:
+        _check_plan(p, profile, cluster)
+    packed = _device.pack(profile, cluster)
+    pos = {g: k for k, g in enumerate(packed.ids)}
+    db = _device.DeviceBatch([(packed, max(p.microbatch_count for p in plans), sum_flags(), None)],
+                             capture_events=False)
+    sps = [_device.SimPlan(inst=0, M=p.microbatch_count,
+                           stages=[(s.layer_start, s.layer_end, [pos[d] for d in s.devices]) for s in p.stages],
+                           flags=_lib.PP_SIM_PE_ORDER) for p in plans]
+    run = _device.SimRun(db, sps, capture_events=False)
+    return [(r["makespan"], r["bound"]) for r in run.fetch()]
+
+
 def lemma1_bound(plan: Plan, profile: ModelProfile, cluster: ClusterGraph) -> float:
     """(M + 4N - 4) * C + max AllReduce (scheduler.py:234-238), computed on the GPU."""
     return _sim(plan, profile, cluster, capture=False)["bound"]

@@ -1,0 +1,75 @@
+"""GPU parity at the BASELINE.json config sizes beyond C3 (C4 batch, C5 simulation).
+
+Bit-exact against the C oracle on samples, plus size-independent properties
+on the full batches.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import block_labels
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2204_10562_b200")
+from paper_2204_10562_b200 import workloads as W  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def _oinst(spec):
+    ids = sorted(spec.gpu_ids)
+    pos = {g: k for k, g in enumerate(ids)}
+    bw = np.zeros((len(ids), len(ids)))
+    for a, b, w in spec.links:
+        bw[pos[a], pos[b]] = bw[pos[b], pos[a]] = w
+    return O.Instance(spec.fwd, spec.bwd, spec.param, spec.efwd, spec.ebwd, bw, spec.M), ids
+
+
+def test_c4_full_batch_sampled_vs_oracle():
+    specs = W.c4_batch(4096)
+    res = P.spp_many([s.to_model() for s in specs])
+    assert len(res) == 4096
+    for r in res:   # properties on every instance
+        feas = [e for e in r.sweep if e.feasible]
+        assert r.makespan == min(e.makespan for e in feas)
+        assert all(e.makespan <= e.bound * (1 + 1e-9) for e in feas)
+        assert sorted(r.device_order) == list(range(1, 17))
+        assert len(r.schedule.events) == r.plan.microbatch_count * (4 * r.plan.num_stages - 3)
+    for k in range(0, 4096, 64):   # 64 instances bit-exact vs the oracle
+        inst, ids = _oinst(specs[k])
+        want = O.spp(inst)
+        r = res[k]
+        assert list(r.device_order) == [ids[x] for x in want["order"]]
+        assert [(e.stage_count, e.feasible, e.workload, e.makespan, e.bound) for e in r.sweep] == want["sweep"]
+        assert r.makespan == want["makespan"]
+        bl = block_labels(r.plan.num_stages)
+        assert [(e.microbatch, e.block, e.start, e.end) for e in r.schedule.events] == \
+            [(m, bl[p][1], s, e) for m, p, s, e in want["events"]]
+
+
+def test_c5_candidate_simulation_vs_oracle():
+    spec = W.c5_instance()
+    profile, cluster, M = spec.to_model()
+    order = P.rdo(cluster).order
+    inst, ids = _oinst(spec)
+    assert [ids[x] for x in O.rdo(inst)] == list(order)
+    plans, oplans = [], []
+    pos = {g: k for k, g in enumerate(ids)}
+    for xi in range(1, 257):
+        st = W.even_split_plan(spec.L, order, xi)
+        plans.append(P.Plan(tuple(P.Stage(n + 1, a, b, d) for n, (a, b, d) in enumerate(st)), M))
+        oplans.append(O.Plan([(a, b, tuple(pos[g] for g in d)) for a, b, d in st], M))
+    got = P.simulate_pe_many(plans, profile, cluster)
+    want = O.simulate_pe_batch(inst, oplans, 16)
+    assert [m for m, _ in got] == list(want)
+    best = min(range(256), key=lambda k: (got[k][0], k))
+    assert best + 1 == min(range(256), key=lambda k: (want[k], k)) + 1
+    for k in (0, 59, 255):
+        assert got[k][1] == O.lemma1_bound(inst, oplans[k])
