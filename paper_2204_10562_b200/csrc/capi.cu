@@ -2,6 +2,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -52,6 +53,25 @@ static int fail(int code, const char* fmt, ...) {
     } while (0)
 
 static inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// Upper bound on the per-item CTA split of k_combine_s (PP_COMBINE_SPLIT env, default 1).
+static int read_max_parts() {
+    const char* e = getenv("PP_COMBINE_SPLIT");
+    const int v = e ? atoi(e) : 1;
+    return v < 1 ? 1 : (v > 8 ? 8 : v);
+}
+static const int g_max_parts = read_max_parts();
+
+static int num_sms() {
+    static thread_local int dev = -1, sms = 148;
+    int d = 0;
+    cudaGetDevice(&d);
+    if (d != dev) {
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+        dev = d;
+    }
+    return sms;
+}
 static inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
 
 extern "C" {
@@ -181,7 +201,11 @@ static int prm_chain(const pp_batch* b, void* stream) {
                 k_expand_s<<<ge, 128, sizeof(double) * (size_t)j * maxV, S(stream)>>>(*b, j);
                 PP_CHECK_LAUNCH("k_expand_s");
             }
-            dim3 gc(b->n_inst, maxV - j);
+            // split every item over `parts` CTAs so a launch fills ~2 waves of the SMs
+            const int items = b->n_inst * (maxV - j);
+            int parts = (2 * num_sms() + items - 1) / items;
+            parts = parts < 1 ? 1 : (parts > g_max_parts ? g_max_parts : parts);
+            dim3 gc(b->n_inst, maxV - j, parts);
             const size_t sm = sizeof(double) * ((maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 +
                                                 (size_t)(maxL > 1 ? maxL - 1 : 0) * j);
             k_combine_s<<<gc, 256, sm, S(stream)>>>(*b, j);

@@ -698,21 +698,28 @@ __device__ __forceinline__ void combine_tiles_s(double* Wi, int i, int r, int L,
     constexpr int TL = 16 / TX;
     const int t = threadIdx.x;
     const int ntl = (L + TL - 1) / TL, ntx = (j + TX - 1) / TX, ntiles = ntl * ntx;
-    // order tiles by trip count (descending) so each warp's lanes run equal-length loops
+    // the item is split over gridDim.z CTAs: CTA `part` owns the tiles with id = part (mod nparts)
+    const int part = blockIdx.z, nparts = gridDim.z;
+    const int nmine = ntiles > part ? (ntiles - part + nparts - 1) / nparts : 0;
+    // order its tiles by trip count (descending) so each warp's lanes run equal-length loops
     for (int k = t; k < L + 2; k += blockDim.x) hist[k] = 0;
     __syncthreads();
-    for (int id = t; id < ntiles; id += blockDim.x)
+    for (int k = t; k < nmine; k += blockDim.x) {
+        const int id = part + k * nparts;
         atomicAdd(&hist[L - tile_nfast<TX>(L, 1 + TL * (id / ntx), 2 + TX * (id % ntx))], 1);
+    }
     __syncthreads();
     if (t == 0) {
         int o = 0;
         for (int k = 0; k < L + 2; ++k) { const int c = hist[k]; hist[k] = o; o += c; }
     }
     __syncthreads();
-    for (int id = t; id < ntiles; id += blockDim.x)
+    for (int k = t; k < nmine; k += blockDim.x) {
+        const int id = part + k * nparts;
         order[atomicAdd(&hist[L - tile_nfast<TX>(L, 1 + TL * (id / ntx), 2 + TX * (id % ntx))], 1)] = id;
+    }
     __syncthreads();
-    for (int q = t; q < ntiles; q += blockDim.x) {
+    for (int q = t; q < nmine; q += blockDim.x) {
         const int id = order[q];
         const int l0 = 1 + TL * (id / ntx), xi0 = 2 + TX * (id % ntx);
         double acc[TL][TX];
@@ -751,31 +758,18 @@ __global__ void __launch_bounds__(256, 2) k_combine_s(pp_batch b, int j) {
         int o = 0;
         for (int lp = 1; lp < L; ++lp) { trio[lp] = o; o += L - lp; }
     }
-    // X(., ., r, i): rows l' = 1..L-1, one contiguous copy (4 loads in flight per thread)
-    const double* Xg = ws + lay.X + X_base(L, i, r);
+    // stage X(., ., r, i) (rows l' = 1..L-1, contiguous) and the item's stage-term
+    // triangle (its k_stab slot) with cp.async: every copy of the CTA is in flight at once
     {
-        const int n = (L - 1) * j;
-        for (int e0 = t; e0 < n; e0 += 4 * 256) {
-            double v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) { const int e = e0 + 256 * u; v[u] = (e < n) ? Xg[e] : 0.0; }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) { const int e = e0 + 256 * u; if (e < n) Xs[e] = v[u]; }
-        }
-    }
-    __syncthreads();
-    // stage terms S(l', l) of this item: the shared triangle of its slot (k_stab)
-    {
+        const double* Xg = ws + lay.X + X_base(L, i, r);
+        const int nx = (L - 1) * j;
+        for (int e = t; e < nx; e += blockDim.x) cp_async8(Xs + e, Xg + e);
         const int slot = reinterpret_cast<const int*>(ws + lay.sidx)[(r - 1) * V + (i - 1)];
-        const int n = (L - 1) * L / 2;
-        const double* Sg = ws + lay.Stab + (int64_t)slot * n;
-        for (int e0 = t; e0 < n; e0 += 4 * 256) {
-            double v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) { const int e = e0 + 256 * u; v[u] = (e < n) ? Sg[e] : 0.0; }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) { const int e = e0 + 256 * u; if (e < n) Stri[e] = v[u]; }
-        }
+        const int ns = (L - 1) * L / 2;
+        const double* Sg = ws + lay.Stab + (int64_t)slot * ns;
+        for (int e = t; e < ns; e += blockDim.x) cp_async8(Stri + e, Sg + e);
+        cp_async_commit();
+        cp_async_wait<0>();
     }
     __syncthreads();
     if (j >= 4) combine_tiles_s<4>(Wi, i, r, L, j, Stri, trio, Xs, s_hist, s_order);
