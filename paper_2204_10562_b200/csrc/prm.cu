@@ -636,6 +636,10 @@ __global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
 // combine, step j: one CTA per (instance, r), target i = j + r.  smem: the
 // stage terms of the item as a packed triangle (row l' holds l = l'+1..L,
 // S = T1 + sync, T1 from k_base) and X(., ., r, i) (rows l' = 1..L-1, stride j).
+// combine reads stage terms straight from global memory for j <= this (0 = always
+// stage them in shared memory; j <= 8 measured no better on B200)
+constexpr int S_DIRECT_J = 0;
+
 template <int TX>
 __device__ __forceinline__ int tile_nfast(int L, int l0, int xi0) {
     constexpr int TL = 16 / TX;
@@ -760,21 +764,31 @@ __global__ void __launch_bounds__(256, 2) k_combine_s(pp_batch b, int j) {
     }
     // stage X(., ., r, i) (rows l' = 1..L-1, contiguous) and the item's stage-term
     // triangle (its k_stab slot) with cp.async: every copy of the CTA is in flight at once
+    const double* Sg;
     {
         const double* Xg = ws + lay.X + X_base(L, i, r);
         const int nx = (L - 1) * j;
         for (int e = t; e < nx; e += blockDim.x) cp_async8(Xs + e, Xg + e);
         const int slot = reinterpret_cast<const int*>(ws + lay.sidx)[(r - 1) * V + (i - 1)];
         const int ns = (L - 1) * L / 2;
-        const double* Sg = ws + lay.Stab + (int64_t)slot * ns;
-        for (int e = t; e < ns; e += blockDim.x) cp_async8(Stri + e, Sg + e);
+        Sg = ws + lay.Stab + (int64_t)slot * ns;
+        // each stage term is used by j columns: for small j reading it from L2/L1
+        // once beats copying the whole triangle into shared memory first
+        if (j > S_DIRECT_J)
+            for (int e = t; e < ns; e += blockDim.x) cp_async8(Stri + e, Sg + e);
         cp_async_commit();
         cp_async_wait<0>();
     }
     __syncthreads();
-    if (j >= 4) combine_tiles_s<4>(Wi, i, r, L, j, Stri, trio, Xs, s_hist, s_order);
-    else if (j >= 2) combine_tiles_s<2>(Wi, i, r, L, j, Stri, trio, Xs, s_hist, s_order);
-    else combine_tiles_s<1>(Wi, i, r, L, j, Stri, trio, Xs, s_hist, s_order);
+    if (j > S_DIRECT_J) {
+        if (j >= 4) combine_tiles_s<4>(Wi, i, r, L, j, Stri, trio, Xs, s_hist, s_order);
+        else if (j >= 2) combine_tiles_s<2>(Wi, i, r, L, j, Stri, trio, Xs, s_hist, s_order);
+        else combine_tiles_s<1>(Wi, i, r, L, j, Stri, trio, Xs, s_hist, s_order);
+    } else {
+        if (j >= 4) combine_tiles_s<4>(Wi, i, r, L, j, Sg, trio, Xs, s_hist, s_order);
+        else if (j >= 2) combine_tiles_s<2>(Wi, i, r, L, j, Sg, trio, Xs, s_hist, s_order);
+        else combine_tiles_s<1>(Wi, i, r, L, j, Sg, trio, Xs, s_hist, s_order);
+    }
 }
 
 // ----------------------------------------------------------------------------
