@@ -54,10 +54,11 @@ static int fail(int code, const char* fmt, ...) {
 
 static inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
-// Upper bound on the per-item CTA split of k_combine_s (PP_COMBINE_SPLIT env, default 1).
+// Upper bound on the per-item CTA split of k_combine_s (PP_COMBINE_SPLIT env, default 8):
+// items are split only while the whole step has fewer items than SMs.
 static int read_max_parts() {
     const char* e = getenv("PP_COMBINE_SPLIT");
-    const int v = e ? atoi(e) : 1;
+    const int v = e ? atoi(e) : 8;
     return v < 1 ? 1 : (v > 8 ? 8 : v);
 }
 static const int g_max_parts = read_max_parts();
@@ -125,7 +126,7 @@ int pp_rdo(const pp_batch* b, void* stream) {
     return PP_OK;
 }
 
-static int prm_chain(const pp_batch* b, void* stream);
+static int prm_chain(const pp_batch* b, void* stream, int total_inst);
 
 // The wavefront is a chain of ~2V dependent launches whose last wave is
 // partly empty.  Instance groups run their chains on separate streams so one
@@ -142,7 +143,7 @@ static thread_local SideStreams g_side;
 int pp_prm(const pp_batch* b, void* stream) {
     if (b->n_inst <= 0) return PP_OK;
     const int G = b->n_inst < PP_DP_STREAMS ? b->n_inst : PP_DP_STREAMS;
-    if (G <= 1) return prm_chain(b, stream);
+    if (G <= 1) return prm_chain(b, stream, b->n_inst);
     int dev = 0;
     cudaGetDevice(&dev);
     if (g_side.dev != dev) {
@@ -162,7 +163,7 @@ int pp_prm(const pp_batch* b, void* stream) {
         bg.inst = b->inst + lo;
         bg.n_inst = hi - lo;
         cudaStreamWaitEvent(g_side.s[g], g_side.fork, 0);
-        const int rc = prm_chain(&bg, g_side.s[g]);
+        const int rc = prm_chain(&bg, g_side.s[g], b->n_inst);
         if (rc) return rc;
         cudaEventRecord(g_side.join[g], g_side.s[g]);
         cudaStreamWaitEvent(S(stream), g_side.join[g], 0);
@@ -170,7 +171,7 @@ int pp_prm(const pp_batch* b, void* stream) {
     return PP_OK;
 }
 
-static int prm_chain(const pp_batch* b, void* stream) {
+static int prm_chain(const pp_batch* b, void* stream, int total_inst) {
     const int maxL = b->max_L, maxV = b->max_V;
     dim3 gp(b->n_inst, maxL > maxV ? maxL : maxV);
     k_prep<<<gp, 128, 0, S(stream)>>>(*b);
@@ -202,8 +203,9 @@ static int prm_chain(const pp_batch* b, void* stream) {
                 PP_CHECK_LAUNCH("k_expand_s");
             }
             // split every item over `parts` CTAs so a launch fills ~2 waves of the SMs
-            const int items = b->n_inst * (maxV - j);
-            int parts = (2 * num_sms() + items - 1) / items;
+            // (counted over the whole batch: the groups' launches run concurrently)
+            const int items = total_inst * (maxV - j);
+            int parts = (num_sms() + items - 1) / items;
             parts = parts < 1 ? 1 : (parts > g_max_parts ? g_max_parts : parts);
             dim3 gc(b->n_inst, maxV - j, parts);
             const size_t sm = sizeof(double) * ((maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 +
