@@ -111,3 +111,41 @@ def test_no_gpu_fails_loudly():
     prof, clu, M = W.c2_bert24().to_model()
     with pytest.raises(_lib.BackendUnavailable):
         P.spp(prof, clu, M)
+
+
+def test_cluster_validation_fast_and_slow_paths_agree():
+    good = P.make_cluster([3, 1, 2], [(1, 2, 1.0), (1, 3, 2.0), (2, 3, 3.0)])
+    assert P.validate_cluster(good) is good
+    # both orientations of a pair with equal values: legal in the reference (slow path)
+    both = P.ClusterGraph((1, 2), {(1, 2): 1.0, (2, 1): 1.0})
+    assert P.validate_cluster(both) is both
+    cases = [
+        (P.ClusterGraph((1, 2, 3), {(1, 2): 1.0, (1, 3): 1.0}), "missing pair"),
+        (P.ClusterGraph((1, 2), {(1, 2): 0.0}), "non-positive"),
+        (P.ClusterGraph((1, 2), {(1, 5): 1.0}), "unknown GPU"),
+        (P.ClusterGraph((1, 2), {(1, 1): 1.0}), "self-link"),
+        (P.ClusterGraph((1, 1), {}), "duplicate GPU id"),
+        (P.ClusterGraph((1, 2), {(1, 2): 1.0, (2, 1): 2.0}), "asymmetric"),
+    ]
+    for clu, msg in cases:
+        with pytest.raises(P.ValidationError, match=msg):
+            P.validate_cluster(clu)
+
+
+def test_lazy_events_behave_like_tuples():
+    from paper_2204_10562_b200.model import LazyEvents, ScheduleEvent
+    res = [None, "stage1", "chan1", "stage2"]
+    lab = [None, "fwd1", "comm_fwd1", "fwdbwd2"]
+    ev = LazyEvents(res, lab, np.array([1, 1, 2]), np.array([1, 2, 1]), np.array([0.0, 1.0, 1.0]),
+                    np.array([1.0, 2.0, 2.0]))
+    want = (ScheduleEvent("stage1", 1, "fwd1", 0.0, 1.0), ScheduleEvent("chan1", 1, "comm_fwd1", 1.0, 2.0),
+            ScheduleEvent("stage1", 2, "fwd1", 1.0, 2.0))
+    assert len(ev) == 3 and ev[1] == want[1] and ev[-1] == want[2] and ev[0:2] == want[0:2]
+    assert ev == want and want == ev and tuple(ev) == want and list(ev) == list(want)
+    assert hash(ev) == hash(want)
+    s1 = P.Schedule(events=ev, allreduce=(), makespan=2.0)
+    s2 = P.Schedule(events=want, allreduce=(), makespan=2.0)
+    assert s1 == s2
+    other = LazyEvents(res, lab, np.array([1, 1, 2]), np.array([1, 2, 1]), np.array([0.0, 1.0, 1.0]),
+                       np.array([1.0, 2.0, 2.5]))
+    assert other != ev
