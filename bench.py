@@ -149,11 +149,12 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2204_10562_b200 import _device, _lib, spp_many
+    from paper_2204_10562_b200 import workloads as W
     from paper_2204_10562_b200.partition import sum_flags
 
     dev = torch.device("cuda", local)
     specs = batch_specs(rank)
-    models = [s.to_model() for s in specs]
+    models = W.models_of(specs)   # one cluster object, two profile objects (as a user would)
     items = [(_device.pack(p, c), M, _lib.PP_ALLOW_REPLICATION | sum_flags(), None) for p, c, M in models]
     db = _device.DeviceBatch(items, capture_events=True)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2

@@ -49,18 +49,31 @@ def bound_factor(num_gpus: int, microbatch_count: int) -> float:
 
 
 def _items(instances):
-    items = []
-    packs = []
+    """Validate and pack every instance.  Within one call the same profile /
+    cluster OBJECT (e.g. one cluster planned for several models or M values)
+    is validated and packed once; objects are not cached across calls (their
+    bandwidth dict is mutable)."""
+    items, packs = [], []
+    seen_p, seen_c, seen_pc = {}, {}, {}
+    flags = _lib.PP_ALLOW_REPLICATION | sum_flags()
     for profile, cluster, M in instances:
-        validate_profile(profile)
-        validate_cluster(cluster)
-        check_numeric_range(profile, cluster)
+        if id(profile) not in seen_p:
+            validate_profile(profile)
+            seen_p[id(profile)] = profile
+        if id(cluster) not in seen_c:
+            validate_cluster(cluster)
+            seen_c[id(cluster)] = cluster
+        key = (id(profile), id(cluster))
+        p = seen_pc.get(key)
+        if p is None:
+            check_numeric_range(profile, cluster)
+            p = _device.pack(profile, cluster)
+            seen_pc[key] = p
         if M < 1:
             from .model import ValidationError
             raise ValidationError("microbatch count must be positive")
-        p = _device.pack(profile, cluster)
         packs.append(p)
-        items.append((p, int(M), _lib.PP_ALLOW_REPLICATION | sum_flags(), None))
+        items.append((p, int(M), flags, None))
     return items, packs
 
 

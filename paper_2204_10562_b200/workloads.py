@@ -59,6 +59,27 @@ class InstanceSpec:
                             self.gpu_ids, self.links, int(M), dict(self.meta))
 
 
+def models_of(specs: Sequence["InstanceSpec"]):
+    """(profile, cluster, M) triples where equal profiles / clusters are the SAME
+    objects — how a user plans one physical cluster for several models and
+    microbatch counts."""
+    from .model import InterLayerEdge, LayerProfile, ModelProfile, make_cluster
+    profiles, clusters, out = {}, {}, []
+    for s in specs:
+        pk = (s.name.split("_j")[0], tuple(s.fwd), tuple(s.bwd), tuple(s.param), tuple(s.efwd), tuple(s.ebwd))
+        ck = (tuple(s.gpu_ids), tuple(s.links))
+        if pk not in profiles:
+            layers = tuple(LayerProfile(id=i + 1, fwd_time=f, bwd_time=b, param_bytes=p)
+                           for i, (f, b, p) in enumerate(zip(s.fwd, s.bwd, s.param)))
+            edges = tuple(InterLayerEdge(src=i + 1, dst=i + 2, fwd_bytes=a, bwd_bytes=b)
+                          for i, (a, b) in enumerate(zip(s.efwd, s.ebwd)))
+            profiles[pk] = ModelProfile(name=s.name, microbatch_size=1, layers=layers, edges=edges)
+        if ck not in clusters:
+            clusters[ck] = make_cluster(s.gpu_ids, s.links)
+        out.append((profiles[pk], clusters[ck], s.M))
+    return out
+
+
 def _clique(ids: Sequence[int], bw_fn) -> List[Tuple[int, int, float]]:
     return [(a, b, float(bw_fn(a, b))) for i, a in enumerate(ids) for b in ids[i + 1:]]
 
