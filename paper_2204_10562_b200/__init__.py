@@ -7,6 +7,7 @@ libpipeplan_b200.so (sm_100a CUDA) — there is no CPU fallback; without a GPU
 the planning calls raise _lib.BackendUnavailable.
 """
 
+from .baselines import dataparallel_plan, gpipe_plan, gpipe_schedule, noreplication_plan
 from .model import (AllReduceWindow, Block, ClusterGraph, InterLayerEdge, LayerProfile, ModelProfile, Plan,
                     Schedule, ScheduleEvent, Stage, ValidationError, check_numeric_range, make_cluster,
                     plan_uses_all_gpus, validate_cluster, validate_plan, validate_profile)
@@ -22,7 +23,8 @@ __all__ = [
     "AllReduceWindow", "Block", "BoundReport", "ClusterGraph", "DeviceOrdering", "ExecutionOrder",
     "InterLayerEdge", "LayerProfile", "ModelProfile", "Plan", "PartitionSolver", "PrmResult", "Schedule",
     "ScheduleEvent", "SchedulingError", "SppResult", "Stage", "SweepEntry", "ValidationError",
-    "best_partition", "bound_factor", "build_block_list", "check_numeric_range", "compute_execution_order",
+    "best_partition", "bound_factor", "dataparallel_plan", "gpipe_plan", "gpipe_schedule",
+    "noreplication_plan", "build_block_list", "check_numeric_range", "compute_execution_order",
     "global_min_cut", "lemma1_bound", "make_cluster", "phi", "plan_uses_all_gpus", "prm", "rdo",
     "simulate_pe", "simulate_pe_many", "simulate_with_order", "spp", "spp_many", "theorem1_report", "validate_cluster",
     "validate_plan", "validate_profile",

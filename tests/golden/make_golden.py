@@ -254,6 +254,38 @@ def _gpipe_queues(plan):
     return queues
 
 
+def gen_baselines():
+    """gpipe_plan / gpipe_schedule / dataparallel_plan / noreplication_plan
+    through the reference's own API (baselines.py:28-97)."""
+    rng = random.Random(41)
+    insts = [(tiny_profile(), tiny_cluster(), 2)]
+    for _ in range(30):
+        insts.append(random_instance(rng))
+    insts.append(ref_model(W.c1_vgg19()))
+    insts.append(ref_model(W.c2_bert24(M=8)))
+    insts.append(ref_model(W.c3_gpt96(M=16, jitter_seed=96, L=24, nodes=2, per_node=4)))
+    cases = []
+    for prof, clu, M in insts:
+        order = P.rdo(clu)
+        L, V = prof.num_layers, clu.num_gpus
+        gp = []
+        for n in range(0, min(L, V) + 2):
+            try:
+                plan = P.gpipe_plan(prof, clu, order, n, M)
+            except P.ValidationError as e:
+                gp.append([n, "error", str(e)])
+                continue
+            s = P.gpipe_schedule(plan, prof, clu)
+            sc = sched_of(s) if len(s.events) <= 3000 else {"events": None, "makespan": hx(s.makespan),
+                                                             "allreduce": sched_of(s)["allreduce"]}
+            gp.append([n, plan_of(plan), sc])
+        w, plan = P.noreplication_plan(prof, clu, order, M)
+        cases.append({"input": spec_of(prof, clu, M), "order": list(order.order), "gpipe": gp,
+                      "dataparallel": plan_of(P.dataparallel_plan(prof, clu, M)),
+                      "noreplication": [hx(w), None if plan is None else plan_of(plan)]})
+    return {"python": sys.version, "cases": cases}
+
+
 def gen_ordering():
     rng = random.Random(SEED)
     cuts = []
@@ -284,8 +316,9 @@ def gen_ordering():
 
 
 def main():
-    which = sys.argv[1:] or ["pysum", "spp", "prm", "sim", "ordering"]
-    gens = {"pysum": gen_pysum, "spp": gen_spp, "prm": gen_prm, "sim": gen_sim, "ordering": gen_ordering}
+    which = sys.argv[1:] or ["pysum", "spp", "prm", "sim", "ordering", "baselines"]
+    gens = {"pysum": gen_pysum, "spp": gen_spp, "prm": gen_prm, "sim": gen_sim, "ordering": gen_ordering,
+            "baselines": gen_baselines}
     for name in which:
         t0 = time.time()
         data = gens[name]()

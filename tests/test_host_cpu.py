@@ -149,3 +149,30 @@ def test_lazy_events_behave_like_tuples():
     other = LazyEvents(res, lab, np.array([1, 1, 2]), np.array([1, 2, 1]), np.array([0.0, 1.0, 1.0]),
                        np.array([1.0, 2.0, 2.5]))
     assert other != ev
+
+
+def test_baseline_host_planners_match_goldens():
+    """gpipe_plan / dataparallel_plan / the flush queues are host bookkeeping:
+    checked here against the reference goldens without a GPU."""
+    from helpers import load, model_of
+    from paper_2204_10562_b200.baselines import gpipe_queues
+    for case in load("baselines")["cases"]:
+        prof, clu, M = model_of(case["input"])
+        o = tuple(case["order"])
+        ordering = P.DeviceOrdering(order=o, rank={v: k + 1 for k, v in enumerate(o)})
+        for n, *rest in case["gpipe"]:
+            if rest[0] == "error":
+                with pytest.raises(P.ValidationError, match="infeasible stage count"):
+                    P.gpipe_plan(prof, clu, ordering, n, M)
+                continue
+            plan = P.gpipe_plan(prof, clu, ordering, n, M)
+            assert [[s.layer_start, s.layer_end, list(s.devices)] for s in plan.stages] == rest[0]["stages"]
+        dp = P.dataparallel_plan(prof, clu, M)
+        assert [[s.layer_start, s.layer_end, list(s.devices)] for s in dp.stages] == case["dataparallel"]["stages"]
+    for case in load("sim")["cases"]:
+        if "gpipe" not in case["name"]:
+            continue
+        st = case["plan"]["stages"]
+        plan = P.Plan(tuple(P.Stage(n + 1, a, b, tuple(d)) for n, (a, b, d) in enumerate(st)), case["plan"]["M"])
+        want = {k: tuple(map(tuple, v)) for k, v in case["queues"].items()}
+        assert gpipe_queues(plan) == want
