@@ -184,6 +184,19 @@ int pp_peak_minmax(double *d_out, int32_t iters, int64_t *n_ops, void *stream);
 int pp_min_cut(const pp_batch *b, int32_t k, const int32_t *verts, int32_t n, uint8_t *in_a,
                double *weight, void *stream);
 
+/* ---- trace writer (host) ------------------------------------------------ */
+/* write_trace text (fileio.py:170-188; numbers as format_number, fileio.py:32-38)
+ * from event arrays: row k = res_names[ev_pos[k]], ev_m[k], labels[ev_pos[k]],
+ * ev_start[k], ev_end[k]; then one "allreduce" row per window.  Host memory
+ * only; formats on up to nthreads threads.  *out_len = bytes needed; PP_EINVAL
+ * with "non-finite number in output: <x>" at the first inf/nan, or when the
+ * text exceeds cap (out is then unspecified). */
+int pp_format_trace(int64_t n_events, const int32_t *ev_m, const int32_t *ev_pos, const double *ev_start,
+                    const double *ev_end, const char *const *res_names, const char *const *labels,
+                    int32_t n_names, int32_t n_ar, const int32_t *ar_stage, const double *ar_start,
+                    const double *ar_end, double makespan, char *out, int64_t cap, int64_t *out_len,
+                    int32_t nthreads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,6 +8,8 @@ the planning calls raise _lib.BackendUnavailable.
 """
 
 from .baselines import dataparallel_plan, gpipe_plan, gpipe_schedule, noreplication_plan
+from .fileio import (Trace, TraceRow, format_number, load_cluster, load_plan, load_profile, parse_trace, read_trace,
+                     save_cluster, save_plan, save_profile, trace_to_schedule, write_trace)
 from .model import (AllReduceWindow, Block, ClusterGraph, InterLayerEdge, LayerProfile, ModelProfile, Plan,
                     Schedule, ScheduleEvent, Stage, ValidationError, check_numeric_range, make_cluster,
                     plan_uses_all_gpus, validate_cluster, validate_plan, validate_profile)
@@ -28,4 +30,6 @@ __all__ = [
     "global_min_cut", "lemma1_bound", "make_cluster", "phi", "plan_uses_all_gpus", "prm", "rdo",
     "simulate_pe", "simulate_pe_many", "simulate_with_order", "spp", "spp_many", "theorem1_report", "validate_cluster",
     "validate_plan", "validate_profile",
+    "Trace", "TraceRow", "format_number", "load_cluster", "load_plan", "load_profile", "parse_trace", "read_trace",
+    "save_cluster", "save_plan", "save_profile", "trace_to_schedule", "write_trace",
 ]

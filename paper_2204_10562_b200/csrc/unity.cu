@@ -2,3 +2,4 @@
 #include "prm.cu"
 #include "sim.cu"
 #include "capi.cu"
+#include "trace.cu"

@@ -286,6 +286,35 @@ def gen_baselines():
     return {"python": sys.version, "cases": cases}
 
 
+def gen_fileio():
+    """write_trace / save_profile / save_cluster / save_plan text through the
+    reference (fileio.py), for the sim.json schedules and the spp plans."""
+    sim = json.load(open(os.path.join(HERE, "sim.json")))
+    out = []
+    for c in sim["cases"]:
+        if "schedule" not in c:
+            continue
+        spec = c["input"]
+        prof, clu, _ = ref_model(W.InstanceSpec(spec["name"], *[[float.fromhex(x) for x in spec[k]] for k in
+                                                                 ("fwd", "bwd", "param", "efwd", "ebwd")],
+                                                spec["gpu_ids"], [(a, b, float.fromhex(w)) for a, b, w in
+                                                                  spec["links"]], spec["M"]))
+        st = c["plan"]["stages"]
+        plan = P.Plan(tuple(P.Stage(n + 1, a, b, tuple(d)) for n, (a, b, d) in enumerate(st)), c["plan"]["M"])
+        sched = P.simulate_with_order(plan, prof, clu, {k: tuple(map(tuple, v)) for k, v in c["queues"].items()},
+                                      forward_barrier=c["forward_barrier"])
+        out.append({"name": c["name"], "trace": P.write_trace(None, sched), "profile": P.save_profile(None, prof),
+                    "cluster": P.save_cluster(None, clu), "plan": P.save_plan(None, plan)})
+    rng = random.Random(3)
+    nums = [0.0, -0.0, 5.0, 1 / 3, 123456789.0, 1e9, 1e-320, 5e-324, 1.7976931348623157e308, 2.0 ** 53,
+            2.0 ** 53 + 2, 0.1, 1e16, 123456789012.0, 9.9999999995e-5]
+    for _ in range(5000):
+        nums.append(math.exp(rng.uniform(-700, 700)) * rng.choice((1, -1)))
+        nums.append(round(rng.uniform(0, 1e6), rng.randint(0, 12)))
+    fmt = [[hx(x), P.format_number(x)] for x in nums]
+    return {"python": sys.version, "cases": out, "format_number": fmt}
+
+
 def gen_ordering():
     rng = random.Random(SEED)
     cuts = []
@@ -316,9 +345,9 @@ def gen_ordering():
 
 
 def main():
-    which = sys.argv[1:] or ["pysum", "spp", "prm", "sim", "ordering", "baselines"]
+    which = sys.argv[1:] or ["pysum", "spp", "prm", "sim", "ordering", "baselines", "fileio"]
     gens = {"pysum": gen_pysum, "spp": gen_spp, "prm": gen_prm, "sim": gen_sim, "ordering": gen_ordering,
-            "baselines": gen_baselines}
+            "baselines": gen_baselines, "fileio": gen_fileio}
     for name in which:
         t0 = time.time()
         data = gens[name]()

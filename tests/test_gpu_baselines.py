@@ -108,3 +108,15 @@ def test_noreplication_infeasible_when_fewer_layers_than_gpus():
     prof, clu, M = model_of(case["input"])
     w, plan = P.noreplication_plan(prof, clu, P.rdo(clu), M)
     assert math.isinf(w) and plan is None
+
+
+def test_trace_of_device_schedule_matches_object_path():
+    """write_trace on the LazyEvents of a device schedule (arrays straight to
+    pp_format_trace) == write_trace on the materialized ScheduleEvent tuple."""
+    from paper_2204_10562_b200 import workloads as W
+    prof, clu, M = W.c3_gpt96(M=64, nodes=2, per_node=8, L=48).to_model()
+    r = P.spp(prof, clu, M)
+    lazy = P.write_trace(None, r.schedule)
+    objs = P.Schedule(events=tuple(r.schedule.events), allreduce=r.schedule.allreduce, makespan=r.makespan)
+    assert lazy == P.write_trace(None, objs)
+    assert len(lazy.splitlines()) == 2 + len(r.schedule.events) + len(r.schedule.allreduce)
