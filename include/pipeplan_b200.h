@@ -83,6 +83,7 @@ typedef struct {
     double *ev_start, *ev_end;
     double *ar_start, *ar_end;
     double *ws;                       /* fp64 workspace, pp_layout() doubles                      */
+    double *gamma;                    /* [n_inst] cost.py:126-128, written by pp_phi; NULL skips  */
 } pp_batch;
 
 /* ---- host helpers (no device work) ------------------------------------ */
@@ -135,6 +136,16 @@ int pp_prm_query(const pp_batch *b, int32_t n_query, const int32_t *q_inst, cons
  * (0 = stage1, 1 = chan1, 2 = stage2, ...), R = 2N-1 of them. */
 #define PP_SIM_FORWARD_BARRIER 1   /* simulate_with_order(forward_barrier=True)          */
 #define PP_SIM_PE_ORDER 2          /* queues = compute_execution_order(plan) (closed form) */
+#define PP_SIM_CYCLE 4             /* simulate_cycle_schedule (scheduler.py:241-296)       */
+#define PP_SIM_COSTS_ONLY 8        /* per-lane costs + workload + bound, no simulation    */
+
+/* per-lane cost record (lane_cost[(lane_off + r) * PP_LANE_COST_FIELDS + f]) */
+#define PP_LANE_COST_FIELDS 7
+/* stage lane: F (FB for the last stage) duration, B duration, stage_compute_time,
+ *             allreduce_time (0 unless replicated), stage_fwd_time, stage_bwd_time,
+ *             min pairwise bandwidth (+inf for one device)
+ * chan lane : X duration (c_fwd), Y duration (c_bwd), c_fwd + c_bwd, 0, 0, 0,
+ *             min cross bandwidth                                          */
 
 typedef struct {
     int32_t inst;        /* instance (profile + bw) in the pp_batch            */
@@ -162,6 +173,9 @@ typedef struct {
     double *ev_start, *ev_end;        /* per (m,pos); NULL skips event capture   */
     double *ar_start, *ar_end;        /* per stage                               */
     double *scratch;                  /* per (m,pos) completion times (generic queues) */
+    double *lane_cost;                /* per resource PP_LANE_COST_FIELDS doubles; NULL skips */
+    double *workload;                 /* [n_plan] cost_summary workload; NULL skips          */
+    int32_t *cycles;                  /* [n_plan] cycle count (PP_SIM_CYCLE); NULL skips      */
 } pp_sim_batch;
 
 /* simulate_with_order / simulate_pe (scheduler.py:121-231) + lemma1_bound

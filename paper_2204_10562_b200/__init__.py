@@ -8,6 +8,8 @@ the planning calls raise _lib.BackendUnavailable.
 """
 
 from .baselines import dataparallel_plan, gpipe_plan, gpipe_schedule, noreplication_plan
+from .cost import (CostSummary, allreduce_time, block_duration, block_durations, channel_times, cost_summary, gamma,
+                   interstage_comm_time, min_cross_bandwidth, min_pairwise_bandwidth)
 from .fileio import (Trace, TraceRow, format_number, load_cluster, load_plan, load_profile, parse_trace, read_trace,
                      save_cluster, save_plan, save_profile, trace_to_schedule, write_trace)
 from .model import (AllReduceWindow, Block, ClusterGraph, InterLayerEdge, LayerProfile, ModelProfile, Plan,
@@ -17,7 +19,7 @@ from .ordering import DeviceOrdering, global_min_cut, rdo
 from .partition import PartitionSolver, PrmResult, best_partition, prm
 from .planner import BoundReport, SppResult, SweepEntry, bound_factor, phi, spp, spp_many, theorem1_report
 from .scheduler import (ExecutionOrder, SchedulingError, build_block_list, compute_execution_order, lemma1_bound,
-                        simulate_pe, simulate_pe_many, simulate_with_order)
+                        simulate_cycle_schedule, simulate_pe, simulate_pe_many, simulate_with_order)
 
 __version__ = "0.1.0"
 
@@ -32,4 +34,6 @@ __all__ = [
     "validate_plan", "validate_profile",
     "Trace", "TraceRow", "format_number", "load_cluster", "load_plan", "load_profile", "parse_trace", "read_trace",
     "save_cluster", "save_plan", "save_profile", "trace_to_schedule", "write_trace",
+    "CostSummary", "allreduce_time", "block_duration", "block_durations", "channel_times", "cost_summary", "gamma",
+    "interstage_comm_time", "min_cross_bandwidth", "min_pairwise_bandwidth", "simulate_cycle_schedule",
 ]

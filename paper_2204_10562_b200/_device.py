@@ -147,9 +147,9 @@ class DeviceBatch:
         # ---- device allocations
         self.d_fin = _staging.to_device(fin, dev)
         self.d_iin = _staging.to_device(iin, dev)
-        # outputs: fp64 [sweep_w | sweep_mk | sweep_bound | best_mk | phi | ar_s | ar_e | ev_s | ev_e]
+        # outputs: fp64 [sweep_w | sweep_mk | sweep_bound | best_mk | phi | gamma | ar_s | ar_e | ev_s | ev_e]
         ev = n_ev if capture_events else 0
-        self.f_off = np.cumsum([0, n_sweep, n_sweep, n_sweep, n, n, n_ar, n_ar, ev, ev])
+        self.f_off = np.cumsum([0, n_sweep, n_sweep, n_sweep, n, n, n, n_ar, n_ar, ev, ev])
         self.d_fout = torch.empty(int(self.f_off[-1]), dtype=F64, device=dev)
         # int32 outputs: [sweep_r | ls | le | dlo | dhi | best_xi]
         self.i_off = np.cumsum([0, n_sweep, n_stage, n_stage, n_stage, n_stage, n])
@@ -173,9 +173,10 @@ class DeviceBatch:
         fo = self.d_fout.data_ptr()
         fo_ = [fo + 8 * int(x) for x in self.f_off]
         b.sweep_w, b.sweep_mk, b.sweep_bound, b.best_mk, b.phi = fo_[0], fo_[1], fo_[2], fo_[3], fo_[4]
-        b.ar_start, b.ar_end = fo_[5], fo_[6]
-        b.ev_start = fo_[7] if capture_events else None
-        b.ev_end = fo_[8] if capture_events else None
+        b.gamma = fo_[5]
+        b.ar_start, b.ar_end = fo_[6], fo_[7]
+        b.ev_start = fo_[8] if capture_events else None
+        b.ev_end = fo_[9] if capture_events else None
         io = self.d_iout.data_ptr()
         io_ = [io + 4 * int(x) for x in self.i_off]
         b.sweep_r, b.stage_ls, b.stage_le, b.stage_dlo, b.stage_dhi, b.best_xi = io_[:6]
@@ -196,7 +197,7 @@ class DeviceBatch:
         io = self.d_iout.cpu().numpy()
         order = self.d_iin[self.n_ib:].cpu().numpy()
         f = {k: fo[int(self.f_off[i]):int(self.f_off[i + 1])]
-             for i, k in enumerate(("sweep_w", "sweep_mk", "sweep_bound", "best_mk", "phi",
+             for i, k in enumerate(("sweep_w", "sweep_mk", "sweep_bound", "best_mk", "phi", "gamma",
                                     "ar_start", "ar_end", "ev_start", "ev_end"))}
         g = {k: io[int(self.i_off[i]):int(self.i_off[i + 1])]
              for i, k in enumerate(("sweep_r", "ls", "le", "dlo", "dhi", "best_xi"))}
@@ -248,7 +249,7 @@ class SimPlan:
 class SimRun:
     """Run pp_simulate for plans over a DeviceBatch's instances."""
 
-    def __init__(self, db: DeviceBatch, plans: Sequence[SimPlan], capture_events=True):
+    def __init__(self, db: DeviceBatch, plans: Sequence[SimPlan], capture_events=True, costs=False):
         lib = db.lib
         dev = db.d_fin.device
         n = len(plans)
@@ -294,11 +295,14 @@ class SimRun:
         offs = np.cumsum([0] + [a.size for a in ints])
         d_in = _staging.to_device(np.concatenate(ints), dev)
         # fp64 outputs: makespan | bound | ar_s | ar_e | ev_s | ev_e | scratch (generic queues only)
+        #              | lane costs | workload (costs=True only)
         evn = ev if capture_events else 0
         scr = ev if any(sp.queues is not None for sp in plans) else 1
-        self.f_off = np.cumsum([0, n, n, ar, ar, evn, evn, scr])
+        nlc, nwl = (lane * _lib.PP_LANE_COST_FIELDS, n) if costs else (0, 0)
+        self.f_off = np.cumsum([0, n, n, ar, ar, evn, evn, scr, nlc, nwl])
         self.d_f = torch.empty(int(self.f_off[-1]), dtype=F64, device=dev)
-        self.i_off = np.cumsum([0, n, lane])
+        # int32 outputs: status | head | cycles
+        self.i_off = np.cumsum([0, n, lane, n])
         self.d_i = torch.empty(int(self.i_off[-1]), dtype=I32, device=dev)
         self.d_done = torch.empty(n, dtype=torch.int64, device=dev)
         s = PPSimBatch()
@@ -311,13 +315,16 @@ class SimRun:
         s.ev_start = fo[4] if capture_events else None
         s.ev_end = fo[5] if capture_events else None
         s.scratch = fo[6]
+        s.lane_cost = fo[7] if costs else None
+        s.workload = fo[8] if costs else None
         io = self.d_i.data_ptr()
-        s.status, s.head = io, io + 4 * n
+        s.status, s.head, s.cycles = io, io + 4 * n, io + 4 * int(self.i_off[2])
         s.n_done = self.d_done.data_ptr()
         self._keep = d_in
         self.sim = s
         self.n = n
         self.capture_events = capture_events
+        self.costs = costs
         _lib.check(lib.pp_simulate(C.byref(db.batch), C.byref(s), _stream()))
 
     def fetch(self):
@@ -331,8 +338,13 @@ class SimRun:
                        head=i[self.i_off[1] + lane: self.i_off[1] + lane + R],
                        ar_start=f[self.f_off[2] + ar: self.f_off[2] + ar + N],
                        ar_end=f[self.f_off[3] + ar: self.f_off[3] + ar + N])
+            rec["cycles"] = int(i[self.i_off[2] + k])
             if self.capture_events:
                 rec["ev_start"] = f[self.f_off[4] + ev: self.f_off[4] + ev + M * J]
                 rec["ev_end"] = f[self.f_off[5] + ev: self.f_off[5] + ev + M * J]
+            if self.costs:
+                F_ = _lib.PP_LANE_COST_FIELDS
+                rec["lane_cost"] = f[self.f_off[7] + lane * F_: self.f_off[7] + (lane + R) * F_].reshape(R, F_)
+                rec["workload"] = float(f[self.f_off[8] + k])
             out.append(rec)
         return out

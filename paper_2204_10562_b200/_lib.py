@@ -22,6 +22,9 @@ PP_SUM_NAIVE = 2
 PP_GIVEN_ORDER = 4
 PP_SIM_FORWARD_BARRIER = 1
 PP_SIM_PE_ORDER = 2
+PP_SIM_CYCLE = 4
+PP_SIM_COSTS_ONLY = 8
+PP_LANE_COST_FIELDS = 7
 PP_MAX_LAYERS = 4096
 PP_MAX_GPUS = 512
 
@@ -60,7 +63,7 @@ class PPBatch(C.Structure):
                 ("best_xi", C.c_void_p), ("best_mk", C.c_void_p), ("phi", C.c_void_p),
                 ("ev_start", C.c_void_p), ("ev_end", C.c_void_p),
                 ("ar_start", C.c_void_p), ("ar_end", C.c_void_p),
-                ("ws", C.c_void_p)]
+                ("ws", C.c_void_p), ("gamma", C.c_void_p)]
 
 
 class PPPlan(C.Structure):
@@ -76,7 +79,8 @@ class PPSimBatch(C.Structure):
                 ("makespan", C.c_void_p), ("bound", C.c_void_p), ("status", C.c_void_p),
                 ("n_done", C.c_void_p), ("head", C.c_void_p),
                 ("ev_start", C.c_void_p), ("ev_end", C.c_void_p),
-                ("ar_start", C.c_void_p), ("ar_end", C.c_void_p), ("scratch", C.c_void_p)]
+                ("ar_start", C.c_void_p), ("ar_end", C.c_void_p), ("scratch", C.c_void_p),
+                ("lane_cost", C.c_void_p), ("workload", C.c_void_p), ("cycles", C.c_void_p)]
 
 
 EXPORTS = ("pp_version", "pp_last_error", "pp_device_count", "pp_layout", "pp_rdo", "pp_prm",

@@ -1,4 +1,5 @@
 // capi.cu — extern "C" entry points of libpipeplan_b200.so (include/pipeplan_b200.h).
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -297,7 +298,7 @@ int pp_prm_query(const pp_batch* b, int32_t n_query, const int32_t* q_inst, cons
 int pp_simulate(const pp_batch* ib, const pp_sim_batch* s, void* stream) {
     if (s->n_plan <= 0) return PP_OK;
     if (s->max_N < 1 || s->max_N > PP_MAX_GPUS) return fail(PP_EINVAL, "max_N=%d outside 1..%d", s->max_N, PP_MAX_GPUS);
-    const size_t smem = sim_smem(s->max_N);
+    const size_t smem = std::max(sim_smem(s->max_N), sizeof(double) * 128);   // + plan_costs / cycle scratch
     cudaFuncSetAttribute(k_sim_plans, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_sim_plans<<<s->n_plan, sim_block(s->max_N), smem, S(stream)>>>(*ib, *s);
     PP_CHECK_LAUNCH("k_sim_plans");

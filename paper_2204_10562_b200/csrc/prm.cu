@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(128) k_phi(pp_batch b) {
         phi = num / gamma * (1.0 / mn - 1.0 / mx);
     }
     b.phi[blockIdx.x] = phi;
+    if (b.gamma) b.gamma[blockIdx.x] = gamma;
 }
 
 // ----------------------------------------------------------------------------

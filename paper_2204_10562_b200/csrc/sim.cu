@@ -57,11 +57,13 @@ struct LaneCost {
     double cyc;         // per-stage compute or per-channel comm (cost_summary)
     double ar;          // AllReduce time (replicated stages)
     bool has_ar;
+    double sf, sb;      // stage_fwd_time / stage_bwd_time (cost.py:44-53); 0 on channels
+    double mbw;         // min pairwise (stage) / min cross (chan) bandwidth (cost.py:64-80)
 };
 
 template <class P>
 __device__ LaneCost lane_cost(const P& p, const InstView& I, int N, int lane) {
-    LaneCost c{0.0, 0.0, 0.0, 0.0, false};
+    LaneCost c{0.0, 0.0, 0.0, 0.0, false, 0.0, 0.0, PP_INF};
     const int n = lane / 2 + 1;
     if ((lane & 1) == 0) {
         const int k = p.k(n), a = p.stage_ls(n), e = p.stage_le(n);
@@ -70,6 +72,8 @@ __device__ LaneCost lane_cost(const P& p, const InstView& I, int N, int lane) {
         if (n < N) { c.dA = sf / (double)k; c.dB = sb / (double)k; }             // cost.py:215-218
         else { c.dA = (sf + sb) / (double)k; c.dB = c.dA; }                      // cost.py:219-220
         c.cyc = sf + sb;                                                          // cost.py:56-61
+        c.sf = sf;
+        c.sb = sb;
         if (k >= 2) {
             const double total = pysum(I.par + a - 1, e - a + 1, I.naive);
             double mp = PP_INF;
@@ -77,6 +81,7 @@ __device__ LaneCost lane_cost(const P& p, const InstView& I, int N, int lane) {
                 for (int y = x + 1; y < k; ++y) mp = dmin(mp, I.w(p.dev(n, x), p.dev(n, y)));
             c.ar = 2.0 * (double)(k - 1) * total / ((double)k * mp);              // cost.py:99
             c.has_ar = true;
+            c.mbw = mp;
         }
     } else {
         const int kl = p.k(n), kr = p.k(n + 1);
@@ -88,6 +93,7 @@ __device__ LaneCost lane_cost(const P& p, const InstView& I, int N, int lane) {
         c.dA = I.efwd[edge - 1] / denom;
         c.dB = I.ebwd[edge - 1] / denom;
         c.cyc = c.dA + c.dB;                                                      // cost.py:194
+        c.mbw = mc;
     }
     return c;
 }
@@ -125,7 +131,7 @@ __device__ void pe_simulate(const P& p, const InstView& I, int N, int M, int nth
     double* be = sm + 2 * R;    // [2][R]
     double* red = sm + 4 * R;   // [64]
     __shared__ double s_cyc, s_armax;
-    LaneCost c{0.0, 0.0, 0.0, 0.0, false};
+    LaneCost c{0.0, 0.0, 0.0, 0.0, false, 0.0, 0.0, PP_INF};
     if (lane < R) c = lane_cost(p, I, N, lane);
     reduce_costs(c, lane, R, nthr, red, &s_cyc, &s_armax);
     if (lane == 0) *o_bound = (double)(M + 4 * N - 4) * s_cyc + s_armax;   // scheduler.py:238
@@ -253,6 +259,101 @@ __global__ void __launch_bounds__(1024) k_replay(pp_batch b) {
                 b.ar_start + I.ar_off, b.ar_end + I.ar_off);
 }
 
+// ---- plan costs (cost_summary, cost.py:172-202; channel_times :162-169;
+// block_durations :205-230): per-lane records + workload + Lemma-1 bound.
+// workload = max(M*compute_s (+ A_s if replicated), M*(c_fwd+c_bwd)_n); max is
+// order-free, so the lane-parallel reduction is the reference's max(w_terms).
+__device__ void plan_costs(const LaneCost& c, int lane, int R, int M, int nthr, double* red, double* lane_out,
+                           double* o_workload) {
+    if (lane < R && lane_out) {
+        double* o = lane_out + (int64_t)lane * PP_LANE_COST_FIELDS;
+        o[0] = c.dA; o[1] = c.dB; o[2] = c.cyc; o[3] = c.has_ar ? c.ar : 0.0;
+        o[4] = c.sf; o[5] = c.sb; o[6] = c.mbw;
+    }
+    if (!o_workload) return;
+    double w = -PP_INF;
+    if (lane < R) {
+        w = (double)M * c.cyc;
+        if (c.has_ar) w = w + c.ar;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) w = dmax(w, __shfl_xor_sync(0xffffffffu, w, off));
+    if ((lane & 31) == 0) red[64 + (lane >> 5)] = w;
+    bar_sync(nthr);
+    if (lane == 0) {
+        double a = -PP_INF;
+        for (int k = 0; k < nthr / 32; ++k) a = dmax(a, red[64 + k]);
+        *o_workload = a;
+    }
+    bar_sync(nthr);
+}
+
+// ---- lockstep cycle schedule (scheduler.py:241-296) ---------------------------
+// Cycle c runs position p on microbatch m = c - p + 1 (the wavefront the
+// "completed[p-1] > completed[p]" rule produces); a resource runs its chosen
+// blocks back to back in ascending position order starting at the cycle
+// start t, and the next cycle starts at max(t, every end of this cycle).
+// M + 4N - 4 cycles.  red: [2][32] doubles (double-buffered cycle maxima).
+__device__ void cycle_simulate(const LaneCost& c, int N, int M, int nthr, double* red, double* ev_s, double* ev_e,
+                               double* ar_s, double* ar_e, double* o_mk) {
+    const int R = 2 * N - 1, J = 4 * N - 3;
+    const int lane = threadIdx.x;
+    const bool is_stage = (lane & 1) == 0;
+    const int n = lane / 2 + 1;
+    int p_lo, p_hi;   // ascending positions; p_hi = 0 when the lane has one block
+    if (is_stage) {
+        if (n < N) { p_lo = 2 * n - 1; p_hi = 4 * N - 1 - 2 * n; }   // F_n, B_n
+        else { p_lo = 2 * N - 1; p_hi = 0; }                        // FB_N
+    } else { p_lo = 2 * n; p_hi = 4 * N - 2 - 2 * n; }              // X_n, Y_n
+    const int nw = nthr / 32;
+    double t = 0.0, last = 0.0;
+    const int cycles = M + J - 1;
+    for (int cy = 1; cy <= cycles; ++cy) {
+        double clock = t;
+        if (lane < R) {
+            int m = cy - p_lo + 1;
+            if (m >= 1 && m <= M) {
+                const double st = clock, en = st + c.dA;
+                clock = en;
+                last = en;
+                if (ev_s) { const int64_t x = (int64_t)(m - 1) * J + p_lo - 1; ev_s[x] = st; ev_e[x] = en; }
+            }
+            m = cy - p_hi + 1;
+            if (p_hi && m >= 1 && m <= M) {
+                const double st = clock, en = st + c.dB;
+                clock = en;
+                last = en;
+                if (ev_s) { const int64_t x = (int64_t)(m - 1) * J + p_hi - 1; ev_s[x] = st; ev_e[x] = en; }
+            }
+        }
+        double v = clock;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v = dmax(v, __shfl_xor_sync(0xffffffffu, v, off));
+        double* buf = red + (cy & 1) * 32;
+        if ((lane & 31) == 0) buf[lane >> 5] = v;
+        bar_sync(nthr);
+        double tn = buf[0];
+        for (int k = 1; k < nw; ++k) tn = dmax(tn, buf[k]);
+        t = tn;
+    }
+    // AllReduce at the stage's last compute end; makespan = max(end of B_1(M) / FB_1(M), AR ends)
+    double arend = -PP_INF;
+    if (lane < R && is_stage && c.has_ar) {
+        arend = last + c.ar;
+        if (ar_s) { ar_s[n - 1] = last; ar_e[n - 1] = arend; }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) arend = dmax(arend, __shfl_xor_sync(0xffffffffu, arend, off));
+    if ((lane & 31) == 0) red[64 + (lane >> 5)] = arend;
+    if (lane == 0) red[96] = last;
+    bar_sync(nthr);
+    if (lane == 0) {
+        double mk = red[96];
+        for (int k = 0; k < nw; ++k) mk = dmax(mk, red[64 + k]);
+        *o_mk = mk;
+    }
+}
+
 // ---- caller plans -------------------------------------------------------------
 __global__ void __launch_bounds__(1024) k_sim_plans(pp_batch b, pp_sim_batch s) {
     const pp_plan P = s.plan[blockIdx.x];
@@ -265,6 +366,32 @@ __global__ void __launch_bounds__(1024) k_sim_plans(pp_batch b, pp_sim_batch s) 
     InstView iv(b, I);
     double* ev_s = s.ev_start ? s.ev_start + P.ev_off : nullptr;
     double* ev_e = s.ev_end ? s.ev_end + P.ev_off : nullptr;
+    if (P.flags & (PP_SIM_CYCLE | PP_SIM_COSTS_ONLY) || s.lane_cost || s.workload) {
+        const int lane = threadIdx.x;
+        double* red = smem_d;   // [128]
+        __shared__ double s_cyc, s_armax;
+        LaneCost c{0.0, 0.0, 0.0, 0.0, false, 0.0, 0.0, PP_INF};
+        if (lane < R) c = lane_cost(pv, iv, N, lane);
+        reduce_costs(c, lane, R, nthr, red, &s_cyc, &s_armax);
+        if (lane == 0) s.bound[blockIdx.x] = (double)(M + 4 * N - 4) * s_cyc + s_armax;
+        plan_costs(c, lane, R, M, nthr, red, s.lane_cost ? s.lane_cost + P.lane_off * PP_LANE_COST_FIELDS : nullptr,
+                   s.workload ? s.workload + blockIdx.x : nullptr);
+        if (P.flags & (PP_SIM_CYCLE | PP_SIM_COSTS_ONLY)) {
+            const bool cyc = P.flags & PP_SIM_CYCLE;
+            if (cyc)
+                cycle_simulate(c, N, M, nthr, red, ev_s, ev_e, s.ar_start + P.ar_off, s.ar_end + P.ar_off,
+                               s.makespan + blockIdx.x);
+            if (lane == 0) {
+                s.status[blockIdx.x] = 0;
+                s.n_done[blockIdx.x] = cyc ? (int64_t)M * J : 0;
+                if (!cyc) s.makespan[blockIdx.x] = 0.0;
+                if (s.cycles) s.cycles[blockIdx.x] = cyc ? M + J - 1 : 0;
+            }
+            for (int r = lane; r < R; r += nthr) s.head[P.lane_off + r] = -1;
+            return;
+        }
+        bar_sync(nthr);
+    }
     if (P.flags & PP_SIM_PE_ORDER) {
         pe_simulate(pv, iv, N, M, nthr, smem_d, s.makespan + blockIdx.x, s.bound + blockIdx.x, ev_s, ev_e,
                     s.ar_start + P.ar_off, s.ar_end + P.ar_off);
@@ -280,7 +407,7 @@ __global__ void __launch_bounds__(1024) k_sim_plans(pp_batch b, pp_sim_batch s) 
     __shared__ int s_open;
     __shared__ long long s_prog, s_fwd;
     __shared__ double s_fmax[32];
-    LaneCost c{0.0, 0.0, 0.0, 0.0, false};
+    LaneCost c{0.0, 0.0, 0.0, 0.0, false, 0.0, 0.0, PP_INF};
     if (lane < R) c = lane_cost(pv, iv, N, lane);
     reduce_costs(c, lane, R, nthr, red, &s_cyc, &s_armax);
     if (lane == 0) s.bound[blockIdx.x] = (double)(M + 4 * N - 4) * s_cyc + s_armax;

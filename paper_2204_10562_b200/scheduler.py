@@ -157,7 +157,7 @@ def _check_plan(plan: Plan, profile: ModelProfile, cluster: ClusterGraph) -> Non
         raise ValidationError(f"plans with more than {_lib.PP_MAX_GPUS} stages are outside this build")
 
 
-def _sim(plan, profile, cluster, queue_lists=None, forward_barrier=False, capture=True):
+def _sim(plan, profile, cluster, queue_lists=None, forward_barrier=False, capture=True, cycle=False):
     check_numeric_range(profile, cluster)
     _check_plan(plan, profile, cluster)
     packed = _device.pack(profile, cluster)
@@ -165,7 +165,9 @@ def _sim(plan, profile, cluster, queue_lists=None, forward_barrier=False, captur
     db = _device.DeviceBatch([(packed, plan.microbatch_count, sum_flags(), None)], capture_events=False)
     stages = [(s.layer_start, s.layer_end, [pos[d] for d in s.devices]) for s in plan.stages]
     flags = (_lib.PP_SIM_FORWARD_BARRIER if forward_barrier else 0)
-    if queue_lists is None:
+    if cycle:
+        flags |= _lib.PP_SIM_CYCLE
+    elif queue_lists is None:
         flags |= _lib.PP_SIM_PE_ORDER
     sp = _device.SimPlan(inst=0, M=plan.microbatch_count, stages=stages, flags=flags, queues=queue_lists)
     run = _device.SimRun(db, [sp], capture_events=capture)
@@ -254,6 +256,16 @@ def simulate_pe_many(plans: Sequence[Plan], profile: ModelProfile, cluster: Clus
                            flags=_lib.PP_SIM_PE_ORDER) for p in plans]
     run = _device.SimRun(db, sps, capture_events=False)
     return [(r["makespan"], r["bound"]) for r in run.fetch()]
+
+
+def simulate_cycle_schedule(plan: Plan, profile: ModelProfile, cluster: ClusterGraph) -> Schedule:
+    """Lockstep cycle schedule, M + 4N - 4 cycles (scheduler.py:241-296), on the GPU
+    (k_sim_plans, PP_SIM_CYCLE).  Same-start ties sort by (resource, microbatch,
+    position) — the reference's stable order, since a resource meets the same
+    microbatch again only in a later cycle at a higher position."""
+    rec = _sim(plan, profile, cluster, cycle=True)
+    s = _build_schedule(plan, rec)
+    return Schedule(events=s.events, allreduce=s.allreduce, makespan=s.makespan, cycle_count=rec["cycles"])
 
 
 def lemma1_bound(plan: Plan, profile: ModelProfile, cluster: ClusterGraph) -> float:

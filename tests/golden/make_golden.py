@@ -315,6 +315,67 @@ def gen_fileio():
     return {"python": sys.version, "cases": out, "format_number": fmt}
 
 
+def _sim_case_models():
+    sim = json.load(open(os.path.join(HERE, "sim.json")))
+    seen = set()
+    for c in sim["cases"]:
+        spec = c["input"]
+        key = (json.dumps(spec, sort_keys=True), json.dumps(c["plan"]))
+        if key in seen:
+            continue
+        seen.add(key)
+        prof, clu, _ = ref_model(W.InstanceSpec(spec["name"], *[[float.fromhex(x) for x in spec[k]] for k in
+                                                                 ("fwd", "bwd", "param", "efwd", "ebwd")],
+                                                spec["gpu_ids"], [(a, b, float.fromhex(w)) for a, b, w in
+                                                                  spec["links"]], spec["M"]))
+        st = c["plan"]["stages"]
+        plan = P.Plan(tuple(P.Stage(n + 1, a, b, tuple(d)) for n, (a, b, d) in enumerate(st)), c["plan"]["M"])
+        yield c["name"], spec, prof, clu, plan
+
+
+def gen_costs():
+    """cost_summary / channel_times / block_durations / scalar cost helpers /
+    simulate_cycle_schedule through the reference (cost.py, scheduler.py:241-296)."""
+    cases = []
+    extra = []
+    for ws in (W.c2_bert24(M=6), W.c1_vgg19(M=5)):
+        prof, clu, M = ref_model(ws)
+        order = P.rdo(clu)
+        for n in range(1, min(prof.num_layers, clu.num_gpus) + 1):
+            extra.append((f"{ws.name}_gpipe{n}", spec_of(prof, clu, M), prof, clu, P.gpipe_plan(prof, clu, order, n, M)))
+        extra.append((f"{ws.name}_dp", spec_of(prof, clu, M), prof, clu, P.dataparallel_plan(prof, clu, M)))
+    zl = tuple(P.LayerProfile(id=i, fwd_time=0.0 if i % 2 else 1.0, bwd_time=0.0, param_bytes=1e8) for i in range(1, 7))
+    ze = tuple(P.InterLayerEdge(src=i, dst=i + 1, fwd_bytes=0.0, bwd_bytes=1e8 * (i % 2)) for i in range(1, 6))
+    zprof = P.ModelProfile(name="zeros", microbatch_size=1, layers=zl, edges=ze)
+    zclu = P.make_cluster([1, 2, 3, 4], [(a, b, 1e9) for a in range(1, 5) for b in range(a + 1, 5)])
+    for st in (((1, 2, (1,)), (3, 4, (2, 3)), (5, 6, (4,))), ((1, 1, (1,)), (2, 3, (2,)), (4, 6, (3, 4)))):
+        plan = P.Plan(tuple(P.Stage(n + 1, a, b, d) for n, (a, b, d) in enumerate(st)), 4)
+        extra.append((f"zeros{len(extra)}", spec_of(zprof, zclu, 4), zprof, zclu, plan))
+    for name, spec, prof, clu, plan in list(_sim_case_models()) + extra:
+        cs = P.cost_summary(plan, prof, clu)
+        blocks = P.build_block_list(plan)
+        cyc = P.simulate_cycle_schedule(plan, prof, clu)
+        rec = {"name": name, "input": spec, "plan": plan_of(plan),
+               "summary": {"per_stage_compute": {str(k): hx(v) for k, v in cs.per_stage_compute.items()},
+                           "per_channel_comm": {str(k): hx(v) for k, v in cs.per_channel_comm.items()},
+                           "allreduce": {str(k): hx(v) for k, v in cs.allreduce.items()},
+                           "cycle_time": hx(cs.cycle_time), "workload": hx(cs.workload), "gamma": hx(cs.gamma),
+                           "phi": hx(cs.phi)},
+               "channel_times": {str(k): [hx(a), hx(b)] for k, (a, b) in P.channel_times(plan, prof, clu).items()},
+               "block_durations": {str(k): hx(v) for k, v in P.block_durations(blocks, plan, prof, clu).items()},
+               "allreduce_time": [hx(P.allreduce_time(prof, s.layer_start, s.layer_end, s.devices, clu))
+                                  for s in plan.stages],
+               "min_pairwise": [hx(P.min_pairwise_bandwidth(clu, s.devices)) for s in plan.stages],
+               "min_cross": [hx(P.min_cross_bandwidth(clu, a.devices, b.devices))
+                             for a, b in zip(plan.stages, plan.stages[1:])],
+               "interstage": [[hx(x) for x in P.interstage_comm_time(prof, a.layer_end, a.devices, b.devices, clu)]
+                              for a, b in zip(plan.stages, plan.stages[1:])],
+               "gamma": hx(P.gamma(prof, clu)),
+               "cycle": sched_of(cyc), "cycle_count": cyc.cycle_count}
+        cases.append(rec)
+    return {"python": sys.version, "cases": cases}
+
+
 def gen_ordering():
     rng = random.Random(SEED)
     cuts = []
@@ -345,9 +406,9 @@ def gen_ordering():
 
 
 def main():
-    which = sys.argv[1:] or ["pysum", "spp", "prm", "sim", "ordering", "baselines", "fileio"]
+    which = sys.argv[1:] or ["pysum", "spp", "prm", "sim", "ordering", "baselines", "fileio", "costs"]
     gens = {"pysum": gen_pysum, "spp": gen_spp, "prm": gen_prm, "sim": gen_sim, "ordering": gen_ordering,
-            "baselines": gen_baselines, "fileio": gen_fileio}
+            "baselines": gen_baselines, "fileio": gen_fileio, "costs": gen_costs}
     for name in which:
         t0 = time.time()
         data = gens[name]()
