@@ -142,7 +142,8 @@ int pp_prm_query(const pp_batch *b, int32_t n_query, const int32_t *q_inst, cons
 /* per-lane cost record (lane_cost[(lane_off + r) * PP_LANE_COST_FIELDS + f]) */
 #define PP_LANE_COST_FIELDS 7
 /* stage lane: F (FB for the last stage) duration, B duration, stage_compute_time,
- *             allreduce_time (0 unless replicated), stage_fwd_time, stage_bwd_time,
+ *             allreduce_time (0 unless replicated), split F duration and split B
+ *             duration (stage_*_time / k, also for the last stage),
  *             min pairwise bandwidth (+inf for one device)
  * chan lane : X duration (c_fwd), Y duration (c_bwd), c_fwd + c_bwd, 0, 0, 0,
  *             min cross bandwidth                                          */
@@ -197,6 +198,54 @@ int pp_peak_minmax(double *d_out, int32_t iters, int64_t *n_ops, void *stream);
  * verts (device, ascending, n of them); in_a[v] = 1 for side_a; weight[0]. */
 int pp_min_cut(const pp_batch *b, int32_t k, const int32_t *verts, int32_t n, uint8_t *in_a,
                double *weight, void *stream);
+
+/* ---- schedule validation (validate_schedule, scheduler.py:303-452) -------
+ * Expected blocks of an N-stage plan, "expected index" e (scheduler.py:322-338):
+ *   stages n = 1..N : fwd n, bwd n  (the last stage: fwdbwd N alone when merged_last)
+ *   channels n = 1..N-1 : comm_fwd n, comm_bwd n
+ * The host maps every event's label to e (-1 = not an expected block) and
+ * its resource string to res_ok.  Slots are (m-1) * n_exp + e.
+ * Phase 1 (structural, pp_validate_schedule with phase = 1):
+ *   ev_flags[k] : 1 duplicate (not the first event of its slot), 2 ends
+ *                 before it starts, 4 unexpected block, 8 unknown microbatch
+ *   slot_flags  : 1 missing, 2 wrong resource, 4 wrong duration
+ *                 (the LAST event of a slot is the one checked, as by_key keeps it)
+ * Phase 2 (ordering; only meaningful when phase 1 found nothing):
+ *   mn_flags[(m-1)*N + n-1] : bits 0..5 the six channel-n checks of
+ *                 scheduler.py:376-391 in order, bit 6 the last-stage check (:392-393)
+ *   ar_flags[n-1] : 1 missing, 2 starts early, 4 wrong duration, 8 unexpected
+ *   ov_idx / ov_flags : per resource, its events sorted by (start, end, k);
+ *                 ov_flags[j] = 1 when sorted item j overlaps item j-1
+ *   scal[0..3] : expected makespan, forward max, backward min, f_start(1,1)
+ *   stat[0..2] : first-start violated, barrier violated, makespan mismatch
+ * Resources are stage n (lane 2n-2) / chan n (lane 2n-1); res_off[lane] is the
+ * start of the lane's block in ov_idx (M items per expected label it hosts). */
+#define PP_VAL_MERGED_LAST 1
+#define PP_VAL_FORWARD_BARRIER 2
+
+typedef struct {
+    int32_t N, M, flags, n_exp;
+    int64_t n_ev;
+    const int32_t *ev_m, *ev_e;       /* microbatch, expected index (-1 unknown)  */
+    const uint8_t *ev_res_ok;         /* resource string matches e's resource     */
+    const double *ev_start, *ev_end;
+    const double *lane_cost;          /* the plan's PP_LANE_COST_FIELDS records   */
+    const uint8_t *win_has;           /* [N] AllReduce window given for stage n   */
+    const double *win_start, *win_end;/* [N] (the last window given per stage)    */
+    int32_t n_win_all;                /* every window's end enters the makespan   */
+    const double *win_all_end;        /* [n_win_all]                              */
+    double makespan;
+    /* scratch + outputs (device) */
+    int32_t *slot_first, *slot_last, *slot_count;   /* [M*n_exp] */
+    uint8_t *ev_flags, *slot_flags, *mn_flags, *ar_flags, *ov_flags;
+    int32_t *ov_idx;                  /* [M*n_exp] */
+    const int32_t *res_off;           /* [2N] */
+    double *part;                     /* [3*M + N] per-microbatch partials scratch  */
+    double *scal;                     /* [4] */
+    int32_t *stat;                    /* [3] */
+} pp_validate_args;
+
+int pp_validate_schedule(const pp_validate_args *a, int32_t phase, void *stream);
 
 /* ---- trace writer (host) ------------------------------------------------ */
 /* write_trace text (fileio.py:170-188; numbers as format_number, fileio.py:32-38)

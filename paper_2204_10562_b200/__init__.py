@@ -8,6 +8,7 @@ the planning calls raise _lib.BackendUnavailable.
 """
 
 from .baselines import dataparallel_plan, gpipe_plan, gpipe_schedule, noreplication_plan
+from .checker import validate_schedule
 from .cost import (CostSummary, allreduce_time, block_duration, block_durations, channel_times, cost_summary, gamma,
                    interstage_comm_time, min_cross_bandwidth, min_pairwise_bandwidth)
 from .fileio import (Trace, TraceRow, format_number, load_cluster, load_plan, load_profile, parse_trace, read_trace,
@@ -35,5 +36,5 @@ __all__ = [
     "Trace", "TraceRow", "format_number", "load_cluster", "load_plan", "load_profile", "parse_trace", "read_trace",
     "save_cluster", "save_plan", "save_profile", "trace_to_schedule", "write_trace",
     "CostSummary", "allreduce_time", "block_duration", "block_durations", "channel_times", "cost_summary", "gamma",
-    "interstage_comm_time", "min_cross_bandwidth", "min_pairwise_bandwidth", "simulate_cycle_schedule",
+    "interstage_comm_time", "min_cross_bandwidth", "min_pairwise_bandwidth", "simulate_cycle_schedule", "validate_schedule",
 ]

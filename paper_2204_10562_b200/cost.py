@@ -20,7 +20,7 @@ from .model import (BWD, COMM_FWD, FWD, Block, ClusterGraph, InterLayerEdge, Lay
 from .partition import sum_flags
 
 # lane record fields (include/pipeplan_b200.h, PP_LANE_COST_FIELDS)
-_DA, _DB, _CYC, _AR, _SF, _SB, _MBW = range(7)
+_DA, _DB, _CYC, _AR, _FS, _BS, _MBW = range(7)
 
 
 @dataclass(frozen=True)
@@ -209,13 +209,12 @@ def block_durations(blocks: Sequence[Block], plan: Plan, profile: ModelProfile,
         if b.is_compute:
             row = lc[2 * (b.stage - 1)]
             k = plan.stages[b.stage - 1].replication
-            if b.kind == FWD:
-                # F = (sum f / k) / k: the lane's F duration, or its stage_fwd_time / k on the last stage
-                out[b.position] = float(row[_DA]) if b.stage < N else float(row[_SF]) / k
+            if b.kind == FWD:   # F = (sum f / k) / k, also on the last stage
+                out[b.position] = float(row[_FS])
             elif b.kind == BWD:
-                out[b.position] = float(row[_DB]) if b.stage < N else float(row[_SB]) / k
-            else:
-                out[b.position] = float(row[_DA]) if b.stage == N else (float(row[_SF]) + float(row[_SB])) / k
+                out[b.position] = float(row[_BS])
+            else:               # FB = stage_compute_time / k (the lane's FB on the last stage)
+                out[b.position] = float(row[_DA]) if b.stage == N else float(row[_CYC]) / k
         else:
             row = lc[2 * b.channel - 1]
             out[b.position] = float(row[_DA] if b.kind == COMM_FWD else row[_DB])

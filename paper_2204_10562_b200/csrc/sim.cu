@@ -57,7 +57,7 @@ struct LaneCost {
     double cyc;         // per-stage compute or per-channel comm (cost_summary)
     double ar;          // AllReduce time (replicated stages)
     bool has_ar;
-    double sf, sb;      // stage_fwd_time / stage_bwd_time (cost.py:44-53); 0 on channels
+    double fs, bs;      // split F / B durations (stage_*_time / k, cost.py:215-218) of ANY stage; 0 on channels
     double mbw;         // min pairwise (stage) / min cross (chan) bandwidth (cost.py:64-80)
 };
 
@@ -72,8 +72,8 @@ __device__ LaneCost lane_cost(const P& p, const InstView& I, int N, int lane) {
         if (n < N) { c.dA = sf / (double)k; c.dB = sb / (double)k; }             // cost.py:215-218
         else { c.dA = (sf + sb) / (double)k; c.dB = c.dA; }                      // cost.py:219-220
         c.cyc = sf + sb;                                                          // cost.py:56-61
-        c.sf = sf;
-        c.sb = sb;
+        c.fs = sf / (double)k;
+        c.bs = sb / (double)k;
         if (k >= 2) {
             const double total = pysum(I.par + a - 1, e - a + 1, I.naive);
             double mp = PP_INF;
@@ -268,7 +268,7 @@ __device__ void plan_costs(const LaneCost& c, int lane, int R, int M, int nthr, 
     if (lane < R && lane_out) {
         double* o = lane_out + (int64_t)lane * PP_LANE_COST_FIELDS;
         o[0] = c.dA; o[1] = c.dB; o[2] = c.cyc; o[3] = c.has_ar ? c.ar : 0.0;
-        o[4] = c.sf; o[5] = c.sb; o[6] = c.mbw;
+        o[4] = c.fs; o[5] = c.bs; o[6] = c.mbw;
     }
     if (!o_workload) return;
     double w = -PP_INF;

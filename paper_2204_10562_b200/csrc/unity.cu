@@ -3,3 +3,4 @@
 #include "sim.cu"
 #include "capi.cu"
 #include "trace.cu"
+#include "validate.cu"

@@ -376,6 +376,80 @@ def gen_costs():
     return {"python": sys.version, "cases": cases}
 
 
+def _perturb(rng, sched, plan):
+    """A few deterministic corruptions of a valid schedule (each a separate case)."""
+    ev = list(sched.events)
+    E = len(ev)
+    out = [("valid", sched)]
+
+    def mk(name, events=None, allreduce=None, makespan=None):
+        out.append((name, P.Schedule(events=tuple(ev if events is None else events),
+                                     allreduce=tuple(sched.allreduce if allreduce is None else allreduce),
+                                     makespan=sched.makespan if makespan is None else makespan)))
+
+    k = rng.randrange(E)
+    e = ev[k]
+    sh = 0.5 * (e.end - e.start) + 1e-3
+    mk("shift", ev[:k] + [P.ScheduleEvent(e.resource, e.microbatch, e.block, e.start - sh, e.end - sh)] + ev[k + 1:])
+    mk("late", ev[:k] + [P.ScheduleEvent(e.resource, e.microbatch, e.block, e.start + sh, e.end + sh)] + ev[k + 1:])
+    mk("drop", ev[:k] + ev[k + 1:])
+    mk("dup", ev[:k + 1] + [e] + ev[k + 1:])
+    mk("resource", ev[:k] + [P.ScheduleEvent("stage99", e.microbatch, e.block, e.start, e.end)] + ev[k + 1:])
+    mk("duration", ev[:k] + [P.ScheduleEvent(e.resource, e.microbatch, e.block, e.start, e.end + 0.25)] + ev[k + 1:])
+    mk("unknown_block", ev + [P.ScheduleEvent("stage1", 1, "fwd99", 0.0, 1.0)])
+    mk("unknown_micro", ev + [P.ScheduleEvent(e.resource, plan.microbatch_count + 3, e.block, 0.0, 1.0)])
+    mk("backwards", ev[:k] + [P.ScheduleEvent(e.resource, e.microbatch, e.block, e.end + 1.0, e.start)] + ev[k + 1:])
+    mk("makespan", makespan=sched.makespan * 1.5 + 1.0)
+    mk("swap_starts", sorted((P.ScheduleEvent(x.resource, x.microbatch, x.block, x.start * 0.5, x.start * 0.5 +
+                                              (x.end - x.start)) for x in ev), key=lambda x: x.start))
+    mk("extra_window", allreduce=tuple(sched.allreduce) + (P.AllReduceWindow(1, sched.makespan, sched.makespan + 1),))
+    if sched.allreduce:
+        w = sched.allreduce[0]
+        mk("no_window", allreduce=tuple(sched.allreduce[1:]))
+        mk("early_window", allreduce=(P.AllReduceWindow(w.stage, w.start - 1.0, w.end - 1.0),) +
+           tuple(sched.allreduce[1:]))
+    mk("reversed", list(reversed(ev)))
+    return out
+
+
+def gen_validate():
+    """validate_schedule messages through the reference on valid and corrupted schedules."""
+    rng = random.Random(77)
+    cases = []
+    for name, spec, prof, clu, plan in _sim_case_models():
+        if name.startswith("tiny_circular") or name.startswith("tiny_missing"):
+            continue
+        for barrier in (False, True):
+            if barrier and any(s.replicated for s in plan.stages):
+                continue
+            sched = (P.gpipe_schedule(plan, prof, clu) if barrier else P.simulate_pe(plan, prof, clu))
+            for kind, s2 in _perturb(rng, sched, plan):
+                msgs = P.validate_schedule(s2, plan, prof, clu, forward_barrier=barrier)
+                cases.append({"name": f"{name}_{'gpipe' if barrier else 'pe'}_{kind}", "input": spec,
+                              "plan": plan_of(plan), "forward_barrier": barrier, "schedule": sched_of(s2),
+                              "messages": msgs})
+    # cross-checks: a PE schedule under the barrier rule, a split last stage
+    prof, clu, M = tiny_profile(), tiny_cluster(), 2
+    plan = P.Plan((P.Stage(1, 1, 1, (1,)), P.Stage(2, 2, 2, (2,))), M)
+    pe = P.simulate_pe(plan, prof, clu)
+    cases.append({"name": "tiny_pe_under_barrier", "input": spec_of(prof, clu, M), "plan": plan_of(plan),
+                  "forward_barrier": True, "schedule": sched_of(pe),
+                  "messages": P.validate_schedule(pe, plan, prof, clu, forward_barrier=True)})
+    split = []
+    for e in pe.events:
+        if e.block == "fwdbwd2":
+            mid = e.start + 1.0
+            split.append(P.ScheduleEvent(e.resource, e.microbatch, "fwd2", e.start, mid))
+            split.append(P.ScheduleEvent(e.resource, e.microbatch, "bwd2", mid, e.end))
+        else:
+            split.append(e)
+    ss = P.Schedule(events=tuple(split), allreduce=pe.allreduce, makespan=pe.makespan)
+    cases.append({"name": "tiny_split_last", "input": spec_of(prof, clu, M), "plan": plan_of(plan),
+                  "forward_barrier": False, "schedule": sched_of(ss),
+                  "messages": P.validate_schedule(ss, plan, prof, clu)})
+    return {"python": sys.version, "cases": cases}
+
+
 def gen_ordering():
     rng = random.Random(SEED)
     cuts = []
@@ -406,9 +480,9 @@ def gen_ordering():
 
 
 def main():
-    which = sys.argv[1:] or ["pysum", "spp", "prm", "sim", "ordering", "baselines", "fileio", "costs"]
+    which = sys.argv[1:] or ["pysum", "spp", "prm", "sim", "ordering", "baselines", "fileio", "costs", "validate"]
     gens = {"pysum": gen_pysum, "spp": gen_spp, "prm": gen_prm, "sim": gen_sim, "ordering": gen_ordering,
-            "baselines": gen_baselines, "fileio": gen_fileio, "costs": gen_costs}
+            "baselines": gen_baselines, "fileio": gen_fileio, "costs": gen_costs, "validate": gen_validate}
     for name in which:
         t0 = time.time()
         data = gens[name]()
