@@ -85,7 +85,7 @@ class PPSimBatch(C.Structure):
 
 EXPORTS = ("pp_version", "pp_last_error", "pp_device_count", "pp_layout", "pp_rdo", "pp_prm",
            "pp_pe_sweep", "pp_select", "pp_spp", "pp_prm_query", "pp_simulate", "pp_min_cut",
-           "pp_launch_count", "pp_phi", "pp_peak_minmax", "pp_format_trace")
+           "pp_launch_count", "pp_phi", "pp_peak_minmax", "pp_format_trace", "pp_validate_schedule")
 
 _lib = None
 
@@ -129,6 +129,8 @@ def _declare(L):
     L.pp_format_trace.argtypes = [C.c_int64, vp, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, C.c_double, vp,
                                   C.c_int64, vp, i32]
     L.pp_format_trace.restype = C.c_int
+    L.pp_validate_schedule.argtypes = [vp, i32, vp]
+    L.pp_validate_schedule.restype = C.c_int
 
 
 def check(rc):
