@@ -85,7 +85,8 @@ class PPSimBatch(C.Structure):
 
 EXPORTS = ("pp_version", "pp_last_error", "pp_device_count", "pp_layout", "pp_rdo", "pp_prm",
            "pp_pe_sweep", "pp_select", "pp_spp", "pp_prm_query", "pp_simulate", "pp_min_cut",
-           "pp_launch_count", "pp_phi", "pp_peak_minmax", "pp_format_trace", "pp_validate_schedule")
+           "pp_launch_count", "pp_phi", "pp_peak_minmax", "pp_format_trace", "pp_validate_schedule",
+           "pp_rdo_set_rounds")
 
 _lib = None
 
@@ -131,6 +132,17 @@ def _declare(L):
     L.pp_format_trace.restype = C.c_int
     L.pp_validate_schedule.argtypes = [vp, i32, vp]
     L.pp_validate_schedule.restype = C.c_int
+    L.pp_rdo_set_rounds.argtypes = [i32]
+    L.pp_rdo_set_rounds.restype = C.c_int
+
+
+def rdo_rounds(rounds: int) -> int:
+    """Set the speculative RDO round count (0 = sequential recursion only);
+    returns the previous value.  The order is identical either way."""
+    prev = load(require_device=False).pp_rdo_set_rounds(int(rounds))
+    if prev < 0:
+        check(prev)
+    return prev
 
 
 def check(rc):

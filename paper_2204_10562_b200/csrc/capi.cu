@@ -21,7 +21,9 @@ __global__ void k_combine_s(pp_batch b, int j);
 __global__ void k_backtrack(pp_batch b);
 __global__ void k_query(pp_batch b, int n, const int* qi, const int* ql, const int* qx, const int* qr,
                         const int* qd, int max_xi, double* w, int* frag, int* feas);
-template <bool SMEM> __global__ void k_rdo(pp_batch b);
+template <bool SMEM> __global__ void k_rdo(pp_batch b, int resume);
+__global__ void k_rdo_plan(pp_batch b, int round, int predict);
+template <bool SMEM> __global__ void k_rdo_cut(pp_batch b);
 template <bool SMEM>
 __global__ void k_min_cut(pp_batch b, int k, const int* verts, int n, unsigned char* in_a, double* weight);
 __global__ void k_pe_sweep(pp_batch b);
@@ -111,17 +113,41 @@ int pp_layout(int32_t n, const int32_t* L, const int32_t* V, const int32_t* M, c
     return PP_OK;
 }
 
+// Speculative rounds before the sequential finisher (rdo.cu); 0 = sequential only.
+static std::atomic<int> g_rdo_rounds{3};
+
+int pp_rdo_set_rounds(int32_t rounds) {
+    if (rounds < 0 || rounds > 64) return fail(PP_EINVAL, "rdo rounds %d outside 0..64", rounds);
+    return g_rdo_rounds.exchange(rounds);
+}
+
 int pp_rdo(const pp_batch* b, void* stream) {
     if (b->n_inst <= 0) return PP_OK;
     const int V = b->max_V;
-    const int in_smem = V <= 128;
+    const int in_smem = V <= RDO_SMEM_MAX;
+    const int rounds = V >= 2 ? g_rdo_rounds.load() : 0;
+    if (rounds > 0) {
+        const size_t plan_smem = sizeof(int) * (size_t)V * (3 + RDO_WARPS);
+        const size_t cut_smem = (in_smem ? sizeof(double) * V * V : 0) + sizeof(int) * V + V + 16;
+        cudaFuncSetAttribute(k_rdo_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan_smem);
+        if (in_smem) cudaFuncSetAttribute(k_rdo_cut<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cut_smem);
+        const dim3 gc(b->n_inst, V - 1);
+        for (int r = 0; r <= rounds; ++r) {
+            k_rdo_plan<<<b->n_inst, 32 * RDO_WARPS, plan_smem, S(stream)>>>(*b, r, r < rounds);
+            PP_CHECK_LAUNCH("k_rdo_plan");
+            if (r == rounds) break;
+            if (in_smem) k_rdo_cut<true><<<gc, 32, cut_smem, S(stream)>>>(*b);
+            else k_rdo_cut<false><<<gc, 32, cut_smem, S(stream)>>>(*b);
+            PP_CHECK_LAUNCH("k_rdo_cut");
+        }
+    }
     const size_t smem = (in_smem ? sizeof(double) * V * V : 0) + rdo_state_bytes(V);
     if (in_smem) {
         cudaFuncSetAttribute(k_rdo<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_rdo<true><<<b->n_inst, 128, smem, S(stream)>>>(*b);
+        k_rdo<true><<<b->n_inst, 32 * RDO_WARPS, smem, S(stream)>>>(*b, rounds > 0);
     } else {
         cudaFuncSetAttribute(k_rdo<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_rdo<false><<<b->n_inst, 128, smem, S(stream)>>>(*b);
+        k_rdo<false><<<b->n_inst, 32 * RDO_WARPS, smem, S(stream)>>>(*b, rounds > 0);
     }
     PP_CHECK_LAUNCH("k_rdo");
     return PP_OK;
@@ -320,7 +346,7 @@ int pp_min_cut(const pp_batch* b, int32_t k, const int32_t* verts, int32_t n, ui
                void* stream) {
     if (n < 2) return fail(PP_EINVAL, "min cut needs at least 2 vertices");
     const int V = b->max_V;
-    const int in_smem = V <= 128;
+    const int in_smem = V <= RDO_SMEM_MAX;
     const size_t smem = (in_smem ? sizeof(double) * V * V : 0) + rdo_state_bytes(V);
     if (in_smem) {
         cudaFuncSetAttribute(k_min_cut<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -1,6 +1,6 @@
-// prm.cu — device ordering (RDO), DP tables and the PRM dynamic program.
+// prm.cu — DP tables and the PRM dynamic program.
 //
-// Reference: ordering.py:30-113 (Stoer-Wagner RDO), partition.py:41-162
+// Reference: partition.py:41-162
 // (W(l, xi, r, i) recursion), cost.py:64-99 (bandwidth minima, AllReduce).
 //
 // The DP runs as a wavefront over the device prefix i (W(., ., ., i) needs
@@ -913,209 +913,5 @@ __global__ void __launch_bounds__(32) k_query(pp_batch b, int n, const int* qi, 
         fr[4 * n2 + 0] = s_ls[n2]; fr[4 * n2 + 1] = s_le[n2]; fr[4 * n2 + 2] = s_dlo[n2]; fr[4 * n2 + 3] = s_dhi[n2];
     }
 }
-
-// ----------------------------------------------------------------------------
-// RDO (ordering.py:30-113).  One CTA per instance; each warp runs the
-// Stoer-Wagner min cut of one vertex group (a node of the recursion tree);
-// groups of one recursion level are cut concurrently by different warps.
-// A group is identified by its lowest rank `lo`; every vertex stores the lo
-// of its current group, so the final rank of vertex v is lo[v].
-//
-// Inside a cut, vertex k of the group (k = position in the ascending member
-// list, so local order == GPU-id order) lives on lane k % 32, register slot
-// k / 32: adjacency, supernode and flags never touch memory.  The group's
-// weights are a local n x n matrix (shared memory when the instance fits,
-// else the instance's global scratch), rebuilt from the cluster for every
-// cut as the reference does (ordering.py:50-54).  Arg-max per step: the
-// adjacencies are positive doubles, which order like their uint64 bit
-// patterns, so the max is two 32-bit __reduce_max_sync (high word, then low
-// word among high-word winners) and the reference's smallest-id tie rule
-// (ordering.py:66) is a __reduce_min_sync over the tied local indices.
-// ----------------------------------------------------------------------------
-template <int SLOTS>
-__device__ __forceinline__ double warp_min_cut_t(double* wl, const double* bw, int V, const int* mem, int n,
-                                                 unsigned char* side_out) {
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    for (int e = lane; e < n * n; e += 32) {
-        const int a = e / n, c = e - a * n;
-        wl[e] = (a == c) ? 0.0 : bw[(int64_t)mem[a] * V + mem[c]];
-    }
-    __syncwarp();
-    double adj[SLOTS];
-    int grp[SLOTS];
-    bool alive[SLOTS], inadj[SLOTS], side[SLOTS];
-#pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-        const int k = lane + 32 * s;
-        alive[s] = k < n; grp[s] = k; side[s] = false; inadj[s] = false; adj[s] = 0.0;
-    }
-    double best_weight = PP_INF;
-    for (int n_alive = n; n_alive > 1; --n_alive) {
-#pragma unroll
-        for (int s = 0; s < SLOTS; ++s) {   // phase starts at the smallest id (ordering.py:61-64)
-            const int k = lane + 32 * s;
-            inadj[s] = alive[s] && k != 0;
-            if (inadj[s]) adj[s] = wl[k];
-        }
-        int sv = 0, tv = 0;
-        double cut = 0.0;
-        for (int step = 0; step < n_alive - 1; ++step) {
-            unsigned long long bu = 0ull;
-            int bk = 0x7fffffff;
-#pragma unroll
-            for (int s = 0; s < SLOTS; ++s) {
-                const unsigned long long u = (unsigned long long)__double_as_longlong(adj[s]);
-                if (inadj[s] && u > bu) { bu = u; bk = lane + 32 * s; }
-            }
-            // (ties are the common case on structured clusters: three REDUX beat ballot fast paths)
-            const unsigned hi = (unsigned)(bu >> 32), lo = (unsigned)bu;
-            const unsigned mhi = __reduce_max_sync(FULL, hi);
-            const unsigned mlo = __reduce_max_sync(FULL, hi == mhi ? lo : 0u);
-            const bool win = bk != 0x7fffffff && hi == mhi && lo == mlo;
-            const int nk = (int)__reduce_min_sync(FULL, win ? (unsigned)bk : 0x7fffffffu);
-            cut = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
-            sv = tv; tv = nk;
-            const double* row = wl + nk * n;
-#pragma unroll
-            for (int s = 0; s < SLOTS; ++s) {   // adj[u] += wt(next_v, u)  (ordering.py:69-70)
-                const int k = lane + 32 * s;
-                if (k == nk) inadj[s] = false;
-                if (inadj[s]) adj[s] = adj[s] + row[k];
-            }
-        }
-        if (cut < best_weight) {   // first minimum cut-of-phase (ordering.py:73-75)
-            best_weight = cut;
-#pragma unroll
-            for (int s = 0; s < SLOTS; ++s) side[s] = (grp[s] == tv);
-        }
-        const int merged = min(sv, tv), other = max(sv, tv);   // ordering.py:77-85
-#pragma unroll
-        for (int s = 0; s < SLOTS; ++s) {
-            const int u = lane + 32 * s;
-            if (alive[s] && u != sv && u != tv) {
-                const double x = wl[sv * n + u] + wl[tv * n + u];
-                wl[merged * n + u] = x;
-                wl[u * n + merged] = x;
-            }
-        }
-        __syncwarp();
-#pragma unroll
-        for (int s = 0; s < SLOTS; ++s) {
-            if (grp[s] == other) grp[s] = merged;
-            if (lane + 32 * s == other) alive[s] = false;
-        }
-    }
-    // the side holding the smallest id becomes side_a (ordering.py:87-91)
-    const bool low = __shfl_sync(FULL, side[0], 0);
-#pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-        const int k = lane + 32 * s;
-        if (k < n) side_out[k] = low ? side[s] : !side[s];
-    }
-    __syncwarp();
-    return best_weight;
-}
-
-__device__ __forceinline__ double warp_min_cut(double* wl, const double* bw, int V, const int* mem, int n,
-                                               unsigned char* side) {
-    if (n <= 32) return warp_min_cut_t<1>(wl, bw, V, mem, n, side);
-    if (n <= 64) return warp_min_cut_t<2>(wl, bw, V, mem, n, side);
-    if (n <= 128) return warp_min_cut_t<4>(wl, bw, V, mem, n, side);
-    if (n <= 256) return warp_min_cut_t<8>(wl, bw, V, mem, n, side);
-    return warp_min_cut_t<16>(wl, bw, V, mem, n, side);
-}
-
-// SMEM: the contracted weights live in shared memory (V <= 128); a template
-// parameter so the compiler sees the address space and emits LDS/STS.
-template <bool SMEM>
-__global__ void __launch_bounds__(32 * RDO_WARPS) k_rdo(pp_batch b) {
-    const pp_instance I = b.inst[blockIdx.x];
-    if (I.flags & PP_GIVEN_ORDER) return;
-    const int V = I.V;
-    extern __shared__ double smem_d[];
-    char* sm = (char*)smem_d;
-    double* W;
-    if constexpr (SMEM) { W = smem_d; sm += sizeof(double) * V * V; }
-    else W = b.ws + I.ws_off + ws_layout(I.L, V).rdo_w;
-    int* lo = (int*)sm;      sm += sizeof(int) * V;
-    int* cnt = (int*)sm;     sm += sizeof(int) * V;
-    int* first = (int*)sm;   sm += sizeof(int) * V;
-    int* glist = (int*)sm;   sm += sizeof(int) * V;
-    int* goff = (int*)sm;    sm += sizeof(int) * V;
-    int* memall = (int*)sm;  sm += sizeof(int) * V * RDO_WARPS;
-    unsigned char* sideall = (unsigned char*)sm;
-    const double* bw = b.bw + I.bw_off;
-    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-    for (int v = t; v < V; v += blockDim.x) lo[v] = 1;
-    __syncthreads();
-    __shared__ int s_ngroups;
-    for (;;) {
-        for (int v = t; v < V; v += blockDim.x) { cnt[v] = 0; first[v] = 0x7fffffff; }
-        if (t == 0) s_ngroups = 0;
-        __syncthreads();
-        for (int v = t; v < V; v += blockDim.x) { atomicAdd(&cnt[lo[v] - 1], 1); atomicMin(&first[lo[v] - 1], v); }
-        __syncthreads();
-        for (int v = t; v < V; v += blockDim.x) {
-            const int g = lo[v];
-            if (cnt[g - 1] >= 2 && first[g - 1] == v) glist[atomicAdd(&s_ngroups, 1)] = g;
-        }
-        __syncthreads();
-        const int ng = s_ngroups;
-        if (ng == 0) break;
-        if (t == 0) {   // disjoint groups: sum of n^2 <= V^2 fits the V x V region
-            int o = 0;
-            for (int gi = 0; gi < ng; ++gi) { goff[gi] = o; const int c = cnt[glist[gi] - 1]; o += c * c; }
-        }
-        __syncthreads();
-        for (int gi = warp; gi < ng; gi += RDO_WARPS) {
-            const int g = glist[gi];
-            int* mem = memall + warp * V;
-            unsigned char* side = sideall + warp * V;
-            int n = 0;
-            for (int v0 = 0; v0 < V; v0 += 32) {   // ascending member list
-                const int v = v0 + lane;
-                const bool in = v < V && lo[v] == g;
-                const unsigned m = __ballot_sync(0xffffffffu, in);
-                if (in) mem[n + __popc(m & ((1u << lane) - 1))] = v;
-                n += __popc(m);
-            }
-            __syncwarp();
-            warp_min_cut(W + goff[gi], bw, V, mem, n, side);
-            int na = 0;
-            for (int k0 = 0; k0 < n; k0 += 32) {
-                const int k = k0 + lane;
-                na += __popc(__ballot_sync(0xffffffffu, k < n && side[k]));
-            }
-            for (int k = lane; k < n; k += 32) lo[mem[k]] = side[k] ? g : g + na;
-            __syncwarp();
-        }
-        __syncthreads();
-    }
-    int* order = b.order + I.order_off;
-    for (int v = t; v < V; v += blockDim.x) order[lo[v] - 1] = v;
-}
-
-// global_min_cut on a vertex subset (ordering.py:30-91): one warp.
-template <bool SMEM>
-__global__ void __launch_bounds__(32) k_min_cut(pp_batch b, int k, const int* verts, int n, unsigned char* in_a,
-                                                double* weight) {
-    const pp_instance I = b.inst[k];
-    const int V = I.V;
-    extern __shared__ double smem_d[];
-    char* sm = (char*)smem_d;
-    double* W;
-    if constexpr (SMEM) { W = smem_d; sm += sizeof(double) * V * V; }
-    else W = b.ws + I.ws_off + ws_layout(I.L, V).rdo_w;
-    int* mem = (int*)sm;
-    for (int q = threadIdx.x; q < n; q += 32) mem[q] = verts[q];
-    __syncwarp();
-    const double cw = warp_min_cut(W, b.bw + I.bw_off, V, mem, n, in_a);
-    if (threadIdx.x == 0) weight[0] = cw;
-}
-template __global__ void k_rdo<true>(pp_batch);
-template __global__ void k_rdo<false>(pp_batch);
-template __global__ void k_min_cut<true>(pp_batch, int, const int*, int, unsigned char*, double*);
-template __global__ void k_min_cut<false>(pp_batch, int, const int*, int, unsigned char*, double*);
 
 }  // namespace pp

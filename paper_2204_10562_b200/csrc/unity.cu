@@ -1,5 +1,6 @@
 // Single translation unit for libpipeplan_b200.so.
 #include "prm.cu"
+#include "rdo.cu"
 #include "sim.cu"
 #include "capi.cu"
 #include "trace.cu"

@@ -1,0 +1,114 @@
+"""Speculative RDO (rdo.cu) vs the reference goldens and the C oracle.
+
+The speculative rounds only decide which exact cuts are computed in
+parallel, so the order must equal the reference's for every round count —
+including clusters whose recursion tree is not a chain (prediction misses),
+ties everywhere (uniform bandwidths) and V > 128 (global-memory cut scratch).
+"""
+
+import random
+
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import fx, load
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2204_10562_b200")
+from paper_2204_10562_b200 import _lib, spp_many, workloads as W  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    _lib.load()
+
+
+@pytest.fixture
+def rounds():
+    prev = _lib.rdo_rounds(3)
+    yield _lib.rdo_rounds
+    _lib.rdo_rounds(prev)
+
+
+def oracle_order(ids, links):
+    ids = sorted(ids)
+    pos = {g: k for k, g in enumerate(ids)}
+    V = len(ids)
+    bw = np.zeros((V, V))
+    for a, b, w in links:
+        bw[pos[a], pos[b]] = bw[pos[b], pos[a]] = w
+    one = np.ones(1)
+    inst = O.Instance(one, one, one, np.zeros(0), np.zeros(0), bw, 1)
+    return tuple(ids[k] for k in O.rdo(inst))
+
+
+def clique(ids, fn):
+    return [(a, b, fn(a, b)) for i, a in enumerate(ids) for b in ids[i + 1:]]
+
+
+def clusters():
+    rng = random.Random(2204)
+    out = []
+    for nodes, per in ((8, 8), (4, 4), (3, 5), (2, 2), (5, 3), (16, 8), (6, 7)):
+        ids, links = W.two_tier_cluster(nodes, per)
+        out.append((f"tier{nodes}x{per}", ids, links))
+    spec = W.c2_bert24()
+    out.append(("dgx1", spec.gpu_ids, spec.links))
+    for V in (2, 3, 5, 8, 13, 16, 31, 32, 33, 47, 64, 65, 100):
+        ids = list(range(1, V + 1))
+        out.append((f"rand{V}", ids, clique(ids, lambda a, b: W._logu(rng, 1e8, 1e11))))
+    for V in (7, 24, 64):   # every cut ties: the first-found rules decide everything
+        ids = list(range(1, V + 1))
+        out.append((f"uniform{V}", ids, clique(ids, lambda a, b: 25e9)))
+    # two dense blocks joined weakly: balanced splits, so chain predictions miss
+    ids = list(range(1, 41))
+    out.append(("blocks", ids, clique(ids, lambda a, b: 100e9 if (a <= 17) == (b <= 17) else rng.uniform(1e9, 2e9))))
+    # non-contiguous ids, shuffled per-node structure
+    ids = [3 * k + 7 for k in range(30)]
+    grp = {g: rng.randrange(4) for g in ids}
+    out.append(("sparse-ids", ids, clique(ids, lambda a, b: 300e9 if grp[a] == grp[b] else rng.choice((10e9, 12e9)))))
+    return out
+
+
+@pytest.mark.parametrize("n_rounds", [0, 1, 2, 3, 8])
+def test_rdo_every_round_count_matches_oracle(rounds, n_rounds):
+    rounds(n_rounds)
+    for name, ids, links in clusters():
+        got = P.rdo(P.make_cluster(ids, links)).order
+        assert got == oracle_order(ids, links), (name, n_rounds)
+
+
+def test_rdo_goldens_with_speculation(rounds):
+    for n_rounds in (1, 3):
+        rounds(n_rounds)
+        for case in load("ordering")["rdo"]:
+            clu = P.make_cluster(case["gpu_ids"], [(a, b, fx(w)) for a, b, w in case["links"]])
+            assert list(P.rdo(clu).order) == case["order"]
+
+
+def test_rdo_global_scratch_path(rounds):
+    """V > 128: contracted weights per chain item live in the workspace."""
+    rng = random.Random(7)
+    ids, links = W.two_tier_cluster(18, 8)   # V = 144
+    rand = list(range(1, 161))
+    cases = [("tier18x8", ids, links),
+             ("rand160", rand, clique(rand, lambda a, b: W._logu(rng, 1e8, 1e11)))]
+    for n_rounds in (0, 3):
+        rounds(n_rounds)
+        for name, i, l in cases:
+            assert P.rdo(P.make_cluster(i, l)).order == oracle_order(i, l), (name, n_rounds)
+
+
+def test_spp_batch_orders_with_speculation(rounds):
+    """spp_many over mixed clusters (C3, C4 random, C2): orders equal the oracle's."""
+    specs = [W.c3_gpt96(8), W.c2_bert24()] + W.c4_batch(24)
+    for n_rounds in (0, 3):
+        rounds(n_rounds)
+        res = spp_many(W.models_of(specs))
+        for s, r in zip(specs, res):
+            assert r.device_order == oracle_order(s.gpu_ids, s.links), (s.name, n_rounds)
