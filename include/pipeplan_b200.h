@@ -114,6 +114,24 @@ int pp_rdo_set_rounds(int32_t rounds);
  * (partition.py:41-162): fills sweep_w, sweep_r, stage_*. */
 int pp_prm(const pp_batch *b, void *stream);
 
+/* DP schedule for batches inside the shared-memory limits (L, V <= 128):
+ * 1 = one persistent dependency-driven kernel, 0 = one launch pair per
+ * wavefront step, 2 (default) = persistent for batches of <= 6 instances.
+ * Bit-identical results; a performance / test knob.  Returns the previous
+ * mode.  Process-wide. */
+int pp_dp_set_persistent(int32_t mode);
+
+/* Combine early exit (default 1): for stage-term triangles certified
+ * non-increasing in l', the (min, max) fold scans l' downward and stops once no
+ * remaining candidate can lower a cell.  Identical results; a test knob.
+ * Returns the previous value (needs a device: the flag is device state). */
+int pp_dp_set_early_exit(int32_t on);
+
+/* Debug: record the persistent DP's per-task timeline (4 x u64 per task:
+ * smid << 32 | kind, fetch, inputs-ready, end; globaltimer ns) into the device
+ * buffer d_buf of 4 * cap entries; NULL disables.  Not on the planning path. */
+int pp_dp_trace(uint64_t *d_buf, int32_t cap);
+
 /* simulate_pe + lemma1_bound for every feasible xi plan (scheduler.py:75-238):
  * fills sweep_mk, sweep_bound. */
 int pp_pe_sweep(const pp_batch *b, void *stream);

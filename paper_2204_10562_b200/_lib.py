@@ -86,7 +86,8 @@ class PPSimBatch(C.Structure):
 EXPORTS = ("pp_version", "pp_last_error", "pp_device_count", "pp_layout", "pp_rdo", "pp_prm",
            "pp_pe_sweep", "pp_select", "pp_spp", "pp_prm_query", "pp_simulate", "pp_min_cut",
            "pp_launch_count", "pp_phi", "pp_peak_minmax", "pp_format_trace", "pp_validate_schedule",
-           "pp_rdo_set_rounds")
+           "pp_rdo_set_rounds", "pp_dp_set_persistent", "pp_dp_trace",
+           "pp_dp_set_early_exit")
 
 _lib = None
 
@@ -134,6 +135,27 @@ def _declare(L):
     L.pp_validate_schedule.restype = C.c_int
     L.pp_rdo_set_rounds.argtypes = [i32]
     L.pp_rdo_set_rounds.restype = C.c_int
+    L.pp_dp_set_persistent.argtypes = [i32]
+    L.pp_dp_set_persistent.restype = C.c_int
+    L.pp_dp_set_early_exit.argtypes = [i32]
+    L.pp_dp_set_early_exit.restype = C.c_int
+    L.pp_dp_trace.argtypes = [vp, i32]
+    L.pp_dp_trace.restype = C.c_int
+
+
+def dp_persistent(mode) -> int:
+    """DP schedule: True/1 persistent kernel, False/0 per-step launches, 2 auto
+    (default: persistent for small batches).  Returns the previous mode.
+    Results are identical either way."""
+    return int(load(require_device=False).pp_dp_set_persistent(int(mode)))
+
+
+def dp_early_exit(on: bool) -> bool:
+    """Toggle the combine's certified early exit; returns the previous setting."""
+    prev = load().pp_dp_set_early_exit(1 if on else 0)
+    if prev < 0:
+        check(prev)
+    return bool(prev)
 
 
 def rdo_rounds(rounds: int) -> int:

@@ -18,6 +18,8 @@ __global__ void k_expand_s(pp_batch b, int j);
 __global__ void k_sdedup(pp_batch b);
 __global__ void k_stab(pp_batch b);
 __global__ void k_combine_s(pp_batch b, int j);
+__global__ void k_dp_reset(pp_batch b);
+__global__ void k_dp_persist(pp_batch b);
 __global__ void k_backtrack(pp_batch b);
 __global__ void k_query(pp_batch b, int n, const int* qi, const int* ql, const int* qx, const int* qr,
                         const int* qd, int max_xi, double* w, int* frag, int* feas);
@@ -167,8 +169,67 @@ struct SideStreams {
 };
 static thread_local SideStreams g_side;
 
+// Shared-memory-path DP schedule (same bits either way):
+//   1 = one persistent dependency-driven kernel (dp_persist.cu): the critical
+//       chain runs ahead, so small batches finish sooner (latency);
+//   0 = the launch-per-step wavefront (prm_chain): better throughput once the
+//       batch fills the GPU on its own;
+//   2 = auto (default): persistent for batches of <= PP_DP_PERSIST_MAX instances.
+static constexpr int PP_DP_PERSIST_MAX = 6;
+static std::atomic<int> g_dp_persist{2};
+
+int pp_dp_set_persistent(int32_t mode) { return g_dp_persist.exchange(mode < 0 ? 2 : (mode > 2 ? 2 : mode)); }
+
+int pp_dp_set_early_exit(int32_t on) {
+    int prev = 1, v = on ? 1 : 0;
+    if (cudaMemcpyFromSymbol(&prev, g_combine_early_exit, sizeof(int)) != cudaSuccess ||
+        cudaMemcpyToSymbol(g_combine_early_exit, &v, sizeof(int)) != cudaSuccess)
+        return fail(PP_ECUDA, "pp_dp_set_early_exit: %s", cudaGetErrorString(cudaGetLastError()));
+    return prev;
+}
+
+// Debug: per-task timeline of the persistent DP into a caller device buffer of
+// 4 * cap u64 (NULL / 0 disables).  Not part of the planning path.
+int pp_dp_trace(uint64_t* d_buf, int32_t cap) {
+    unsigned long long* p = reinterpret_cast<unsigned long long*>(d_buf);
+    if (cudaMemcpyToSymbol(g_dp_trace, &p, sizeof(p)) != cudaSuccess ||
+        cudaMemcpyToSymbol(g_dp_trace_cap, &cap, sizeof(cap)) != cudaSuccess)
+        return fail(PP_ECUDA, "pp_dp_trace: %s", cudaGetErrorString(cudaGetLastError()));
+    return PP_OK;
+}
+
+static int prm_prep(const pp_batch* b, void* stream);
+
+static int prm_persist(const pp_batch* b, void* stream) {
+    const int maxL = b->max_L, maxV = b->max_V;
+    int rc;
+    if ((rc = prm_prep(b, stream))) return rc;
+    k_dp_reset<<<b->n_inst, 128, 0, S(stream)>>>(*b);
+    PP_CHECK_LAUNCH("k_dp_reset");
+    if (maxV > 1) {
+        const size_t cs = (size_t)(maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 +
+                          (size_t)(maxL > 1 ? maxL - 1 : 0) * (maxV - 1);
+        const size_t ex = (size_t)(maxV - 1) * (maxV - 1);
+        const size_t ch = (size_t)(DP_T / 32) * maxV;   // expand_r1's per-warp chan rows
+        const size_t smem = sizeof(double) * std::max(cs, std::max(ex, ch));
+        cudaFuncSetAttribute(k_dp_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dp_persist, DP_T, smem);
+        if (per_sm < 1) return fail(PP_ECUDA, "k_dp_persist does not fit an SM (smem %zu)", smem);
+        k_dp_persist<<<per_sm * num_sms(), DP_T, smem, S(stream)>>>(*b);
+        PP_CHECK_LAUNCH("k_dp_persist");
+    }
+    dim3 gb(b->n_inst, maxV);
+    k_backtrack<<<gb, 32, 0, S(stream)>>>(*b);
+    PP_CHECK_LAUNCH("k_backtrack");
+    return PP_OK;
+}
+
 int pp_prm(const pp_batch* b, void* stream) {
     if (b->n_inst <= 0) return PP_OK;
+    const int mode = g_dp_persist.load();
+    const bool persist = mode == 1 || (mode == 2 && b->n_inst <= PP_DP_PERSIST_MAX);
+    if (persist && b->max_L <= SR_MAX && b->max_V <= SR_MAX) return prm_persist(b, stream);
     const int G = b->n_inst < PP_DP_STREAMS ? b->n_inst : PP_DP_STREAMS;
     if (G <= 1) return prm_chain(b, stream, b->n_inst);
     int dev = 0;
@@ -198,7 +259,9 @@ int pp_prm(const pp_batch* b, void* stream) {
     return PP_OK;
 }
 
-static int prm_chain(const pp_batch* b, void* stream, int total_inst) {
+// Tables every DP schedule needs: prep, base rows, and (shared-memory path)
+// the deduplicated stage-term triangles.
+static int prm_prep(const pp_batch* b, void* stream) {
     const int maxL = b->max_L, maxV = b->max_V;
     dim3 gp(b->n_inst, maxL > maxV ? maxL : maxV);
     k_prep<<<gp, 128, 0, S(stream)>>>(*b);
@@ -206,11 +269,7 @@ static int prm_chain(const pp_batch* b, void* stream, int total_inst) {
     dim3 gbase(b->n_inst, maxL > maxV ? maxL : maxV);
     k_base<<<gbase, 128, 0, S(stream)>>>(*b, !(maxL <= SR_MAX && maxV <= SR_MAX));
     PP_CHECK_LAUNCH("k_base");
-    // wavefront: step j = expand(j) (X for every target (r, j+r) + their stage
-    // terms) then combine_diag(j) (W for every target (r, j+r)); afterwards
-    // slice j+1 is complete.
     if (maxL <= SR_MAX && maxV <= SR_MAX) {
-        // shared-memory-resident path: one barrier per work item
         k_sdedup<<<b->n_inst, 128, 0, S(stream)>>>(*b);
         PP_CHECK_LAUNCH("k_sdedup");
         if (maxV > 1 && maxL > 1) {
@@ -218,6 +277,19 @@ static int prm_chain(const pp_batch* b, void* stream, int total_inst) {
             k_stab<<<gs, 128, 0, S(stream)>>>(*b);
             PP_CHECK_LAUNCH("k_stab");
         }
+    }
+    return PP_OK;
+}
+
+static int prm_chain(const pp_batch* b, void* stream, int total_inst) {
+    const int maxL = b->max_L, maxV = b->max_V;
+    int rc;
+    if ((rc = prm_prep(b, stream))) return rc;
+    // wavefront: step j = expand(j) (X for every target (r, j+r) + their stage
+    // terms) then combine_diag(j) (W for every target (r, j+r)); afterwards
+    // slice j+1 is complete.
+    if (maxL <= SR_MAX && maxV <= SR_MAX) {
+        // shared-memory-resident path: one barrier per work item
         const size_t ex_smem = sizeof(double) * (size_t)maxV * maxV;
         const size_t cs_smem = sizeof(double) * ((maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 +
                                                  (size_t)(maxL > 1 ? maxL - 1 : 0) * maxV);

@@ -276,6 +276,23 @@ __global__ void __launch_bounds__(128) k_stab(pp_batch b) {
         }
         off += L - lp;
     }
+    // Is the triangle non-increasing in l' (S(l', l) >= S(l'+1, l) for every l)?
+    // In exact arithmetic it is (span and parameter sums shrink as the stage
+    // loses layers); the flag certifies it for these rounded values, and only a
+    // certified triangle lets the combine stop scanning l' early.
+    __syncthreads();
+    __shared__ int s_bad;
+    if (t == 0) s_bad = 0;
+    __syncthreads();
+    int bad = 0;
+    for (int lp = 1 + warp; lp + 1 < L; lp += nw) {
+        const int o0 = (lp - 1) * L - (lp - 1) * lp / 2, o1 = lp * L - lp * (lp + 1) / 2;
+        for (int l = lp + 2 + lane; l <= L; l += 32)
+            bad |= !(out[o0 + (l - lp - 1)] >= out[o1 + (l - lp - 2)]);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&s_bad, 1);
+    __syncthreads();
+    if (t == 0) reinterpret_cast<int*>(ws + lay.smono)[slot] = !s_bad;
 }
 
 // (min, max) micro-kernel: a thread owns a TA x TB register tile and folds one
@@ -557,33 +574,41 @@ __global__ void __launch_bounds__(CD_T, 2) k_combine_diag(pp_batch b, int j, int
 // expand, step j: one CTA per (instance, l').  smem: A = W_j(l', ., .) block
 // [r'][xi'] (j x j, one contiguous copy), B = chan(l', r', r) [r'][r]
 // (j x (V-j) exact divisions).  Tiles 4 xi x 4 r; tile K range r' <= j - xi0 + 2.
-__global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
-    const pp_instance I = b.inst[blockIdx.x];
+// Targets r = rfirst..V-j of row l' (rfirst = 2 leaves the r = 1 target to the
+// fused critical-path task of the persistent DP).  ex_smem: j * (j + nt) doubles.
+__device__ __forceinline__ void expand_row_s(const pp_batch& b, const pp_instance& I, int j, int lp, int rfirst,
+                                             double* ex_smem) {
     const int L = I.L, V = I.V, M = I.M;
-    const int lp = blockIdx.y + 1;
-    if (j >= V || lp > L - 1) return;
-    const int nr = V - j;
+    const int nr = V - j, nt = nr - rfirst + 1;
+    if (nt <= 0) return;
     const WsLayout lay = ws_layout(L, V);
     double* ws = b.ws + I.ws_off;
     const double* Wsrc = ws + lay.W + W_idx(L, j, lp, 1, 1);
     const double* cross = ws + lay.cross;
     const double Mp = (double)M * (b.efwd[I.layer_off + lp - 1] + b.ebwd[I.layer_off + lp - 1]);   // partition.py:131,137
-    extern __shared__ __align__(16) double ex_smem[];
     double* A = ex_smem;             // [r'-1][xi'-1], stride j
-    double* B = ex_smem + j * j;     // [r'-1][r-1],   stride nr
+    double* B = ex_smem + j * j;     // [r'-1][r-rfirst], stride nt
     const int t = threadIdx.x;
     const bool allow = I.flags & PP_ALLOW_REPLICATION;
     const int lane = t & 31;
-    for (int e = t; e < j * j; e += blockDim.x) {   // A[r'-1][xi'-1] = W_j(l', xi', r')
-        const int rp = 1 + e / j, xip = 1 + e % j;
-        A[e] = W_structural(j, rp, xip, allow) ? Wsrc[e] : PP_INF;
-    }
-    for (int e = t; e < j * nr; e += blockDim.x) {   // B[r'-1][r-1] = chan(l', r', r, j + r)
-        const int rp = 1 + e / nr, r = 1 + e % nr;
-        B[e] = Mp / ((double)(rp * r) * cross[cross_idx(V, j + r, r, rp)]);
-    }
+    const int warp = t >> 5, nw = blockDim.x >> 5;
+    // A[r'-1][xi'-1] = W_j(l', xi', r'): materialised cells by cp.async (all in
+    // flight at once), structural ones (never written by the DP) as +inf
+    for (int rp = 1 + warp; rp <= j; rp += nw)
+        for (int xip = 1 + lane; xip <= j; xip += 32) {
+            const int e = (rp - 1) * j + (xip - 1);
+            if (W_structural(j, rp, xip, allow)) cp_async8(A + e, Wsrc + e);
+            else A[e] = PP_INF;
+        }
+    cp_async_commit();
+    for (int rp = 1 + warp; rp <= j; rp += nw)   // B[r'-1][r-rfirst] = chan(l', r', r, j + r)
+        for (int q = lane; q < nt; q += 32) {
+            const int r = rfirst + q;
+            B[(rp - 1) * nt + q] = Mp / ((double)(rp * r) * cross[cross_idx(V, j + r, r, rp)]);
+        }
+    cp_async_wait<0>();
     __syncthreads();
-    const int ntx = (j + 3) >> 2, ntr = (nr + 3) >> 2, ntiles = ntx * ntr;
+    const int ntx = (j + 3) >> 2, ntr = (nt + 3) >> 2, ntiles = ntx * ntr;
     // split-K when the plane has few tiles: ks consecutive lanes share a tile,
     // fold interleaved r' subsets and min-reduce with shuffles
     int ks = 1;
@@ -593,7 +618,7 @@ __global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
     double* X = ws + lay.X;
     for (int id = t / ks; id < ntiles; id += blockDim.x / ks) {
         const int tx = id % ntx, tr = id / ntx;
-        const int xi0 = 2 + 4 * tx, r0 = 1 + 4 * tr;
+        const int xi0 = 2 + 4 * tx, r0 = rfirst + 4 * tr;
         const int kend = j - xi0 + 2;   // W_j(l', xi-1, r') = inf for r' > j - xi + 2
         double acc[4][4];
 #pragma unroll
@@ -602,10 +627,11 @@ __global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
             for (int c = 0; c < 4; ++c) acc[a][c] = PP_INF;
         // padded columns read in-range garbage-free copies: clamp and mask at the end
         const int xa[4] = {min(xi0 - 1, j) - 1, min(xi0, j) - 1, min(xi0 + 1, j) - 1, min(xi0 + 2, j) - 1};
-        const int ra[4] = {min(r0, nr) - 1, min(r0 + 1, nr) - 1, min(r0 + 2, nr) - 1, min(r0 + 3, nr) - 1};
+        const int ra[4] = {min(r0, nr) - rfirst, min(r0 + 1, nr) - rfirst, min(r0 + 2, nr) - rfirst,
+                           min(r0 + 3, nr) - rfirst};
         for (int rp = 1 + sub; rp <= kend; rp += ks) {
             const double* Ar = A + (rp - 1) * j;
-            const double* Br = B + (rp - 1) * nr;
+            const double* Br = B + (rp - 1) * nt;
             double p[4], q[4];
 #pragma unroll
             for (int a = 0; a < 4; ++a) { p[a] = Ar[xa[a]]; q[a] = Br[ra[a]]; }
@@ -634,17 +660,28 @@ __global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
     }
 }
 
+__global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
+    const pp_instance I = b.inst[blockIdx.x];
+    const int lp = blockIdx.y + 1;
+    if (j >= I.V || lp > I.L - 1) return;
+    extern __shared__ __align__(16) double ex_smem[];
+    expand_row_s(b, I, j, lp, 1, ex_smem);
+}
+
 // combine, step j: one CTA per (instance, r), target i = j + r.  smem: the
 // stage terms of the item as a packed triangle (row l' holds l = l'+1..L,
 // S = T1 + sync, T1 from k_base) and X(., ., r, i) (rows l' = 1..L-1, stride j).
 // combine reads stage terms straight from global memory for j <= this (0 = always
 // stage them in shared memory; j <= 8 measured no better on B200)
 constexpr int S_DIRECT_J = 0;
+// combine stops scanning l' once no remaining candidate can lower a cell (needs a
+// certified monotone stage-term triangle, k_stab); pp_dp_set_early_exit toggles it
+__device__ int g_combine_early_exit = 1;
 
 template <int TX>
-__device__ __forceinline__ int tile_nfast(int L, int l0, int xi0) {
+__device__ __forceinline__ int tile_nfast(int L, int l0, int xi0, int lA, int lB) {
     constexpr int TL = 16 / TX;
-    const int kb = max(1, xi0 - 1), ke = min(L - 1, l0 + TL - 2);
+    const int kb = max(max(1, xi0 - 1), lA), ke = min(min(L - 1, l0 + TL - 2), lB);
     return max(0, min(ke, l0 - 1) - kb + 1);
 }
 
@@ -654,7 +691,7 @@ __device__ __forceinline__ int tile_nfast(int L, int l0, int xi0) {
 // at different l'.
 template <int TX>
 __device__ __forceinline__ void combine_tile_s(const double* Stri, const int* trio, const double* Xs, int L, int j,
-                                               int l0, int xi0, double (&acc)[16 / TX][TX]) {
+                                               int l0, int xi0, int lA, int lB, double (&acc)[16 / TX][TX]) {
     constexpr int TL = 16 / TX;
 #pragma unroll
     for (int a = 0; a < TL; ++a)
@@ -663,8 +700,8 @@ __device__ __forceinline__ void combine_tile_s(const double* Stri, const int* tr
     int xc[TX];
 #pragma unroll
     for (int c = 0; c < TX; ++c) xc[c] = min(xi0 + c, j + 1) - 2;   // clamp padded columns; masked on write
-    const int kb = max(1, xi0 - 1);
-    const int ke = min(L - 1, l0 + TL - 2);
+    const int kb = max(max(1, xi0 - 1), lA);   // l' restricted to [lA, lB] (split-K parts)
+    const int ke = min(min(L - 1, l0 + TL - 2), lB);
     const int nfast = max(0, min(ke, l0 - 1) - kb + 1);   // l' < l0: every row of the tile has l > l'
     const double* Sr = Stri + trio[kb] + (l0 - kb - 1);  // S(kb, l0)
     const double* Xr = Xs + (kb - 1) * j;
@@ -697,21 +734,84 @@ __device__ __forceinline__ void combine_tile_s(const double* Stri, const int* tr
     }
 }
 
+// Same tile, l' descending, for a certified non-increasing S triangle: the
+// candidates of row a at l'' < l' are >= S(l'', l0+a) >= S(l', l0+a) = p[a],
+// so once p[a] >= max_c acc[a][c] for every row, no remaining l' can lower any
+// cell and the fold stops (the min is unchanged, so the bits are too).
+template <int TX>
+__device__ __forceinline__ void combine_tile_s_desc(const double* Stri, const int* trio, const double* Xs, int L,
+                                                    int j, int l0, int xi0, int lA, int lB,
+                                                    double (&acc)[16 / TX][TX]) {
+    constexpr int TL = 16 / TX;
+#pragma unroll
+    for (int a = 0; a < TL; ++a)
+#pragma unroll
+        for (int c = 0; c < TX; ++c) acc[a][c] = PP_INF;
+    int xc[TX];
+#pragma unroll
+    for (int c = 0; c < TX; ++c) xc[c] = min(xi0 + c, j + 1) - 2;
+    const int kb = max(max(1, xi0 - 1), lA);
+    const int ke = min(min(L - 1, l0 + TL - 2), lB);
+    for (int lp = ke; lp >= max(kb, l0); --lp) {   // the tile's diagonal first: rows l <= l' are +inf
+        const double* Xd = Xs + (lp - 1) * j;
+        double q[TX];
+#pragma unroll
+        for (int c = 0; c < TX; ++c) q[c] = Xd[xc[c]];
+#pragma unroll
+        for (int a = 0; a < TL; ++a) {
+            const int l = l0 + a;
+            if (l <= lp || l > L) continue;
+            const double pa = Stri[trio[lp] + (l - lp - 1)];
+#pragma unroll
+            for (int c = 0; c < TX; ++c) acc[a][c] = dmin(acc[a][c], dmax(pa, q[c]));
+        }
+    }
+    const int hi = min(ke, l0 - 1);
+    if (hi < kb) return;
+    const double* Sr = Stri + trio[hi] + (l0 - hi - 1);   // S(hi, l0)
+    const double* Xr = Xs + (hi - 1) * j;
+    const int nrow = min(TL, L - l0 + 1);                 // rows past L hold no cell
+    for (int lp = hi; lp >= kb; --lp) {
+        double p[TL], q[TX];
+#pragma unroll
+        for (int a = 0; a < TL; ++a) p[a] = Sr[a];
+#pragma unroll
+        for (int c = 0; c < TX; ++c) q[c] = Xr[xc[c]];
+#pragma unroll
+        for (int a = 0; a < TL; ++a)
+#pragma unroll
+            for (int c = 0; c < TX; ++c) acc[a][c] = dmin(acc[a][c], dmax(p[a], q[c]));
+        if (((hi - lp) & 3) == 3) {
+            bool done = true;
+#pragma unroll
+            for (int a = 0; a < TL; ++a) {
+                double m = acc[a][0];
+#pragma unroll
+                for (int c = 1; c < TX; ++c) m = dmax(m, acc[a][c]);
+                done &= (a >= nrow) || p[a] >= m;
+            }
+            if (done) break;
+        }
+        Sr -= L - lp;   // S(l'-1, l0) = S(l', l0) - (L - l')
+        Xr -= j;
+    }
+}
+
 template <int TX>
 __device__ __forceinline__ void combine_tiles_s(double* Wi, int i, int r, int L, int j, const double* Stri,
-                                                const int* trio, const double* Xs, int* hist, int* order) {
+                                                const int* trio, const double* Xs, int* hist, int* order,
+                                                int part, int nparts, int lA, int lB, bool atomic, bool mono) {
     constexpr int TL = 16 / TX;
     const int t = threadIdx.x;
     const int ntl = (L + TL - 1) / TL, ntx = (j + TX - 1) / TX, ntiles = ntl * ntx;
-    // the item is split over gridDim.z CTAs: CTA `part` owns the tiles with id = part (mod nparts)
-    const int part = blockIdx.z, nparts = gridDim.z;
+    // the item is split over nparts CTAs: CTA `part` owns the tiles with id = part (mod nparts)
     const int nmine = ntiles > part ? (ntiles - part + nparts - 1) / nparts : 0;
     // order its tiles by trip count (descending) so each warp's lanes run equal-length loops
     for (int k = t; k < L + 2; k += blockDim.x) hist[k] = 0;
     __syncthreads();
     for (int k = t; k < nmine; k += blockDim.x) {
         const int id = part + k * nparts;
-        atomicAdd(&hist[L - tile_nfast<TX>(L, 1 + TL * (id / ntx), 2 + TX * (id % ntx))], 1);
+        atomicAdd(&hist[L - tile_nfast<TX>(L, 1 + TL * (id / ntx), 2 + TX * (id % ntx), lA, lB)], 1);
     }
     __syncthreads();
     if (t == 0) {
@@ -721,75 +821,88 @@ __device__ __forceinline__ void combine_tiles_s(double* Wi, int i, int r, int L,
     __syncthreads();
     for (int k = t; k < nmine; k += blockDim.x) {
         const int id = part + k * nparts;
-        order[atomicAdd(&hist[L - tile_nfast<TX>(L, 1 + TL * (id / ntx), 2 + TX * (id % ntx))], 1)] = id;
+        order[atomicAdd(&hist[L - tile_nfast<TX>(L, 1 + TL * (id / ntx), 2 + TX * (id % ntx), lA, lB)], 1)] = id;
     }
     __syncthreads();
     for (int q = t; q < nmine; q += blockDim.x) {
         const int id = order[q];
         const int l0 = 1 + TL * (id / ntx), xi0 = 2 + TX * (id % ntx);
         double acc[TL][TX];
-        combine_tile_s<TX>(Stri, trio, Xs, L, j, l0, xi0, acc);
+        if (mono) combine_tile_s_desc<TX>(Stri, trio, Xs, L, j, l0, xi0, lA, lB, acc);
+        else combine_tile_s<TX>(Stri, trio, Xs, L, j, l0, xi0, lA, lB, acc);
 #pragma unroll
         for (int a = 0; a < TL; ++a) {
             const int l = l0 + a;
             if (l > L) continue;
             double* row = Wi + ((int64_t)(l - 1) * i + (r - 1)) * i;
 #pragma unroll
-            for (int c = 0; c < TX; ++c) if (xi0 + c <= j + 1) row[xi0 + c - 1] = acc[a][c];
+            for (int c = 0; c < TX; ++c) {
+                if (xi0 + c > j + 1) continue;
+                if (!atomic) { row[xi0 + c - 1] = acc[a][c]; continue; }
+                // split-K part: min into a cell preset to +inf.  Non-negative doubles
+                // order like their bit patterns, so a 64-bit atomicMin is the exact min.
+                if (acc[a][c] < PP_INF)
+                    atomicMin(reinterpret_cast<unsigned long long*>(row + xi0 + c - 1),
+                              (unsigned long long)__double_as_longlong(acc[a][c]));
+            }
         }
     }
 }
 
-__global__ void __launch_bounds__(256, 2) k_combine_s(pp_batch b, int j) {
-    const pp_instance I = b.inst[blockIdx.x];
+// One combine work item (r, i = j + r), tiles part (mod nparts).  x_staged: Xs
+// already holds X(., ., r, i) (the fused critical-path task computed it).
+// smem: trio (L+1)/2+1, Stri (L-1)L/2, Xs (L-1) x j doubles; hist/order scratch.
+__device__ __forceinline__ void combine_item_s(const pp_batch& b, const pp_instance& I, int j, int r, int part,
+                                               int nparts, double* cs_smem, int* s_hist, int* s_order,
+                                               bool x_staged, int lA = 1, int lB = PP_MAX_LAYERS, bool atomic = false) {
     const int L = I.L, V = I.V;
-    const int r = blockIdx.y + 1;
     if (j >= V || r > V - j) return;
     const int i = j + r;
     const bool allow = I.flags & PP_ALLOW_REPLICATION;
+    // cells outside xi in [2, j+1] and disabled widths are structural +inf (W_at)
+    if (!(allow || r == 1)) return;   // partition.py:103-104
     const WsLayout lay = ws_layout(L, V);
     double* ws = b.ws + I.ws_off;
     double* Wi = ws + lay.W + W_base(L, i);
     const int t = threadIdx.x;
-    // cells outside xi in [2, j+1] and disabled widths are structural +inf (W_at)
-    if (!(allow || r == 1)) return;   // partition.py:103-104
-    extern __shared__ __align__(16) double cs_smem[];
     int* trio = reinterpret_cast<int*>(cs_smem);                 // [L] triangle row offsets
     double* Stri = cs_smem + (L + 1) / 2 + 1;                    // (L-1)L/2
     double* Xs = Stri + (L - 1) * L / 2;                         // (L-1) x j
-    __shared__ int s_hist[SR_MAX + 2];
-    __shared__ int s_order[1024];
-    if (t == 0) {
-        int o = 0;
-        for (int lp = 1; lp < L; ++lp) { trio[lp] = o; o += L - lp; }
-    }
-    // stage X(., ., r, i) (rows l' = 1..L-1, contiguous) and the item's stage-term
-    // triangle (its k_stab slot) with cp.async: every copy of the CTA is in flight at once
+    for (int lp = 1 + t; lp < L; lp += blockDim.x) trio[lp] = (lp - 1) * L - (lp - 1) * lp / 2;
+    // stage X(., ., r, i) and the item's stage-term triangle (its k_stab slot),
+    // rows l' in [la, lb] only (a split-K part folds just those), with cp.async:
+    // every copy of the CTA is in flight at once
+    const int la = max(lA, 1), lb = min(lB, L - 1);
     const double* Sg;
+    const int slot = reinterpret_cast<const int*>(ws + lay.sidx)[(r - 1) * V + (i - 1)];
     {
         const double* Xg = ws + lay.X + X_base(L, i, r);
-        const int nx = (L - 1) * j;
-        for (int e = t; e < nx; e += blockDim.x) cp_async8(Xs + e, Xg + e);
-        const int slot = reinterpret_cast<const int*>(ws + lay.sidx)[(r - 1) * V + (i - 1)];
+        if (!x_staged)
+            for (int e = (la - 1) * j + t; e < lb * j; e += blockDim.x) cp_async8(Xs + e, Xg + e);
         const int ns = (L - 1) * L / 2;
         Sg = ws + lay.Stab + (int64_t)slot * ns;
         // each stage term is used by j columns: for small j reading it from L2/L1
         // once beats copying the whole triangle into shared memory first
+        const int s0 = (la - 1) * L - (la - 1) * la / 2, s1 = lb * L - lb * (lb + 1) / 2;
         if (j > S_DIRECT_J)
-            for (int e = t; e < ns; e += blockDim.x) cp_async8(Stri + e, Sg + e);
+            for (int e = s0 + t; e < s1; e += blockDim.x) cp_async8(Stri + e, Sg + e);
         cp_async_commit();
         cp_async_wait<0>();
     }
     __syncthreads();
-    if (j > S_DIRECT_J) {
-        if (j >= 4) combine_tiles_s<4>(Wi, i, r, L, j, Stri, trio, Xs, s_hist, s_order);
-        else if (j >= 2) combine_tiles_s<2>(Wi, i, r, L, j, Stri, trio, Xs, s_hist, s_order);
-        else combine_tiles_s<1>(Wi, i, r, L, j, Stri, trio, Xs, s_hist, s_order);
-    } else {
-        if (j >= 4) combine_tiles_s<4>(Wi, i, r, L, j, Sg, trio, Xs, s_hist, s_order);
-        else if (j >= 2) combine_tiles_s<2>(Wi, i, r, L, j, Sg, trio, Xs, s_hist, s_order);
-        else combine_tiles_s<1>(Wi, i, r, L, j, Sg, trio, Xs, s_hist, s_order);
-    }
+    const double* S = j > S_DIRECT_J ? Stri : Sg;
+    const bool mono = g_combine_early_exit && reinterpret_cast<const int*>(ws + lay.smono)[slot];
+    if (j >= 4) combine_tiles_s<4>(Wi, i, r, L, j, S, trio, Xs, s_hist, s_order, part, nparts, lA, lB, atomic, mono);
+    else if (j >= 2) combine_tiles_s<2>(Wi, i, r, L, j, S, trio, Xs, s_hist, s_order, part, nparts, lA, lB, atomic, mono);
+    else combine_tiles_s<1>(Wi, i, r, L, j, S, trio, Xs, s_hist, s_order, part, nparts, lA, lB, atomic, mono);
+}
+
+__global__ void __launch_bounds__(256, 2) k_combine_s(pp_batch b, int j) {
+    const pp_instance I = b.inst[blockIdx.x];
+    extern __shared__ __align__(16) double cs_smem[];
+    __shared__ int s_hist[SR_MAX + 2];
+    __shared__ int s_order[1024];
+    combine_item_s(b, I, j, blockIdx.y + 1, blockIdx.z, gridDim.z, cs_smem, s_hist, s_order, false);
 }
 
 // ----------------------------------------------------------------------------

@@ -1,6 +1,7 @@
 // Single translation unit for libpipeplan_b200.so.
 #include "prm.cu"
 #include "rdo.cu"
+#include "dp_persist.cu"
 #include "sim.cu"
 #include "capi.cu"
 #include "trace.cu"

@@ -1,0 +1,130 @@
+"""Persistent dependency-driven DP (dp_persist.cu) vs the launch-per-step wavefront.
+
+Both schedules evaluate the same fp64 expressions over the same min/max sets,
+so every SppResult (plans, workloads, makespans, events) and every
+PartitionSolver cell must be identical; the oracle pins both.
+"""
+
+import math
+import random
+
+import pytest
+
+import oracle as O
+from helpers import model_of, oracle_instance
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2204_10562_b200")
+from paper_2204_10562_b200 import _lib, workloads as W  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    _lib.load()
+
+
+@pytest.fixture
+def persistent():
+    prev = _lib.dp_persistent(True)
+    yield _lib.dp_persistent
+    _lib.dp_persistent(prev)
+
+
+def test_default_mode_is_auto():
+    prev = _lib.dp_persistent(2)
+    assert prev == 2
+    _lib.dp_persistent(prev)
+
+
+@pytest.fixture
+def early_exit():
+    prev = _lib.dp_early_exit(True)
+    yield _lib.dp_early_exit
+    _lib.dp_early_exit(prev)
+
+
+@pytest.mark.parametrize("mode", [(True, False), (False, False), (False, True)])
+def test_early_exit_identical(persistent, early_exit, mode):
+    """Early exit on (default, persistent) vs off / per-step: identical results."""
+    rng = random.Random(99)
+    specs = _rand_specs(rng, 30, 60, 20) + [W.c3_gpt96(M=64, jitter_seed=3), W.c2_bert24()] + W.c4_batch(4)
+    models = [s.to_model() for s in specs]
+    persistent(True); early_exit(True)
+    ref = P.spp_many(models)
+    persistent(mode[1]); early_exit(mode[0])
+    got = P.spp_many(models)
+    for s, x, y in zip(specs, ref, got):
+        assert x == y, (s.name, mode)
+
+
+def _rand_specs(rng, n, Lmax, Vmax, Mmax=32):
+    out = []
+    lu = lambda lo, hi: math.exp(rng.uniform(math.log(lo), math.log(hi)))
+    for k in range(n):
+        L, V, M = rng.randint(1, Lmax), rng.randint(1, Vmax), rng.randint(1, Mmax)
+        ids = rng.sample(range(1, 1000), V)
+        out.append(W.InstanceSpec(f"r{k}", [lu(1e-3, 1.0) for _ in range(L)], [lu(1e-3, 2.0) for _ in range(L)],
+                                  [lu(1e6, 1e10) for _ in range(L)], [lu(1e5, 1e9) for _ in range(L - 1)],
+                                  [lu(1e5, 1e9) for _ in range(L - 1)], ids,
+                                  [(a, b, lu(1e8, 1e11)) for i, a in enumerate(ids) for b in ids[i + 1:]], M))
+    return out
+
+
+def _both(persistent, specs):
+    models = [s.to_model() for s in specs]
+    persistent(True)
+    a = P.spp_many(models)
+    persistent(False)
+    b = P.spp_many(models)
+    return a, b
+
+
+def test_mixed_batch_modes_identical(persistent):
+    """Ragged batch: instances far below the batch maxima exercise the skipped tasks."""
+    rng = random.Random(31337)
+    specs = _rand_specs(rng, 60, 40, 24) + [W.c2_bert24(), W.c1_vgg19()] + W.c4_batch(6)
+    specs += [W.c3_gpt96(M=16, nodes=3, per_node=8)]
+    a, b = _both(persistent, specs)
+    for s, x, y in zip(specs, a, b):
+        assert x == y, s.name
+
+
+def test_c3_modes_identical_and_match_oracle(persistent):
+    specs = [W.c3_gpt96(M=32), W.c3_gpt96(M=128, jitter_seed=5)]
+    a, b = _both(persistent, specs)
+    for s, x, y in zip(specs, a, b):
+        assert x == y, s.name
+        inst = O.Instance(s.fwd, s.bwd, s.param, s.efwd, s.ebwd, _bw(s), s.M)
+        want = O.spp(inst, with_events=False)
+        assert x.makespan == want["makespan"]
+        assert [e.workload for e in x.sweep] == [w for _, _, w, _, _ in want["sweep"]]
+
+
+def _bw(s):
+    import numpy as np
+    ids = sorted(s.gpu_ids)
+    pos = {g: k for k, g in enumerate(ids)}
+    bw = np.zeros((len(ids), len(ids)))
+    for a, b, w in s.links:
+        bw[pos[a], pos[b]] = bw[pos[b], pos[a]] = w
+    return bw
+
+
+@pytest.mark.parametrize("allow", [True, False])
+def test_partition_solver_cells_modes_identical(persistent, allow):
+    rng = random.Random(5 + allow)
+    for s in _rand_specs(rng, 6, 30, 20):
+        prof, clu, M = s.to_model()
+        order = P.rdo(clu)
+        cells = [(l, x, r, i) for i in range(1, s.V + 1) for r in range(1, i + 1)
+                 for x in range(1, i + 1) for l in range(1, s.L + 1) if (l + x + r + i) % 3 == 0]
+        got = {}
+        for mode in (True, False):
+            persistent(mode)
+            solver = P.PartitionSolver(prof, clu, order, M, allow_replication=allow)
+            got[mode] = [(g.workload, g.stages) for g in solver.solve_many(cells)]
+        assert got[True] == got[False], s.name
