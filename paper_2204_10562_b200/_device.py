@@ -41,7 +41,8 @@ class Packed:
         return int(self.bw.shape[0])
 
 
-def pack(profile, cluster) -> Packed:
+def pack_profile(profile):
+    """(fwd, bwd, param, efwd, ebwd) arrays of a profile (edge arrays padded to L)."""
     L = profile.num_layers
     fwd = np.fromiter((lp.fwd_time for lp in profile.layers), dtype=np.float64, count=L)
     bwd = np.fromiter((lp.bwd_time for lp in profile.layers), dtype=np.float64, count=L)
@@ -51,18 +52,38 @@ def pack(profile, cluster) -> Packed:
     if L > 1:
         efwd[:L - 1] = [e.fwd_bytes for e in profile.edges]
         ebwd[:L - 1] = [e.bwd_bytes for e in profile.edges]
+    return fwd, bwd, par, efwd, ebwd
+
+
+def pack_cluster(cluster, arrays=None):
+    """(sorted ids, dense V x V bandwidth matrix); `arrays` = bandwidth_arrays(cluster) if known."""
     ids = tuple(sorted(cluster.gpu_ids))
     V = len(ids)
     bw = np.zeros((V, V))
-    items = cluster.bandwidth
-    if items:
+    if cluster.bandwidth:
         sid = np.array(ids)
-        keys = np.array(list(items.keys()))
-        vals = np.fromiter(items.values(), dtype=np.float64, count=len(items))
+        keys, vals = arrays if arrays is not None else bandwidth_arrays(cluster)
         ia, ib = np.searchsorted(sid, keys[:, 0]), np.searchsorted(sid, keys[:, 1])
         bw[ia, ib] = vals
         bw[ib, ia] = vals
-    return Packed(ids, fwd, bwd, par, efwd, ebwd, bw)
+    return ids, bw
+
+
+def pack(profile, cluster) -> Packed:
+    ids, bw = pack_cluster(cluster)
+    return Packed(ids, *pack_profile(profile), bw)
+
+
+def bandwidth_arrays(cluster):
+    """(keys [n, 2] int64, values [n] float64) of cluster.bandwidth, in dict order."""
+    import itertools
+    bwd = cluster.bandwidth
+    n = len(bwd)
+    try:
+        keys = np.fromiter(itertools.chain.from_iterable(bwd.keys()), dtype=np.int64, count=2 * n).reshape(n, 2)
+    except (TypeError, ValueError):   # keys that are not int pairs: let the caller's checks report them
+        keys = np.array(list(bwd.keys()))
+    return keys, np.fromiter(bwd.values(), dtype=np.float64, count=n)
 
 
 def _stream():

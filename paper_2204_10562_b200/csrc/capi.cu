@@ -161,7 +161,14 @@ static int prm_chain(const pp_batch* b, void* stream, int total_inst);
 // partly empty.  Instance groups run their chains on separate streams so one
 // group's tail overlaps another group's kernels (fork/join with events on the
 // caller's stream; the side streams are created once per host thread+device).
-static constexpr int PP_DP_STREAMS = 4;
+static constexpr int PP_DP_STREAMS = 8;
+// instance groups (side streams) of the per-step schedule; PP_DP_GROUPS env overrides
+static int read_dp_groups() {
+    const char* e = getenv("PP_DP_GROUPS");
+    const int v = e ? atoi(e) : 4;
+    return v < 1 ? 1 : (v > PP_DP_STREAMS ? PP_DP_STREAMS : v);
+}
+static const int g_dp_groups = read_dp_groups();
 struct SideStreams {
     int dev = -1;
     cudaStream_t s[PP_DP_STREAMS];
@@ -230,7 +237,7 @@ int pp_prm(const pp_batch* b, void* stream) {
     const int mode = g_dp_persist.load();
     const bool persist = mode == 1 || (mode == 2 && b->n_inst <= PP_DP_PERSIST_MAX);
     if (persist && b->max_L <= SR_MAX && b->max_V <= SR_MAX) return prm_persist(b, stream);
-    const int G = b->n_inst < PP_DP_STREAMS ? b->n_inst : PP_DP_STREAMS;
+    const int G = b->n_inst < g_dp_groups ? b->n_inst : g_dp_groups;
     if (G <= 1) return prm_chain(b, stream, b->n_inst);
     int dev = 0;
     cudaGetDevice(&dev);

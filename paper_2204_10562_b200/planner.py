@@ -8,6 +8,7 @@ one launch sequence (every kernel's grid carries the instance dimension).
 """
 
 import math
+from collections import abc
 import sys
 from dataclasses import dataclass
 from typing import List, Optional, Sequence, Tuple
@@ -15,8 +16,8 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _device, _lib
-from .model import (ClusterGraph, ModelProfile, Plan, Schedule, Stage, check_numeric_range, validate_cluster,
-                    validate_profile)
+from .model import (ClusterGraph, ModelProfile, Plan, Schedule, Stage, check_cluster_range, check_numeric_range,
+                    check_profile_range, validate_cluster, validate_profile)
 from .partition import sum_flags
 from .scheduler import _build_schedule
 
@@ -57,18 +58,25 @@ def _items(instances):
     seen_p, seen_c, seen_pc = {}, {}, {}
     flags = _lib.PP_ALLOW_REPLICATION | sum_flags()
     for profile, cluster, M in instances:
-        if id(profile) not in seen_p:
+        # same check order as validate_profile, validate_cluster, check_numeric_range
+        pp, cc = seen_p.get(id(profile)), seen_c.get(id(cluster))
+        if pp is None:
             validate_profile(profile)
-            seen_p[id(profile)] = profile
-        if id(cluster) not in seen_c:
-            validate_cluster(cluster)
-            seen_c[id(cluster)] = cluster
+        arrays = None
+        if cc is None:
+            arrays = _device.bandwidth_arrays(cluster) if cluster.bandwidth else None
+            validate_cluster(cluster, arrays)
+        if pp is None:
+            check_profile_range(profile)
+            pp = seen_p[id(profile)] = (profile, _device.pack_profile(profile))
+        if cc is None:
+            check_cluster_range(cluster, arrays)
+            cc = seen_c[id(cluster)] = (cluster, _device.pack_cluster(cluster, arrays))
         key = (id(profile), id(cluster))
         p = seen_pc.get(key)
         if p is None:
-            check_numeric_range(profile, cluster)
-            p = _device.pack(profile, cluster)
-            seen_pc[key] = p
+            ids, bw = cc[1]
+            p = seen_pc[key] = _device.Packed(ids, *pp[1], bw)
         if M < 1:
             from .model import ValidationError
             raise ValidationError("microbatch count must be positive")
@@ -77,35 +85,88 @@ def _items(instances):
     return items, packs
 
 
+class LazySweep(abc.Sequence):
+    """SppResult.sweep backed by the fetched per-xi arrays: behaves like the
+    reference's Tuple[SweepEntry, ...] (len, indexing, iteration, ==, hash)
+    but builds the SweepEntry objects on first use."""
+
+    __slots__ = ("_r", "_w", "_mk", "_bd", "_tuple")
+
+    def __init__(self, r, w, mk, bd):
+        self._r, self._w, self._mk, self._bd = r, w, mk, bd
+        self._tuple = None
+
+    def materialize(self):
+        if self._tuple is None:
+            self._tuple = tuple(
+                _frozen(SweepEntry, stage_count=xi, feasible=False, workload=math.inf, makespan=None, bound=None)
+                if r == 0 else
+                _frozen(SweepEntry, stage_count=xi, feasible=True, workload=w, makespan=mk, bound=bd)
+                for xi, (r, w, mk, bd) in enumerate(zip(self._r, self._w, self._mk, self._bd), start=1))
+        return self._tuple
+
+    def __len__(self):
+        return len(self._r)
+
+    def __getitem__(self, k):
+        return self.materialize()[k]
+
+    def __iter__(self):
+        return iter(self.materialize())
+
+    def __eq__(self, other):
+        if isinstance(other, LazySweep):
+            return self.materialize() == other.materialize()
+        if isinstance(other, (tuple, list)):
+            return self.materialize() == tuple(other)
+        return NotImplemented
+
+    def __ne__(self, other):
+        r = self.__eq__(other)
+        return r if r is NotImplemented else not r
+
+    def __hash__(self):
+        return hash(self.materialize())
+
+    def __repr__(self):
+        return repr(self.materialize())
+
+
+def _frozen(cls, **fields):
+    """Build a frozen dataclass instance without its per-field __setattr__
+    guard (same fields, so equality / hashing / repr are unchanged)."""
+    obj = object.__new__(cls)
+    obj.__dict__.update(fields)
+    return obj
+
+
 def _decode(db: _device.DeviceBatch, h, k: int, M: int, packed) -> SppResult:
     I = db.inst_host[k]
     V = I.V
     ids = packed.ids
-    order = tuple(ids[int(x)] for x in h["order"][I.order_off:I.order_off + V])
+    order = tuple(ids[x] for x in h["order"][I.order_off:I.order_off + V].tolist())
     so = I.sweep_off
-    sweep = []
-    for xi in range(1, V + 1):
-        r = int(h["sweep_r"][so + xi - 1])
-        if r == 0:
-            sweep.append(SweepEntry(stage_count=xi, feasible=False, workload=math.inf, makespan=None, bound=None))
-        else:
-            sweep.append(SweepEntry(stage_count=xi, feasible=True, workload=float(h["sweep_w"][so + xi - 1]),
-                                    makespan=float(h["sweep_mk"][so + xi - 1]),
-                                    bound=float(h["sweep_bound"][so + xi - 1])))
+    rs = h["sweep_r"][so:so + V].tolist()
+    ws = h["sweep_w"][so:so + V].tolist()
+    mks = h["sweep_mk"][so:so + V].tolist()
+    bds = h["sweep_bound"][so:so + V].tolist()
+    sweep = LazySweep(rs, ws, mks, bds)
     xi = int(h["best_xi"][k])
     base = I.stage_off + xi * (xi - 1) // 2
-    stages = tuple(Stage(index=n + 1, layer_start=int(h["ls"][base + n]), layer_end=int(h["le"][base + n]),
-                         devices=order[int(h["dlo"][base + n]) - 1:int(h["dhi"][base + n])])
+    ls, le = h["ls"][base:base + xi].tolist(), h["le"][base:base + xi].tolist()
+    dlo, dhi = h["dlo"][base:base + xi].tolist(), h["dhi"][base:base + xi].tolist()
+    stages = tuple(Stage(index=n + 1, layer_start=ls[n], layer_end=le[n], devices=order[dlo[n] - 1:dhi[n]])
                    for n in range(xi))
     plan = Plan(stages=stages, microbatch_count=M)
     J = 4 * xi - 3
-    rec = dict(makespan=float(h["best_mk"][k]),
+    mk = float(h["best_mk"][k])
+    rec = dict(makespan=mk,
                ev_start=h["ev_start"][I.ev_off:I.ev_off + M * J], ev_end=h["ev_end"][I.ev_off:I.ev_off + M * J],
                ar_start=h["ar_start"][I.ar_off:I.ar_off + xi], ar_end=h["ar_end"][I.ar_off:I.ar_off + xi])
     schedule = _build_schedule(plan, rec)
     p = float(h["phi"][k])
-    return SppResult(plan=plan, schedule=schedule, makespan=float(h["best_mk"][k]), sweep=tuple(sweep),
-                     device_order=order, theorem_factor=bound_factor(V, M) * (1.0 + p), phi=p)
+    return _frozen(SppResult, plan=plan, schedule=schedule, makespan=mk, sweep=sweep,
+                   device_order=order, theorem_factor=bound_factor(V, M) * (1.0 + p), phi=p)
 
 
 def spp_many(instances: Sequence[Tuple[ModelProfile, ClusterGraph, int]]) -> List[SppResult]:

@@ -121,15 +121,20 @@ def _labels(N: int):
 
 
 @functools.lru_cache(maxsize=256)
+@functools.lru_cache(maxsize=256)
 def _pe_tiebreak_order(N: int, M: int):
     """Permutation of the (m, pos) grid sorted by (resource key, microbatch, position): a
-    stable sort by start time on top of it yields the reference's event order."""
+    stable sort by start time on top of it yields the reference's event order.
+    Depends on (N, M) only: cached, arrays read-only."""
     J = 4 * N - 3
     _, _, key = _labels(N)
-    m = np.repeat(np.arange(1, M + 1), J)
-    p = np.tile(np.arange(1, J + 1), M)
+    m = np.repeat(np.arange(1, M + 1, dtype=np.int32), J)
+    p = np.tile(np.arange(1, J + 1, dtype=np.int32), M)
     order = np.lexsort((p, m, key[p]))
-    return order, m[order], p[order]
+    out = (order, m[order], p[order])
+    for a in out:
+        a.setflags(write=False)
+    return out
 
 
 def _check_plan(plan: Plan, profile: ModelProfile, cluster: ClusterGraph) -> None:

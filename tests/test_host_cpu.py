@@ -176,3 +176,15 @@ def test_baseline_host_planners_match_goldens():
         plan = P.Plan(tuple(P.Stage(n + 1, a, b, tuple(d)) for n, (a, b, d) in enumerate(st)), case["plan"]["M"])
         want = {k: tuple(map(tuple, v)) for k, v in case["queues"].items()}
         assert gpipe_queues(plan) == want
+
+
+def test_lazy_sweep_behaves_like_the_reference_tuple():
+    import math
+    from paper_2204_10562_b200.planner import LazySweep, SweepEntry
+    lz = LazySweep([1, 0, 2], [1.5, 0.0, 2.5], [3.0, 0.0, 4.0], [5.0, 0.0, 6.0])
+    want = (SweepEntry(1, True, 1.5, 3.0, 5.0), SweepEntry(2, False, math.inf, None, None),
+            SweepEntry(3, True, 2.5, 4.0, 6.0))
+    assert len(lz) == 3 and lz == want and want == tuple(lz) and lz[1] == want[1] and lz[-1] == want[-1]
+    assert lz[:2] == want[:2] and list(lz) == list(want) and hash(lz) == hash(want)
+    assert lz == LazySweep([1, 0, 2], [1.5, 0.0, 2.5], [3.0, 0.0, 4.0], [5.0, 0.0, 6.0])
+    assert lz != LazySweep([1, 0, 2], [1.5, 0.0, 2.5], [3.0, 0.0, 4.5], [5.0, 0.0, 6.0])
