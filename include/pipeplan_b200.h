@@ -116,7 +116,8 @@ int pp_prm(const pp_batch *b, void *stream);
 
 /* DP schedule for batches inside the shared-memory limits (L, V <= 128):
  * 1 = one persistent dependency-driven kernel, 0 = one launch pair per
- * wavefront step, 2 (default) = persistent for batches of <= 6 instances.
+ * wavefront step, 3 = one CTA per instance, 2 (default) = auto (instance per
+ * CTA for >= 2 x SMs instances, persistent for <= 6, else per step).
  * Bit-identical results; a performance / test knob.  Returns the previous
  * mode.  Process-wide. */
 int pp_dp_set_persistent(int32_t mode);

@@ -144,8 +144,8 @@ def _declare(L):
 
 
 def dp_persistent(mode) -> int:
-    """DP schedule: True/1 persistent kernel, False/0 per-step launches, 2 auto
-    (default: persistent for small batches).  Returns the previous mode.
+    """DP schedule: True/1 persistent kernel, False/0 per-step launches, 3 one
+    CTA per instance, 2 auto (default).  Returns the previous mode.
     Results are identical either way."""
     return int(load(require_device=False).pp_dp_set_persistent(int(mode)))
 

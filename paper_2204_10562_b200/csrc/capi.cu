@@ -20,6 +20,7 @@ __global__ void k_stab(pp_batch b);
 __global__ void k_combine_s(pp_batch b, int j);
 __global__ void k_dp_reset(pp_batch b);
 __global__ void k_dp_persist(pp_batch b);
+__global__ void k_dp_inst(pp_batch b, int smem_doubles);
 __global__ void k_backtrack(pp_batch b);
 __global__ void k_query(pp_batch b, int n, const int* qi, const int* ql, const int* qx, const int* qr,
                         const int* qd, int max_xi, double* w, int* frag, int* feas);
@@ -181,11 +182,36 @@ static thread_local SideStreams g_side;
 //       chain runs ahead, so small batches finish sooner (latency);
 //   0 = the launch-per-step wavefront (prm_chain): better throughput once the
 //       batch fills the GPU on its own;
-//   2 = auto (default): persistent for batches of <= PP_DP_PERSIST_MAX instances.
+//   3 = one CTA per instance (dp_inst.cu): the whole wavefront of an instance in
+//       one CTA, for batches with many more instances than SMs;
+//   2 = auto (default): instance-per-CTA for >= 2 x SMs instances, persistent
+//       for <= PP_DP_PERSIST_MAX, else per-step.
 static constexpr int PP_DP_PERSIST_MAX = 6;
 static std::atomic<int> g_dp_persist{2};
 
-int pp_dp_set_persistent(int32_t mode) { return g_dp_persist.exchange(mode < 0 ? 2 : (mode > 2 ? 2 : mode)); }
+int pp_dp_set_persistent(int32_t mode) { return g_dp_persist.exchange(mode < 0 || mode > 3 ? 2 : mode); }
+
+static int prm_prep(const pp_batch* b, void* stream);
+
+static int prm_inst(const pp_batch* b, void* stream) {
+    const int maxL = b->max_L, maxV = b->max_V;
+    int rc;
+    if ((rc = prm_prep(b, stream))) return rc;
+    if (maxV > 1) {
+        // smallest chunk: one expand row at j = V-1 or one combine item at j = V-1
+        const int need = std::max((maxV - 1) * maxV, (maxL - 1) * maxL / 2 + std::max(maxL - 1, 0) * (maxV - 1));
+        const int sd = std::min(27000, std::max(need, 12000));
+        if (need > 27000) return fail(PP_EINVAL, "k_dp_inst: L=%d V=%d exceed shared memory", maxL, maxV);
+        const size_t smem = sizeof(double) * (size_t)sd;
+        cudaFuncSetAttribute(k_dp_inst, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_dp_inst<<<b->n_inst, DI_T, smem, S(stream)>>>(*b, sd);
+        PP_CHECK_LAUNCH("k_dp_inst");
+    }
+    dim3 gb(b->n_inst, maxV);
+    k_backtrack<<<gb, 32, 0, S(stream)>>>(*b);
+    PP_CHECK_LAUNCH("k_backtrack");
+    return PP_OK;
+}
 
 int pp_dp_set_early_exit(int32_t on) {
     int prev = 1, v = on ? 1 : 0;
@@ -205,7 +231,6 @@ int pp_dp_trace(uint64_t* d_buf, int32_t cap) {
     return PP_OK;
 }
 
-static int prm_prep(const pp_batch* b, void* stream);
 
 static int prm_persist(const pp_batch* b, void* stream) {
     const int maxL = b->max_L, maxV = b->max_V;
@@ -235,8 +260,10 @@ static int prm_persist(const pp_batch* b, void* stream) {
 int pp_prm(const pp_batch* b, void* stream) {
     if (b->n_inst <= 0) return PP_OK;
     const int mode = g_dp_persist.load();
-    const bool persist = mode == 1 || (mode == 2 && b->n_inst <= PP_DP_PERSIST_MAX);
-    if (persist && b->max_L <= SR_MAX && b->max_V <= SR_MAX) return prm_persist(b, stream);
+    if (b->max_L <= SR_MAX && b->max_V <= SR_MAX) {
+        if (mode == 3 || (mode == 2 && b->n_inst >= 2 * num_sms())) return prm_inst(b, stream);
+        if (mode == 1 || (mode == 2 && b->n_inst <= PP_DP_PERSIST_MAX)) return prm_persist(b, stream);
+    }
     const int G = b->n_inst < g_dp_groups ? b->n_inst : g_dp_groups;
     if (G <= 1) return prm_chain(b, stream, b->n_inst);
     int dev = 0;
@@ -280,7 +307,7 @@ static int prm_prep(const pp_batch* b, void* stream) {
         k_sdedup<<<b->n_inst, 128, 0, S(stream)>>>(*b);
         PP_CHECK_LAUNCH("k_sdedup");
         if (maxV > 1 && maxL > 1) {
-            dim3 gs(b->n_inst, maxV - 1, maxV);
+            dim3 gs(b->n_inst, maxV - 1);
             k_stab<<<gs, 128, 0, S(stream)>>>(*b);
             PP_CHECK_LAUNCH("k_stab");
         }

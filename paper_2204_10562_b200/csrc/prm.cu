@@ -234,11 +234,8 @@ __global__ void __launch_bounds__(128) k_sdedup(pp_batch b) {
     }
 }
 
-__global__ void __launch_bounds__(128) k_stab(pp_batch b) {
-    const pp_instance I = b.inst[blockIdx.x];
+__device__ __forceinline__ void stab_fill(const pp_batch& b, const pp_instance& I, int r, int i) {
     const int L = I.L, V = I.V;
-    const int r = blockIdx.y + 1, i = blockIdx.z + 1;
-    if (L > SR_MAX || V > SR_MAX || r >= V || i <= r || i > V) return;
     const WsLayout lay = ws_layout(L, V);
     double* ws = b.ws + I.ws_off;
     const int* sidx = reinterpret_cast<const int*>(ws + lay.sidx);
@@ -293,6 +290,14 @@ __global__ void __launch_bounds__(128) k_stab(pp_batch b) {
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&s_bad, 1);
     __syncthreads();
     if (t == 0) reinterpret_cast<int*>(ws + lay.smono)[slot] = !s_bad;
+}
+
+// grid (n_inst, maxV - 1): CTA (instance, r) fills the canonical slots of width r
+__global__ void __launch_bounds__(128) k_stab(pp_batch b) {
+    const pp_instance I = b.inst[blockIdx.x];
+    const int r = blockIdx.y + 1;
+    if (I.L > SR_MAX || I.V > SR_MAX || r >= I.V) return;
+    for (int i = r + 1; i <= I.V; ++i) stab_fill(b, I, r, i);
 }
 
 // (min, max) micro-kernel: a thread owns a TA x TB register tile and folds one

@@ -2,6 +2,7 @@
 #include "prm.cu"
 #include "rdo.cu"
 #include "dp_persist.cu"
+#include "dp_inst.cu"
 #include "sim.cu"
 #include "capi.cu"
 #include "trace.cu"

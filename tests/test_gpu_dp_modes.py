@@ -47,13 +47,13 @@ def early_exit():
     _lib.dp_early_exit(prev)
 
 
-@pytest.mark.parametrize("mode", [(True, False), (False, False), (False, True)])
+@pytest.mark.parametrize("mode", [(True, 0), (False, 0), (False, 1), (True, 3), (False, 3)])
 def test_early_exit_identical(persistent, early_exit, mode):
     """Early exit on (default, persistent) vs off / per-step: identical results."""
     rng = random.Random(99)
     specs = _rand_specs(rng, 30, 60, 20) + [W.c3_gpt96(M=64, jitter_seed=3), W.c2_bert24()] + W.c4_batch(4)
     models = [s.to_model() for s in specs]
-    persistent(True); early_exit(True)
+    persistent(1); early_exit(True)
     ref = P.spp_many(models)
     persistent(mode[1]); early_exit(mode[0])
     got = P.spp_many(models)
@@ -74,13 +74,35 @@ def _rand_specs(rng, n, Lmax, Vmax, Mmax=32):
     return out
 
 
-def _both(persistent, specs):
+def _both(persistent, specs, modes=(1, 0)):
     models = [s.to_model() for s in specs]
-    persistent(True)
-    a = P.spp_many(models)
-    persistent(False)
-    b = P.spp_many(models)
-    return a, b
+    out = []
+    for m in modes:
+        persistent(m)
+        out.append(P.spp_many(models))
+    return out
+
+
+def test_instance_per_cta_identical(persistent):
+    """One CTA per instance (mode 3, auto for >= 2 x SMs instances) vs per-step."""
+    rng = random.Random(4242)
+    specs = _rand_specs(rng, 40, 50, 20) + W.c4_batch(12) + [W.c2_bert24(), W.c1_vgg19()]
+    specs += [W.c3_gpt96(M=16, nodes=2, per_node=8), W.c3_gpt96(M=8)]
+    a, b = _both(persistent, specs, modes=(3, 0))
+    for s, x, y in zip(specs, a, b):
+        assert x == y, s.name
+
+
+def test_c4_auto_batch_matches_oracle():
+    """A C4-size batch (auto picks instance-per-CTA): every 64th instance vs the oracle."""
+    specs = W.c4_batch(512)
+    res = P.spp_many(W.models_of(specs))
+    for k in range(0, 512, 64):
+        s = specs[k]
+        want = O.spp(O.Instance(s.fwd, s.bwd, s.param, s.efwd, s.ebwd, _bw(s), s.M), with_events=False)
+        assert res[k].makespan == want["makespan"], k
+        assert [(e.stage_count, e.feasible, e.workload, e.makespan, e.bound) for e in res[k].sweep] == \
+            [tuple(x) for x in want["sweep"]], k
 
 
 def test_mixed_batch_modes_identical(persistent):

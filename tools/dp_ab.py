@@ -29,16 +29,16 @@ def prm_ms(db, reps=5):
 def main():
     sizes = [int(x) for x in sys.argv[1:]] or [12, 1]
     for n in sizes:
-        specs = (W.c3_sweep() * 8)[:n]
+        specs = (W.c3_sweep() * 64)[:n] if n > 0 else W.c4_batch(-n)
         items = [(_device.pack(p, c), M, _lib.PP_ALLOW_REPLICATION | sum_flags(), None)
                  for p, c, M in W.models_of(specs)]
         db = _device.DeviceBatch(items, capture_events=True)
-        for pers in (True, False):
+        for mode in (1, 0, 3):
             for ee in (True, False):
-                _lib.dp_persistent(pers); _lib.dp_early_exit(ee)
+                _lib.dp_persistent(mode); _lib.dp_early_exit(ee)
                 db.run("spp"); torch.cuda.synchronize()
                 mn, med = prm_ms(db)
-                print(f"n={n:3d} persistent={pers!s:5} early_exit={ee!s:5}: prm {mn:7.3f} ms (median {med:7.3f})")
+                print(f"n={n:4d} mode={mode} early_exit={ee!s:5}: prm {mn:7.3f} ms (median {med:7.3f})")
         _lib.dp_persistent(2); _lib.dp_early_exit(True)
 
 
