@@ -21,6 +21,7 @@ __global__ void k_combine_s(pp_batch b, int j);
 __global__ void k_dp_reset(pp_batch b);
 __global__ void k_dp_persist(pp_batch b);
 __global__ void k_dp_inst(pp_batch b, int smem_doubles);
+__global__ void k_dp_cluster(pp_batch b);
 __global__ void k_backtrack(pp_batch b);
 __global__ void k_query(pp_batch b, int n, const int* qi, const int* ql, const int* qx, const int* qr,
                         const int* qd, int max_xi, double* w, int* frag, int* feas);
@@ -184,14 +185,64 @@ static thread_local SideStreams g_side;
 //       batch fills the GPU on its own;
 //   3 = one CTA per instance (dp_inst.cu): the whole wavefront of an instance in
 //       one CTA, for batches with many more instances than SMs;
+//   4 = one thread-block cluster per instance (dp_cluster.cu);
 //   2 = auto (default): instance-per-CTA for >= 2 x SMs instances, persistent
 //       for <= PP_DP_PERSIST_MAX, else per-step.
 static constexpr int PP_DP_PERSIST_MAX = 6;
 static std::atomic<int> g_dp_persist{2};
 
-int pp_dp_set_persistent(int32_t mode) { return g_dp_persist.exchange(mode < 0 || mode > 3 ? 2 : mode); }
+int pp_dp_set_persistent(int32_t mode) { return g_dp_persist.exchange(mode < 0 || mode > 4 ? 2 : mode); }
 
 static int prm_prep(const pp_batch* b, void* stream);
+
+// cluster size of the cluster-per-instance schedule (PP_DP_CLUSTER env: 2..16)
+static int read_cluster_size() {
+    const char* e = getenv("PP_DP_CLUSTER");
+    const int v = e ? atoi(e) : 16;
+    return v < 2 ? 2 : (v > 16 ? 16 : v);
+}
+static const int g_cluster_size = read_cluster_size();
+
+static int prm_cluster(const pp_batch* b, void* stream) {
+    const int maxL = b->max_L, maxV = b->max_V;
+    int rc;
+    if ((rc = prm_prep(b, stream))) return rc;
+    if (maxV > 1) {
+        const size_t cs = (size_t)(maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 +
+                          (size_t)(maxL > 1 ? maxL - 1 : 0) * (maxV - 1);
+        const size_t ex = (size_t)(maxV - 1) * maxV;
+        const size_t smem = sizeof(double) * std::max(cs, ex);
+        cudaFuncSetAttribute(k_dp_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_dp_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        int csz = g_cluster_size;
+        for (;;) {   // largest cluster size (<= requested) the device can co-schedule
+            cfg.gridDim = dim3(b->n_inst * csz);
+            cfg.blockDim = dim3(DC_T);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = S(stream);
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = csz;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, k_dp_cluster, &cfg) == cudaSuccess && nclusters > 0) break;
+            cudaGetLastError();
+            if (csz <= 2) return fail(PP_ECUDA, "k_dp_cluster cannot be scheduled (smem %zu)", smem);
+            csz /= 2;
+        }
+        if (cudaLaunchKernelEx(&cfg, k_dp_cluster, *b) != cudaSuccess)
+            return fail(PP_ECUDA, "k_dp_cluster launch: %s", cudaGetErrorString(cudaGetLastError()));
+        PP_CHECK_LAUNCH("k_dp_cluster");
+    }
+    dim3 gb(b->n_inst, maxV);
+    k_backtrack<<<gb, 32, 0, S(stream)>>>(*b);
+    PP_CHECK_LAUNCH("k_backtrack");
+    return PP_OK;
+}
 
 static int prm_inst(const pp_batch* b, void* stream) {
     const int maxL = b->max_L, maxV = b->max_V;
@@ -262,6 +313,7 @@ int pp_prm(const pp_batch* b, void* stream) {
     const int mode = g_dp_persist.load();
     if (b->max_L <= SR_MAX && b->max_V <= SR_MAX) {
         if (mode == 3 || (mode == 2 && b->n_inst >= 2 * num_sms())) return prm_inst(b, stream);
+        if (mode == 4) return prm_cluster(b, stream);
         if (mode == 1 || (mode == 2 && b->n_inst <= PP_DP_PERSIST_MAX)) return prm_persist(b, stream);
     }
     const int G = b->n_inst < g_dp_groups ? b->n_inst : g_dp_groups;

@@ -802,6 +802,64 @@ __device__ __forceinline__ void combine_tile_s_desc(const double* Stri, const in
     }
 }
 
+// One tile folded by ks lanes (split-K inside the CTA, for items with few
+// tiles): lane `sub` takes l' = ke - sub, ke - sub - ks, ... (descending), so
+// each lane's own remaining candidates only grow in S and a certified-monotone
+// triangle lets the lane stop on its own partial minima; the caller
+// min-reduces the ks partials with shuffles (min is exact and order-free).
+template <int TX>
+__device__ __forceinline__ void combine_tile_split(const double* Stri, const int* trio, const double* Xs, int L,
+                                                   int j, int l0, int xi0, int lA, int lB, int sub, int ks,
+                                                   bool mono, double (&acc)[16 / TX][TX]) {
+    constexpr int TL = 16 / TX;
+#pragma unroll
+    for (int a = 0; a < TL; ++a)
+#pragma unroll
+        for (int c = 0; c < TX; ++c) acc[a][c] = PP_INF;
+    int xc[TX];
+#pragma unroll
+    for (int c = 0; c < TX; ++c) xc[c] = min(xi0 + c, j + 1) - 2;
+    const int kb = max(max(1, xi0 - 1), lA);
+    const int ke = min(min(L - 1, l0 + TL - 2), lB);
+    const int nrow = min(TL, L - l0 + 1);
+    for (int lp = ke - sub; lp >= kb; lp -= ks) {
+        const double* Xr = Xs + (lp - 1) * j;
+        double q[TX];
+#pragma unroll
+        for (int c = 0; c < TX; ++c) q[c] = Xr[xc[c]];
+        if (lp >= l0) {   // the tile's diagonal: rows l <= l' are +inf
+#pragma unroll
+            for (int a = 0; a < TL; ++a) {
+                const int l = l0 + a;
+                if (l <= lp || l > L) continue;
+                const double pa = Stri[trio[lp] + (l - lp - 1)];
+#pragma unroll
+                for (int c = 0; c < TX; ++c) acc[a][c] = dmin(acc[a][c], dmax(pa, q[c]));
+            }
+            continue;
+        }
+        const double* Sr = Stri + trio[lp] + (l0 - lp - 1);
+        double p[TL];
+#pragma unroll
+        for (int a = 0; a < TL; ++a) p[a] = Sr[a];
+#pragma unroll
+        for (int a = 0; a < TL; ++a)
+#pragma unroll
+            for (int c = 0; c < TX; ++c) acc[a][c] = dmin(acc[a][c], dmax(p[a], q[c]));
+        if (mono) {
+            bool done = true;
+#pragma unroll
+            for (int a = 0; a < TL; ++a) {
+                double m = acc[a][0];
+#pragma unroll
+                for (int c = 1; c < TX; ++c) m = dmax(m, acc[a][c]);
+                done &= (a >= nrow) || p[a] >= m;
+            }
+            if (done) break;
+        }
+    }
+}
+
 template <int TX>
 __device__ __forceinline__ void combine_tiles_s(double* Wi, int i, int r, int L, int j, const double* Stri,
                                                 const int* trio, const double* Xs, int* hist, int* order,
@@ -819,9 +877,18 @@ __device__ __forceinline__ void combine_tiles_s(double* Wi, int i, int r, int L,
         atomicAdd(&hist[L - tile_nfast<TX>(L, 1 + TL * (id / ntx), 2 + TX * (id % ntx), lA, lB)], 1);
     }
     __syncthreads();
-    if (t == 0) {
-        int o = 0;
-        for (int k = 0; k < L + 2; ++k) { const int c = hist[k]; hist[k] = o; o += c; }
+    if (t < 32) {   // exclusive prefix over the L + 2 bins: one warp, 5 bins per lane
+        const int per = (L + 2 + 31) / 32, b0 = t * per;
+        int loc = 0;
+        for (int k = b0; k < min(b0 + per, L + 2); ++k) loc += hist[k];
+        int inc = loc;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, inc, off);
+            if (t >= off) inc += v;
+        }
+        int o = inc - loc;
+        for (int k = b0; k < min(b0 + per, L + 2); ++k) { const int c = hist[k]; hist[k] = o; o += c; }
     }
     __syncthreads();
     for (int k = t; k < nmine; k += blockDim.x) {
@@ -829,12 +896,28 @@ __device__ __forceinline__ void combine_tiles_s(double* Wi, int i, int r, int L,
         order[atomicAdd(&hist[L - tile_nfast<TX>(L, 1 + TL * (id / ntx), 2 + TX * (id % ntx), lA, lB)], 1)] = id;
     }
     __syncthreads();
-    for (int q = t; q < nmine; q += blockDim.x) {
+    // few tiles: ks lanes per tile split its l' range (ks a power of two <= 32)
+    int ks = 1;
+    while (ks < 32 && nmine * ks * 2 <= (int)blockDim.x) ks *= 2;
+    const int lane = t & 31;
+    for (int q0 = t; q0 < nmine * ks; q0 += blockDim.x) {
+        const int q = q0 / ks, sub = q0 % ks;
         const int id = order[q];
         const int l0 = 1 + TL * (id / ntx), xi0 = 2 + TX * (id % ntx);
         double acc[TL][TX];
-        if (mono) combine_tile_s_desc<TX>(Stri, trio, Xs, L, j, l0, xi0, lA, lB, acc);
-        else combine_tile_s<TX>(Stri, trio, Xs, L, j, l0, xi0, lA, lB, acc);
+        if (ks == 1) {
+            if (mono) combine_tile_s_desc<TX>(Stri, trio, Xs, L, j, l0, xi0, lA, lB, acc);
+            else combine_tile_s<TX>(Stri, trio, Xs, L, j, l0, xi0, lA, lB, acc);
+        } else {
+            combine_tile_split<TX>(Stri, trio, Xs, L, j, l0, xi0, lA, lB, sub, ks, mono, acc);
+            const unsigned gmask = (ks == 32 ? 0xffffffffu : ((1u << ks) - 1u)) << (lane & ~(ks - 1));
+            for (int off = 1; off < ks; off <<= 1)
+#pragma unroll
+                for (int a = 0; a < TL; ++a)
+#pragma unroll
+                    for (int c = 0; c < TX; ++c) acc[a][c] = dmin(acc[a][c], __shfl_xor_sync(gmask, acc[a][c], off));
+            if (sub != 0) continue;
+        }
 #pragma unroll
         for (int a = 0; a < TL; ++a) {
             const int l = l0 + a;

@@ -150,3 +150,12 @@ def test_partition_solver_cells_modes_identical(persistent, allow):
             solver = P.PartitionSolver(prof, clu, order, M, allow_replication=allow)
             got[mode] = [(g.workload, g.stages) for g in solver.solve_many(cells)]
         assert got[True] == got[False], s.name
+
+
+def test_cluster_per_instance_identical(persistent):
+    """One thread-block cluster per instance (mode 4) vs per-step, ragged batch + C3."""
+    rng = random.Random(777)
+    specs = _rand_specs(rng, 24, 60, 24) + [W.c2_bert24(), W.c3_gpt96(M=32, jitter_seed=7)] + W.c4_batch(4)
+    a, b = _both(persistent, specs, modes=(4, 0))
+    for s, x, y in zip(specs, a, b):
+        assert x == y, s.name
