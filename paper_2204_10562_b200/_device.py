@@ -214,9 +214,13 @@ class DeviceBatch:
     # -- results --------------------------------------------------------------
     def fetch(self):
         """Copy all outputs to host numpy (one D2H per dtype)."""
-        fo = self.d_fout.cpu().numpy()
-        io = self.d_iout.cpu().numpy()
-        order = self.d_iin[self.n_ib:].cpu().numpy()
+        # pinned destinations (torch's caching host allocator), async copies, one sync
+        srcs = (self.d_fout, self.d_iout, self.d_iin[self.n_ib:])
+        dst = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in srcs]
+        for d, t in zip(dst, srcs):
+            d.copy_(t, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        fo, io, order = (d.numpy() for d in dst)
         f = {k: fo[int(self.f_off[i]):int(self.f_off[i + 1])]
              for i, k in enumerate(("sweep_w", "sweep_mk", "sweep_bound", "best_mk", "phi", "gamma",
                                     "ar_start", "ar_end", "ev_start", "ev_end"))}

@@ -10,7 +10,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpipeplan_b200.so")
+LIB_PATH = os.environ.get("PP_LIB_OVERRIDE") or os.path.join(HERE, "libpipeplan_b200.so")
 CSRC = os.path.join(HERE, "csrc")
 REPO = os.path.dirname(HERE)
 

@@ -69,6 +69,14 @@ static int read_max_parts() {
     return v < 1 ? 1 : (v > 8 ? 8 : v);
 }
 static const int g_max_parts = read_max_parts();
+// per-step combine: split items until a launch (over the whole batch) has about
+// PP_COMBINE_WAVES x SMs CTAs
+static int read_combine_waves() {
+    const char* e = getenv("PP_COMBINE_WAVES");
+    const int v = e ? atoi(e) : 1;
+    return v < 1 ? 1 : (v > 16 ? 16 : v);
+}
+static const int g_combine_waves = read_combine_waves();
 
 static int num_sms() {
     static thread_local int dev = -1, sms = 148;
@@ -390,7 +398,7 @@ static int prm_chain(const pp_batch* b, void* stream, int total_inst) {
             // split every item over `parts` CTAs so a launch fills ~2 waves of the SMs
             // (counted over the whole batch: the groups' launches run concurrently)
             const int items = total_inst * (maxV - j);
-            int parts = (num_sms() + items - 1) / items;
+            int parts = (g_combine_waves * num_sms() + items - 1) / items;
             parts = parts < 1 ? 1 : (parts > g_max_parts ? g_max_parts : parts);
             dim3 gc(b->n_inst, maxV - j, parts);
             const size_t sm = sizeof(double) * ((maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 +

@@ -323,6 +323,17 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
 }
+// same, with an L2 eviction-priority policy (createpolicy) for data re-read
+// across wavefront steps (the stage-term triangles)
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void cp_async8_hint(double* dst, const double* src, uint64_t pol) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -972,8 +983,9 @@ __device__ __forceinline__ void combine_item_s(const pp_batch& b, const pp_insta
         // each stage term is used by j columns: for small j reading it from L2/L1
         // once beats copying the whole triangle into shared memory first
         const int s0 = (la - 1) * L - (la - 1) * la / 2, s1 = lb * L - lb * (lb + 1) / 2;
+        const uint64_t pol = l2_evict_last_policy();
         if (j > S_DIRECT_J)
-            for (int e = s0 + t; e < s1; e += blockDim.x) cp_async8(Stri + e, Sg + e);
+            for (int e = s0 + t; e < s1; e += blockDim.x) cp_async8_hint(Stri + e, Sg + e, pol);
         cp_async_commit();
         cp_async_wait<0>();
     }
