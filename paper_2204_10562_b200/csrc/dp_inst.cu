@@ -92,14 +92,22 @@ __global__ void __launch_bounds__(DI_T, 2) k_dp_inst(pp_batch b, int smem_double
                 }
                 cp_async_commit();
                 // B rows chan(l', r', r, j + r) = Mp(l') / ((r' r) cross(r', r, j + r))
+                // (copied from the row's payload-class table when it has one: same bits)
+                const int* rcls = reinterpret_cast<const int*>(ws + lay.chcls + CHAN_CLS);
+                const double* T0 = ws + lay.chan + chan_step(V, j);
+                const int64_t tcls = (int64_t)V * ((int64_t)V * V - 1) / 6;
+                const bool any_cls = rcls[0] > 0;
                 for (int e = t; e < nrow * j * nr; e += blockDim.x) {
                     int k, o, rp, q;
                     divmod_small(e, j * nr, 1.0f / (float)(j * nr), k, o);
+                    const int cls = any_cls ? rcls[la + k] : -1;
+                    double* dst = di_smem + (int64_t)k * per_row + j * j + o;
+                    if (cls >= 0) { cp_async8(dst, T0 + cls * tcls + o); continue; }
                     divmod_small(o, nr, rnr, rp, q);
                     const int r = 1 + q;
-                    di_smem[(int64_t)k * per_row + j * j + o] =
-                        mp_s[la + k] / ((double)((rp + 1) * r) * cross[cross_idx(V, j + r, r, rp + 1)]);
+                    *dst = mp_s[la + k] / ((double)((rp + 1) * r) * cross[cross_idx(V, j + r, r, rp + 1)]);
                 }
+                cp_async_commit();
                 cp_async_wait<0>();
                 __syncthreads();
                 double* X = ws + lay.X;

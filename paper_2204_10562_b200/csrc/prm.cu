@@ -61,6 +61,28 @@ __global__ void __launch_bounds__(128) k_prep(pp_batch b) {
             p = p + fwd[l - 1] + bwd[l - 1];
             ws[lay.prefix + l] = p;
         }
+        if (L <= SR_MAX && V <= SR_MAX) {   // chan payload classes (bitwise-equal M * (efwd + ebwd))
+            double* cv = ws + lay.chcls;
+            int* ci = reinterpret_cast<int*>(cv + CHAN_CLS);
+            int ncls = 0;
+            for (int lp = 1; lp < L; ++lp) {
+                const double Mp = (double)I.M * (b.efwd[I.layer_off + lp - 1] + b.ebwd[I.layer_off + lp - 1]);
+                int c = -1;
+                for (int k = 0; k < ncls; ++k)
+                    if (__double_as_longlong(cv[k]) == __double_as_longlong(Mp)) { c = k; break; }
+                if (c < 0 && ncls < CHAN_CLS) { cv[ncls] = Mp; c = ncls++; }
+                ci[1 + lp - 1] = c;
+            }
+            // a table only pays off when rows share it: drop single-row classes
+            int cnt[CHAN_CLS] = {0, 0, 0, 0}, remap[CHAN_CLS], nk = 0;
+            for (int lp = 1; lp < L; ++lp) if (ci[lp] >= 0) ++cnt[ci[lp]];
+            for (int k = 0; k < ncls; ++k) {
+                remap[k] = cnt[k] >= 2 ? nk : -1;
+                if (cnt[k] >= 2) cv[nk++] = cv[k];
+            }
+            for (int lp = 1; lp < L; ++lp) if (ci[lp] >= 0) ci[lp] = remap[ci[lp]];
+            ci[0] = nk;
+        }
     }
     // psum row ls = row: running CPython sum over le = ls..L
     if (row <= L && t == 0) {
@@ -179,6 +201,20 @@ __global__ void __launch_bounds__(128) k_base(pp_batch b, int full_rows) {
             }
         }
     }
+    if (L <= SR_MAX && V <= SR_MAX && y + 1 < V) {   // chan tables of step j = y + 1, every class
+        const int j = y + 1, nr = V - j;
+        const double* cv = ws + lay.chcls;
+        const int ncls = reinterpret_cast<const int*>(cv + CHAN_CLS)[0];
+        const double* cross = ws + lay.cross;
+        for (int c = 0; c < ncls; ++c) {
+            double* Tj = ws + lay.chan + (int64_t)c * V * ((int64_t)V * V - 1) / 6 + chan_step(V, j);
+            const double Mp = cv[c];
+            for (int e = t; e < j * nr; e += blockDim.x) {
+                const int rp = 1 + e / nr, r = 1 + e % nr;
+                Tj[e] = Mp / ((double)(rp * r) * cross[cross_idx(V, j + r, r, rp)]);   // partition.py:131,137
+            }
+        }
+    }
     if (y >= 1 && y < L) {
         const int lp = y, w = L - lp;
         double* T1 = ws + lay.T1;
@@ -248,6 +284,7 @@ __device__ __forceinline__ void stab_fill(const pp_batch& b, const pp_instance& 
     const double* T1 = ws + lay.T1;
     const double* psum = ws + lay.psum;
     const double den = (double)r * ws[lay.minpair + (int64_t)(i - r) * V + (i - 1)];
+    const uint64_t pol = l2_evict_last_policy();   // re-read by the combine of every step
     const double num = 2.0 * (double)(r - 1);
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31, nw = blockDim.x >> 5;
     int off = 0;
@@ -268,7 +305,7 @@ __device__ __forceinline__ void stab_fill(const pp_batch& b, const pp_instance& 
                 if (l > L) continue;
                 double sv = a[u];
                 if (r > 1) sv += num * p[u] / den;   // partition.py:128-129, cost.py:99
-                out[off + (l - lp - 1)] = sv;
+                st_evict_last(out + off + (l - lp - 1), sv, pol);
             }
         }
         off += L - lp;
@@ -323,13 +360,7 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
 }
-// same, with an L2 eviction-priority policy (createpolicy) for data re-read
-// across wavefront steps (the stage-term triangles)
-__device__ __forceinline__ uint64_t l2_evict_last_policy() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
-    return p;
-}
+// same, with an L2 eviction-priority policy (the stage-term triangles)
 __device__ __forceinline__ void cp_async8_hint(double* dst, const double* src, uint64_t pol) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "l"(pol) : "memory");
@@ -367,6 +398,7 @@ __global__ void __launch_bounds__(EX_T) k_expand(pp_batch b, int j, int planes_r
         const double* T1 = ws + lay.T1;
         const double* psum = ws + lay.psum;
         const double den = (double)r * ws[lay.minpair + (int64_t)(i - r) * V + (i - 1)];
+    const uint64_t pol = l2_evict_last_policy();   // re-read by the combine of every step
         const double num = 2.0 * (double)(r - 1);
         double* S = ws + lay.S + stage_idx(L, r, 0, 1);
 #pragma unroll 4
@@ -616,12 +648,22 @@ __device__ __forceinline__ void expand_row_s(const pp_batch& b, const pp_instanc
             if (W_structural(j, rp, xip, allow)) cp_async8(A + e, Wsrc + e);
             else A[e] = PP_INF;
         }
-    cp_async_commit();
-    for (int rp = 1 + warp; rp <= j; rp += nw)   // B[r'-1][r-rfirst] = chan(l', r', r, j + r)
-        for (int q = lane; q < nt; q += 32) {
-            const int r = rfirst + q;
-            B[(rp - 1) * nt + q] = Mp / ((double)(rp * r) * cross[cross_idx(V, j + r, r, rp)]);
-        }
+    // B[r'-1][r-rfirst] = chan(l', r', r, j + r): copied from the row's payload-class
+    // table (same expression, same bits), else divided here
+    const int cls = reinterpret_cast<const int*>(ws + lay.chcls + CHAN_CLS)[lp];
+    if (cls >= 0) {
+        const double* Tj = ws + lay.chan + (int64_t)cls * V * ((int64_t)V * V - 1) / 6 + chan_step(V, j);
+        for (int rp = 1 + warp; rp <= j; rp += nw)
+            for (int q = lane; q < nt; q += 32) cp_async8(B + (rp - 1) * nt + q, Tj + (rp - 1) * nr + (q + rfirst - 1));
+        cp_async_commit();
+    } else {
+        cp_async_commit();
+        for (int rp = 1 + warp; rp <= j; rp += nw)
+            for (int q = lane; q < nt; q += 32) {
+                const int r = rfirst + q;
+                B[(rp - 1) * nt + q] = Mp / ((double)(rp * r) * cross[cross_idx(V, j + r, r, rp)]);
+            }
+    }
     cp_async_wait<0>();
     __syncthreads();
     const int ntx = (j + 3) >> 2, ntr = (nt + 3) >> 2, ntiles = ntx * ntr;
