@@ -40,6 +40,11 @@ extern "C" {
 #define PP_SUM_NAIVE 2           /* CPython <= 3.11 float sum(); default is the 3.12+ Neumaier sum */
 #define PP_GIVEN_ORDER 4         /* order[] is an input (caller's DeviceOrdering); else RDO fills it */
 
+/* pp_layout reserves the first PP_WS_RESERVED doubles of the workspace for
+ * library-internal device copies of pp_batch descriptors (the per-step DP is
+ * replayed as a cached CUDA graph whose kernels read their batch from there). */
+#define PP_WS_RESERVED 512
+
 /* Build limits (checked by pp_layout). */
 #define PP_MAX_LAYERS 4096
 #define PP_MAX_GPUS 512
@@ -115,9 +120,10 @@ int pp_rdo_set_rounds(int32_t rounds);
 int pp_prm(const pp_batch *b, void *stream);
 
 /* DP schedule for batches inside the shared-memory limits (L, V <= 128):
- * 1 = one persistent dependency-driven kernel, 0 = one launch pair per
- * wavefront step, 3 = one CTA per instance, 2 (default) = auto (instance per
- * CTA for >= 2 x SMs instances, persistent for <= 6, else per step).
+ * 0 = one launch pair per wavefront step (replayed as a cached CUDA graph),
+ * 1 = one persistent dependency-driven kernel, 3 = one CTA per instance,
+ * 4 = one thread-block cluster per instance, 2 (default) = auto (one CTA per
+ * instance for >= 2 x SMs instances with L * V <= 2048, else per step).
  * Bit-identical results; a performance / test knob.  Returns the previous
  * mode.  Process-wide. */
 int pp_dp_set_persistent(int32_t mode);

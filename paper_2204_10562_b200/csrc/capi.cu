@@ -5,11 +5,19 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 
 namespace pp {
 __global__ void k_prep(pp_batch b);
+__global__ void k_prep_p(const pp_batch* bp);
+__global__ void k_base_p(const pp_batch* bp, int full_rows);
+__global__ void k_sdedup_p(const pp_batch* bp);
+__global__ void k_stab_p(const pp_batch* bp);
+__global__ void k_expand_s_p(const pp_batch* bp, int j);
+__global__ void k_combine_s_p(const pp_batch* bp, int j);
+__global__ void k_backtrack_p(const pp_batch* bp);
 __global__ void k_phi(pp_batch b);
 __global__ void k_base(pp_batch b, int full_rows);
 __global__ void k_expand(pp_batch b, int j, int planes_r, int ybase);
@@ -105,7 +113,7 @@ int pp_device_count(void) {
 int pp_layout(int32_t n, const int32_t* L, const int32_t* V, const int32_t* M, const int32_t* flags,
               pp_instance* inst, int64_t* n_layer, int64_t* n_bw, int64_t* n_order, int64_t* n_sweep,
               int64_t* n_stage, int64_t* n_ev, int64_t* n_ar, int64_t* n_ws) {
-    int64_t lo = 0, bo = 0, oo = 0, so = 0, sto = 0, wo = 0, eo = 0, ao = 0;
+    int64_t lo = 0, bo = 0, oo = 0, so = 0, sto = 0, wo = PP_WS_RESERVED, eo = 0, ao = 0;
     for (int k = 0; k < n; ++k) {
         if (L[k] < 1 || L[k] > PP_MAX_LAYERS) return fail(PP_EINVAL, "instance %d: L=%d outside 1..%d", k, L[k], PP_MAX_LAYERS);
         if (V[k] < 1 || V[k] > PP_MAX_GPUS) return fail(PP_EINVAL, "instance %d: V=%d outside 1..%d", k, V[k], PP_MAX_GPUS);
@@ -166,6 +174,9 @@ int pp_rdo(const pp_batch* b, void* stream) {
 }
 
 static int prm_chain(const pp_batch* b, void* stream, int total_inst);
+static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int total_inst);
+static int prm_groups(const pp_batch* b, void* stream);
+static int prm_steps_graph(const pp_batch* b, void* stream);
 
 // The wavefront is a chain of ~2V dependent launches whose last wave is
 // partly empty.  Instance groups run their chains on separate streams so one
@@ -182,6 +193,7 @@ static const int g_dp_groups = read_dp_groups();
 struct SideStreams {
     int dev = -1;
     cudaStream_t s[PP_DP_STREAMS];
+    cudaStream_t capture;   // origin stream of graph captures (the caller's may be the legacy stream)
     cudaEvent_t fork, join[PP_DP_STREAMS];
 };
 static thread_local SideStreams g_side;
@@ -194,9 +206,9 @@ static thread_local SideStreams g_side;
 //   3 = one CTA per instance (dp_inst.cu): the whole wavefront of an instance in
 //       one CTA, for batches with many more instances than SMs;
 //   4 = one thread-block cluster per instance (dp_cluster.cu);
-//   2 = auto (default): instance-per-CTA for >= 2 x SMs instances, persistent
-//       for <= PP_DP_PERSIST_MAX, else per-step.
-static constexpr int PP_DP_PERSIST_MAX = 6;
+//   2 = auto (default): instance-per-CTA for >= 2 x SMs small instances
+//       (L * V <= PP_DP_INST_MAX_LV), else per-step (replayed as a CUDA graph).
+static constexpr int64_t PP_DP_INST_MAX_LV = 2048;
 static std::atomic<int> g_dp_persist{2};
 
 int pp_dp_set_persistent(int32_t mode) { return g_dp_persist.exchange(mode < 0 || mode > 4 ? 2 : mode); }
@@ -320,24 +332,45 @@ int pp_prm(const pp_batch* b, void* stream) {
     if (b->n_inst <= 0) return PP_OK;
     const int mode = g_dp_persist.load();
     if (b->max_L <= SR_MAX && b->max_V <= SR_MAX) {
-        if (mode == 3 || (mode == 2 && b->n_inst >= 2 * num_sms())) return prm_inst(b, stream);
+        // many SMALL instances: one CTA each; otherwise the graph-replayed per-step schedule
+        // (it beats the persistent kernel at every batch size once launches are free)
+        const bool small = (int64_t)b->max_L * b->max_V <= PP_DP_INST_MAX_LV;
+        if (mode == 3 || (mode == 2 && small && b->n_inst >= 2 * num_sms())) return prm_inst(b, stream);
         if (mode == 4) return prm_cluster(b, stream);
-        if (mode == 1 || (mode == 2 && b->n_inst <= PP_DP_PERSIST_MAX)) return prm_persist(b, stream);
+        if (mode == 1) return prm_persist(b, stream);
     }
-    const int G = b->n_inst < g_dp_groups ? b->n_inst : g_dp_groups;
-    if (G <= 1) return prm_chain(b, stream, b->n_inst);
+    if (!(b->max_L <= SR_MAX && b->max_V <= SR_MAX)) return prm_groups(b, stream);
+    return prm_steps_graph(b, stream);
+}
+
+// descriptor slot k of the reserved workspace head (256-byte slots)
+static inline const pp_batch* desc_slot(const pp_batch* base, int k) {
+    return reinterpret_cast<const pp_batch*>(reinterpret_cast<const char*>(base) + 256 * k);
+}
+
+static int ensure_side_streams() {
     int dev = 0;
     cudaGetDevice(&dev);
-    if (g_side.dev != dev) {
-        for (int g = 0; g < PP_DP_STREAMS; ++g) {
-            if (cudaStreamCreateWithFlags(&g_side.s[g], cudaStreamNonBlocking) != cudaSuccess ||
-                cudaEventCreateWithFlags(&g_side.join[g], cudaEventDisableTiming) != cudaSuccess)
-                return fail(PP_ECUDA, "side stream creation: %s", cudaGetErrorString(cudaGetLastError()));
-        }
-        if (cudaEventCreateWithFlags(&g_side.fork, cudaEventDisableTiming) != cudaSuccess)
-            return fail(PP_ECUDA, "event creation: %s", cudaGetErrorString(cudaGetLastError()));
-        g_side.dev = dev;
+    if (g_side.dev == dev) return PP_OK;
+    for (int g = 0; g < PP_DP_STREAMS; ++g) {
+        if (cudaStreamCreateWithFlags(&g_side.s[g], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&g_side.join[g], cudaEventDisableTiming) != cudaSuccess)
+            return fail(PP_ECUDA, "side stream creation: %s", cudaGetErrorString(cudaGetLastError()));
     }
+    if (cudaEventCreateWithFlags(&g_side.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&g_side.capture, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(PP_ECUDA, "event creation: %s", cudaGetErrorString(cudaGetLastError()));
+    g_side.dev = dev;
+    return PP_OK;
+}
+
+// Instance groups on side streams (fork/join on the caller's stream).  `dev`:
+// device descriptors of the groups (per-step shared-memory path) or NULL.
+static int prm_groups_impl(const pp_batch* b, void* stream, const pp_batch* dev) {
+    const int G = b->n_inst < g_dp_groups ? b->n_inst : g_dp_groups;
+    if (G <= 1) return dev ? prm_chain_p(b, desc_slot(dev, 1), stream, b->n_inst) : prm_chain(b, stream, b->n_inst);
+    int rc;
+    if ((rc = ensure_side_streams())) return rc;
     cudaEventRecord(g_side.fork, S(stream));
     for (int g = 0; g < G; ++g) {
         const int lo = (int)((int64_t)g * b->n_inst / G), hi = (int)((int64_t)(g + 1) * b->n_inst / G);
@@ -345,11 +378,83 @@ int pp_prm(const pp_batch* b, void* stream) {
         bg.inst = b->inst + lo;
         bg.n_inst = hi - lo;
         cudaStreamWaitEvent(g_side.s[g], g_side.fork, 0);
-        const int rc = prm_chain(&bg, g_side.s[g], b->n_inst);
+        rc = dev ? prm_chain_p(&bg, desc_slot(dev, 1 + g), g_side.s[g], b->n_inst) : prm_chain(&bg, g_side.s[g], b->n_inst);
         if (rc) return rc;
         cudaEventRecord(g_side.join[g], g_side.s[g]);
         cudaStreamWaitEvent(S(stream), g_side.join[g], 0);
     }
+    return PP_OK;
+}
+static int prm_groups(const pp_batch* b, void* stream) { return prm_groups_impl(b, stream, nullptr); }
+
+// The per-step schedule is ~2V dependent launches per instance group: launched
+// one by one the host's launch rate is the bound (~3.5 us per launch, measured:
+// the empty-kernel chain alone took 1.8 ms on C3).  It is captured once into a
+// CUDA graph and replayed; its kernels read their batch descriptor from the
+// reserved head of the workspace, so the graph stays valid for every batch of
+// the same shape in the same workspace (the descriptors are rewritten per call).
+struct GraphKey {   // what the captured launches bake in: descriptor location and grid shapes
+    const void* ws;
+    int n_inst, max_L, max_V, G, dev;
+    bool operator==(const GraphKey& o) const {
+        return ws == o.ws && n_inst == o.n_inst && max_L == o.max_L && max_V == o.max_V && G == o.G && dev == o.dev;
+    }
+};
+struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec;
+};
+static thread_local std::vector<GraphEntry> g_graphs;
+static constexpr size_t PP_GRAPH_CACHE = 8;
+static_assert(sizeof(pp_batch) <= 256, "descriptor slot");
+static constexpr int PP_DESC_SLOT = 256 / sizeof(double);
+
+static int prm_steps_graph(const pp_batch* b, void* stream) {
+    const int G = b->n_inst < g_dp_groups ? b->n_inst : g_dp_groups;
+    // descriptors: slot 1 + g = group g (slot 1 = the whole batch when G == 1)
+    pp_batch hd[1 + PP_DP_STREAMS];
+    hd[0] = *b;
+    const int ng = G <= 1 ? 1 : G;
+    for (int g = 0; g < ng; ++g) {
+        const int lo = (int)((int64_t)g * b->n_inst / ng), hi = (int)((int64_t)(g + 1) * b->n_inst / ng);
+        hd[1 + g] = *b;
+        hd[1 + g].inst = b->inst + lo;
+        hd[1 + g].n_inst = hi - lo;
+    }
+    pp_batch* dev = reinterpret_cast<pp_batch*>(b->ws);
+    for (int g = 0; g <= ng; ++g)   // pageable source: staged by the driver, safe to reuse at once
+        if (cudaMemcpyAsync(b->ws + g * PP_DESC_SLOT, &hd[g], sizeof(pp_batch), cudaMemcpyHostToDevice, S(stream)) !=
+            cudaSuccess)
+            return fail(PP_ECUDA, "descriptor upload: %s", cudaGetErrorString(cudaGetLastError()));
+    int d = 0;
+    cudaGetDevice(&d);
+    const GraphKey key{b->ws, b->n_inst, b->max_L, b->max_V, G, d};
+    cudaGraphExec_t exec = nullptr;
+    for (size_t k = 0; k < g_graphs.size(); ++k)
+        if (g_graphs[k].key == key) { exec = g_graphs[k].exec; break; }
+    if (!exec) {
+        int rc;
+        if ((rc = ensure_side_streams())) return rc;
+        cudaGraph_t graph;
+        cudaStream_t cs = g_side.capture;
+        if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+            return fail(PP_ECUDA, "graph capture: %s", cudaGetErrorString(cudaGetLastError()));
+        rc = prm_groups_impl(b, cs, dev);
+        const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+        if (rc) return rc;
+        if (ce != cudaSuccess) return fail(PP_ECUDA, "graph capture: %s", cudaGetErrorString(ce));
+        const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ie != cudaSuccess) return fail(PP_ECUDA, "graph instantiate: %s", cudaGetErrorString(ie));
+        if (g_graphs.size() >= PP_GRAPH_CACHE) {
+            cudaGraphExecDestroy(g_graphs.front().exec);
+            g_graphs.erase(g_graphs.begin());
+        }
+        g_graphs.push_back({key, exec});
+    }
+    if (cudaGraphLaunch(exec, S(stream)) != cudaSuccess)
+        return fail(PP_ECUDA, "graph launch: %s", cudaGetErrorString(cudaGetLastError()));
+    g_launches.fetch_add(1 + 2 * (int64_t)ng * (b->max_V - 1) + 5 * ng, std::memory_order_relaxed);
     return PP_OK;
 }
 
@@ -372,6 +477,48 @@ static int prm_prep(const pp_batch* b, void* stream) {
             PP_CHECK_LAUNCH("k_stab");
         }
     }
+    return PP_OK;
+}
+
+// prm_chain for the shared-memory path with device descriptors (graph capture):
+// `b` supplies the host-side shape, `db` is the same batch in device memory.
+static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int total_inst) {
+    const int maxL = b->max_L, maxV = b->max_V;
+    dim3 gp(b->n_inst, maxL > maxV ? maxL : maxV);
+    k_prep_p<<<gp, 128, 0, S(stream)>>>(db);
+    PP_CHECK_LAUNCH("k_prep");
+    k_base_p<<<gp, 128, 0, S(stream)>>>(db, 0);
+    PP_CHECK_LAUNCH("k_base");
+    k_sdedup_p<<<b->n_inst, 128, 0, S(stream)>>>(db);
+    PP_CHECK_LAUNCH("k_sdedup");
+    if (maxV > 1 && maxL > 1) {
+        dim3 gs(b->n_inst, maxV - 1);
+        k_stab_p<<<gs, 128, 0, S(stream)>>>(db);
+        PP_CHECK_LAUNCH("k_stab");
+    }
+    const size_t ex_smem = sizeof(double) * (size_t)maxV * maxV;
+    const size_t cs_smem = sizeof(double) * ((maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 +
+                                             (size_t)(maxL > 1 ? maxL - 1 : 0) * maxV);
+    cudaFuncSetAttribute(k_expand_s_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ex_smem);
+    cudaFuncSetAttribute(k_combine_s_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs_smem);
+    for (int j = 1; j < maxV; ++j) {
+        if (maxL > 1) {
+            dim3 ge(b->n_inst, maxL - 1);
+            k_expand_s_p<<<ge, 128, sizeof(double) * (size_t)j * maxV, S(stream)>>>(db, j);
+            PP_CHECK_LAUNCH("k_expand_s");
+        }
+        const int items = total_inst * (maxV - j);
+        int parts = (g_combine_waves * num_sms() + items - 1) / items;
+        parts = parts < 1 ? 1 : (parts > g_max_parts ? g_max_parts : parts);
+        dim3 gc(b->n_inst, maxV - j, parts);
+        const size_t sm = sizeof(double) * ((maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 +
+                                            (size_t)(maxL > 1 ? maxL - 1 : 0) * j);
+        k_combine_s_p<<<gc, 256, sm, S(stream)>>>(db, j);
+        PP_CHECK_LAUNCH("k_combine_s");
+    }
+    dim3 gb(b->n_inst, maxV);
+    k_backtrack_p<<<gb, 32, 0, S(stream)>>>(db);
+    PP_CHECK_LAUNCH("k_backtrack");
     return PP_OK;
 }
 

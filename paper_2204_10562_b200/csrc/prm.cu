@@ -40,7 +40,7 @@ __device__ __forceinline__ double W_at(const double* W, int L, int i, int l, int
 // grid (n_inst, max(maxL, maxV)); row y handles psum row ls=y+1, minpair row
 // lo=y+1 and the cross table of i=y+1.  Row 0 also computes prefix and phi.
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_prep(pp_batch b) {
+__device__ __forceinline__ void prep_body(const pp_batch& b) {
     const pp_instance I = b.inst[blockIdx.x];
     const int L = I.L, V = I.V;
     const bool naive = I.flags & PP_SUM_NAIVE;
@@ -122,6 +122,11 @@ __global__ void __launch_bounds__(128) k_prep(pp_batch b) {
         }
     }
 }
+__global__ void __launch_bounds__(128) k_prep(pp_batch b) { prep_body(b); }
+__global__ void __launch_bounds__(128) k_prep_p(const pp_batch* __restrict__ bp) {
+    const pp_batch b = *bp;
+    prep_body(b);
+}
 
 // phi (cost.py:126-142): max(p_max * b_max, d_max) / Gamma * (1/b_min - 1/b_max),
 // 0 on single-GPU or uniform clusters.  One CTA (128 threads) per instance.
@@ -170,7 +175,7 @@ __global__ void __launch_bounds__(128) k_phi(pp_batch b) {
 //   l' = y in [1, L): T1[r][l'][l] = (M * span(l'+1, l)) / r for r = 1..V-1, l > l'
 //                    (partition.py:127; the i-independent half of every stage term)
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_base(pp_batch b, int full_rows) {
+__device__ __forceinline__ void base_body(const pp_batch& b, int full_rows) {
     const pp_instance I = b.inst[blockIdx.x];
     const int L = I.L, V = I.V, M = I.M;
     const bool allow = I.flags & PP_ALLOW_REPLICATION;
@@ -224,6 +229,11 @@ __global__ void __launch_bounds__(128) k_base(pp_batch b, int full_rows) {
         }
     }
 }
+__global__ void __launch_bounds__(128) k_base(pp_batch b, int full_rows) { base_body(b, full_rows); }
+__global__ void __launch_bounds__(128) k_base_p(const pp_batch* __restrict__ bp, int full_rows) {
+    const pp_batch b = *bp;
+    base_body(b, full_rows);
+}
 
 // ----------------------------------------------------------------------------
 // Stage-term tables for the shared-memory path.  S(l', l, r, i) depends on the
@@ -234,7 +244,7 @@ __global__ void __launch_bounds__(128) k_base(pp_batch b, int full_rows) {
 // k_stab: one CTA per canonical item fills its packed triangle
 //   row l' (1..L-1): S(l', l) = T1[r][l'][l] (+ sync if r > 1), l = l'+1..L.
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_sdedup(pp_batch b) {
+__device__ __forceinline__ void sdedup_body(const pp_batch& b) {
     const pp_instance I = b.inst[blockIdx.x];
     const int L = I.L, V = I.V;
     if (L > SR_MAX || V > SR_MAX) return;
@@ -268,6 +278,11 @@ __global__ void __launch_bounds__(128) k_sdedup(pp_batch b) {
             *e = (*e >= 0) ? base + *e : sidx[(r - 1) * V + (-*e - 1)];
         }
     }
+}
+__global__ void __launch_bounds__(128) k_sdedup(pp_batch b) { sdedup_body(b); }
+__global__ void __launch_bounds__(128) k_sdedup_p(const pp_batch* __restrict__ bp) {
+    const pp_batch b = *bp;
+    sdedup_body(b);
 }
 
 __device__ __forceinline__ void stab_fill(const pp_batch& b, const pp_instance& I, int r, int i) {
@@ -330,11 +345,16 @@ __device__ __forceinline__ void stab_fill(const pp_batch& b, const pp_instance& 
 }
 
 // grid (n_inst, maxV - 1): CTA (instance, r) fills the canonical slots of width r
-__global__ void __launch_bounds__(128) k_stab(pp_batch b) {
+__device__ __forceinline__ void stab_body(const pp_batch& b) {
     const pp_instance I = b.inst[blockIdx.x];
     const int r = blockIdx.y + 1;
     if (I.L > SR_MAX || I.V > SR_MAX || r >= I.V) return;
     for (int i = r + 1; i <= I.V; ++i) stab_fill(b, I, r, i);
+}
+__global__ void __launch_bounds__(128) k_stab(pp_batch b) { stab_body(b); }
+__global__ void __launch_bounds__(128) k_stab_p(const pp_batch* __restrict__ bp) {
+    const pp_batch b = *bp;
+    stab_body(b);
 }
 
 // (min, max) micro-kernel: a thread owns a TA x TB register tile and folds one
@@ -725,6 +745,14 @@ __global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
     extern __shared__ __align__(16) double ex_smem[];
     expand_row_s(b, I, j, lp, 1, ex_smem);
 }
+__global__ void __launch_bounds__(128) k_expand_s_p(const pp_batch* __restrict__ bp, int j) {
+    const pp_batch b = *bp;
+    const pp_instance I = b.inst[blockIdx.x];
+    const int lp = blockIdx.y + 1;
+    if (j >= I.V || lp > I.L - 1) return;
+    extern __shared__ __align__(16) double ex_smem[];
+    expand_row_s(b, I, j, lp, 1, ex_smem);
+}
 
 // combine, step j: one CTA per (instance, r), target i = j + r.  smem: the
 // stage terms of the item as a packed triangle (row l' holds l = l'+1..L,
@@ -1046,6 +1074,14 @@ __global__ void __launch_bounds__(256, 2) k_combine_s(pp_batch b, int j) {
     __shared__ int s_order[1024];
     combine_item_s(b, I, j, blockIdx.y + 1, blockIdx.z, gridDim.z, cs_smem, s_hist, s_order, false);
 }
+__global__ void __launch_bounds__(256, 2) k_combine_s_p(const pp_batch* __restrict__ bp, int j) {
+    const pp_batch b = *bp;
+    const pp_instance I = b.inst[blockIdx.x];
+    extern __shared__ __align__(16) double cs_smem[];
+    __shared__ int s_hist[SR_MAX + 2];
+    __shared__ int s_order[1024];
+    combine_item_s(b, I, j, blockIdx.y + 1, blockIdx.z, gridDim.z, cs_smem, s_hist, s_order, false);
+}
 
 // ----------------------------------------------------------------------------
 // Backtrack: re-derive the reference's first-found realizing (l', r') of a
@@ -1114,7 +1150,7 @@ __device__ void dp_walk(const pp_batch& b, const pp_instance& I, int l, int x, i
 }
 
 // best_partition(xi) for every xi (partition.py:144-162).  grid (n_inst, maxV), block 32.
-__global__ void __launch_bounds__(32) k_backtrack(pp_batch b) {
+__device__ __forceinline__ void backtrack_body(const pp_batch& b) {
     const pp_instance I = b.inst[blockIdx.x];
     const int xi = blockIdx.y + 1;
     const int L = I.L, V = I.V;
@@ -1139,6 +1175,11 @@ __global__ void __launch_bounds__(32) k_backtrack(pp_batch b) {
     if (br == 0) return;
     const int64_t st = I.stage_off + (int64_t)xi * (xi - 1) / 2;
     dp_walk(b, I, L, xi, br, V, best, b.stage_ls + st, b.stage_le + st, b.stage_dlo + st, b.stage_dhi + st);
+}
+__global__ void __launch_bounds__(32) k_backtrack(pp_batch b) { backtrack_body(b); }
+__global__ void __launch_bounds__(32) k_backtrack_p(const pp_batch* __restrict__ bp) {
+    const pp_batch b = *bp;
+    backtrack_body(b);
 }
 
 // PartitionSolver.solve queries (partition.py:95-142).  One warp per query.
