@@ -139,6 +139,11 @@ int pp_dp_set_early_exit(int32_t on);
  * buffer d_buf of 4 * cap entries; NULL disables.  Not on the planning path. */
 int pp_dp_trace(uint64_t *d_buf, int32_t cap);
 
+/* Debug: per-CTA timeline of the per-step expand / combine kernels (4 x u64 per
+ * CTA: kind << 56 | j << 40 | smid << 32 | block id, start, end, 0); NULL
+ * disables.  Not on the planning path. */
+int pp_step_trace(uint64_t *d_buf, int32_t cap);
+
 /* simulate_pe + lemma1_bound for every feasible xi plan (scheduler.py:75-238):
  * fills sweep_mk, sweep_bound. */
 int pp_pe_sweep(const pp_batch *b, void *stream);

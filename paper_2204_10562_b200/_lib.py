@@ -87,7 +87,7 @@ EXPORTS = ("pp_version", "pp_last_error", "pp_device_count", "pp_layout", "pp_rd
            "pp_pe_sweep", "pp_select", "pp_spp", "pp_prm_query", "pp_simulate", "pp_min_cut",
            "pp_launch_count", "pp_phi", "pp_peak_minmax", "pp_format_trace", "pp_validate_schedule",
            "pp_rdo_set_rounds", "pp_dp_set_persistent", "pp_dp_trace",
-           "pp_dp_set_early_exit")
+           "pp_dp_set_early_exit", "pp_step_trace")
 
 _lib = None
 
@@ -139,6 +139,8 @@ def _declare(L):
     L.pp_dp_set_persistent.restype = C.c_int
     L.pp_dp_set_early_exit.argtypes = [i32]
     L.pp_dp_set_early_exit.restype = C.c_int
+    L.pp_step_trace.argtypes = [vp, i32]
+    L.pp_step_trace.restype = C.c_int
     L.pp_dp_trace.argtypes = [vp, i32]
     L.pp_dp_trace.restype = C.c_int
 

@@ -292,6 +292,18 @@ int pp_dp_set_early_exit(int32_t on) {
     return prev;
 }
 
+// Debug: per-CTA timeline of the per-step expand / combine kernels (4 x u64 per
+// CTA, cap records); NULL disables.  Resets the record counter.
+int pp_step_trace(uint64_t* d_buf, int32_t cap) {
+    unsigned long long* p = reinterpret_cast<unsigned long long*>(d_buf);
+    const int zero = 0;
+    if (cudaMemcpyToSymbol(g_step_trace, &p, sizeof(p)) != cudaSuccess ||
+        cudaMemcpyToSymbol(g_step_trace_cap, &cap, sizeof(cap)) != cudaSuccess ||
+        cudaMemcpyToSymbol(g_step_trace_n, &zero, sizeof(zero)) != cudaSuccess)
+        return fail(PP_ECUDA, "pp_step_trace: %s", cudaGetErrorString(cudaGetLastError()));
+    return PP_OK;
+}
+
 // Debug: per-task timeline of the persistent DP into a caller device buffer of
 // 4 * cap u64 (NULL / 0 disables).  Not part of the planning path.
 int pp_dp_trace(uint64_t* d_buf, int32_t cap) {

@@ -357,6 +357,34 @@ __global__ void __launch_bounds__(128) k_stab_p(const pp_batch* __restrict__ bp)
     stab_body(b);
 }
 
+// Debug timeline of the per-step kernels (tools/step_trace.py): one record of
+// 4 x u64 per CTA when g_step_trace is set: (kind << 56 | j << 40 | smid << 32 | block
+// linear id), start, end, 0 (globaltimer ns).
+__device__ unsigned long long* g_step_trace = nullptr;
+__device__ int g_step_trace_cap = 0;
+__device__ int g_step_trace_n = 0;
+struct StepTrace {
+    unsigned long long t0 = 0;
+    __device__ __forceinline__ void begin() {
+        if (g_step_trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    }
+    __device__ __forceinline__ void end(int kind, int j) {
+        if (!g_step_trace) return;
+        __syncthreads();
+        if (threadIdx.x != 0) return;
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        const int k = atomicAdd(&g_step_trace_n, 1);
+        if (k >= g_step_trace_cap) return;
+        unsigned smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        const unsigned long long bid = blockIdx.x + (unsigned long long)gridDim.x * (blockIdx.y + (unsigned long long)gridDim.y * blockIdx.z);
+        unsigned long long* r = g_step_trace + 4 * (int64_t)k;
+        r[0] = ((unsigned long long)kind << 56) | ((unsigned long long)j << 40) | ((unsigned long long)smid << 32) | (bid & 0xffffffffu);
+        r[1] = t0; r[2] = t1; r[3] = 0;
+    }
+};
+
 // (min, max) micro-kernel: a thread owns a TA x TB register tile and folds one
 // K index per step, acc[a][c] = min(acc[a][c], max(p[a], q[c])).
 template <int TA, int TB>
@@ -746,12 +774,15 @@ __global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
     expand_row_s(b, I, j, lp, 1, ex_smem);
 }
 __global__ void __launch_bounds__(128) k_expand_s_p(const pp_batch* __restrict__ bp, int j) {
+    StepTrace tr;
+    tr.begin();
     const pp_batch b = *bp;
     const pp_instance I = b.inst[blockIdx.x];
     const int lp = blockIdx.y + 1;
     if (j >= I.V || lp > I.L - 1) return;
     extern __shared__ __align__(16) double ex_smem[];
     expand_row_s(b, I, j, lp, 1, ex_smem);
+    tr.end(1, j);
 }
 
 // combine, step j: one CTA per (instance, r), target i = j + r.  smem: the
@@ -1075,12 +1106,15 @@ __global__ void __launch_bounds__(256, 2) k_combine_s(pp_batch b, int j) {
     combine_item_s(b, I, j, blockIdx.y + 1, blockIdx.z, gridDim.z, cs_smem, s_hist, s_order, false);
 }
 __global__ void __launch_bounds__(256, 2) k_combine_s_p(const pp_batch* __restrict__ bp, int j) {
+    StepTrace tr;
+    tr.begin();
     const pp_batch b = *bp;
     const pp_instance I = b.inst[blockIdx.x];
     extern __shared__ __align__(16) double cs_smem[];
     __shared__ int s_hist[SR_MAX + 2];
     __shared__ int s_order[1024];
     combine_item_s(b, I, j, blockIdx.y + 1, blockIdx.z, gridDim.z, cs_smem, s_hist, s_order, false);
+    tr.end(2, j);
 }
 
 // ----------------------------------------------------------------------------

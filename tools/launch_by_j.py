@@ -7,7 +7,7 @@ hi = next(i for i, r in enumerate(rows) if 'Kernel Name' in r)
 h = rows[hi]; data = rows[hi + 1:]
 ki = h.index('Kernel Name'); vi = h.index('Metric Value')
 seq = [(r[ki].split('(')[0].replace('void ', '').replace('pp::', ''), float(r[vi].replace(',', '')) / 1e3) for r in data]
-for name in ("k_combine_s", "k_expand_s"):
+for name in ("k_combine_s", "k_expand_s", "k_combine_s_p", "k_expand_s_p"):
     v = np.array([x for n, x in seq if n == name])
     if v.size % groups:
         continue
