@@ -85,6 +85,8 @@ static int read_combine_waves() {
     return v < 1 ? 1 : (v > 16 ? 16 : v);
 }
 static const int g_combine_waves = read_combine_waves();
+// programmatic dependent launch in the per-step chain (PP_PDL=0 disables)
+static const int g_pdl = getenv("PP_PDL") ? atoi(getenv("PP_PDL")) : 1;
 
 static int num_sms() {
     static thread_local int dev = -1, sms = 148;
@@ -513,19 +515,37 @@ static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int 
                                              (size_t)(maxL > 1 ? maxL - 1 : 0) * maxV);
     cudaFuncSetAttribute(k_expand_s_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ex_smem);
     cudaFuncSetAttribute(k_combine_s_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs_smem);
+    // programmatic dependent launch between consecutive wavefront kernels: each
+    // stages its producer-independent operands while its predecessor drains
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
     for (int j = 1; j < maxV; ++j) {
         if (maxL > 1) {
-            dim3 ge(b->n_inst, maxL - 1);
-            k_expand_s_p<<<ge, 128, sizeof(double) * (size_t)j * maxV, S(stream)>>>(db, j);
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(b->n_inst, maxL - 1);
+            cfg.blockDim = dim3(128);
+            cfg.dynamicSmemBytes = sizeof(double) * (size_t)j * maxV;
+            cfg.stream = S(stream);
+            cfg.attrs = pdl;
+            cfg.numAttrs = 1;
+            if (cudaLaunchKernelEx(&cfg, k_expand_s_p, db, j) != cudaSuccess)
+                return fail(PP_ECUDA, "k_expand_s launch: %s", cudaGetErrorString(cudaGetLastError()));
             PP_CHECK_LAUNCH("k_expand_s");
         }
         const int items = total_inst * (maxV - j);
         int parts = (g_combine_waves * num_sms() + items - 1) / items;
         parts = parts < 1 ? 1 : (parts > g_max_parts ? g_max_parts : parts);
-        dim3 gc(b->n_inst, maxV - j, parts);
-        const size_t sm = sizeof(double) * ((maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 +
-                                            (size_t)(maxL > 1 ? maxL - 1 : 0) * j);
-        k_combine_s_p<<<gc, 256, sm, S(stream)>>>(db, j);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(b->n_inst, maxV - j, parts);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = sizeof(double) * ((maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 +
+                                                 (size_t)(maxL > 1 ? maxL - 1 : 0) * j);
+        cfg.stream = S(stream);
+        cfg.attrs = pdl;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, k_combine_s_p, db, j) != cudaSuccess)
+            return fail(PP_ECUDA, "k_combine_s launch: %s", cudaGetErrorString(cudaGetLastError()));
         PP_CHECK_LAUNCH("k_combine_s");
     }
     dim3 gb(b->n_inst, maxV);

@@ -385,6 +385,12 @@ struct StepTrace {
     }
 };
 
+// Programmatic dependent launch (the graph-replayed per-step chain): a kernel
+// lets its successor launch as soon as all its CTAs run, and the successor
+// stages its producer-independent operands before waiting (no-ops without PDL).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // (min, max) micro-kernel: a thread owns a TA x TB register tile and folds one
 // K index per step, acc[a][c] = min(acc[a][c], max(p[a], q[c])).
 template <int TA, int TB>
@@ -688,14 +694,8 @@ __device__ __forceinline__ void expand_row_s(const pp_batch& b, const pp_instanc
     const bool allow = I.flags & PP_ALLOW_REPLICATION;
     const int lane = t & 31;
     const int warp = t >> 5, nw = blockDim.x >> 5;
-    // A[r'-1][xi'-1] = W_j(l', xi', r'): materialised cells by cp.async (all in
-    // flight at once), structural ones (never written by the DP) as +inf
-    for (int rp = 1 + warp; rp <= j; rp += nw)
-        for (int xip = 1 + lane; xip <= j; xip += 32) {
-            const int e = (rp - 1) * j + (xip - 1);
-            if (W_structural(j, rp, xip, allow)) cp_async8(A + e, Wsrc + e);
-            else A[e] = PP_INF;
-        }
+    // B first: it depends only on tables built before the wavefront, so under
+    // PDL it overlaps the previous kernel's tail; A (slice j) after the wait.
     // B[r'-1][r-rfirst] = chan(l', r', r, j + r): copied from the row's payload-class
     // table (same expression, same bits), else divided here
     const int cls = reinterpret_cast<const int*>(ws + lay.chcls + CHAN_CLS)[lp];
@@ -712,6 +712,16 @@ __device__ __forceinline__ void expand_row_s(const pp_batch& b, const pp_instanc
                 B[(rp - 1) * nt + q] = Mp / ((double)(rp * r) * cross[cross_idx(V, j + r, r, rp)]);
             }
     }
+    pdl_wait();
+    // A[r'-1][xi'-1] = W_j(l', xi', r'): materialised cells by cp.async (all in
+    // flight at once), structural ones (never written by the DP) as +inf
+    for (int rp = 1 + warp; rp <= j; rp += nw)
+        for (int xip = 1 + lane; xip <= j; xip += 32) {
+            const int e = (rp - 1) * j + (xip - 1);
+            if (W_structural(j, rp, xip, allow)) cp_async8(A + e, Wsrc + e);
+            else A[e] = PP_INF;
+        }
+    cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
     const int ntx = (j + 3) >> 2, ntr = (nt + 3) >> 2, ntiles = ntx * ntr;
@@ -774,6 +784,7 @@ __global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
     expand_row_s(b, I, j, lp, 1, ex_smem);
 }
 __global__ void __launch_bounds__(128) k_expand_s_p(const pp_batch* __restrict__ bp, int j) {
+    pdl_trigger();
     StepTrace tr;
     tr.begin();
     const pp_batch b = *bp;
@@ -1076,17 +1087,19 @@ __device__ __forceinline__ void combine_item_s(const pp_batch& b, const pp_insta
     const double* Sg;
     const int slot = reinterpret_cast<const int*>(ws + lay.sidx)[(r - 1) * V + (i - 1)];
     {
-        const double* Xg = ws + lay.X + X_base(L, i, r);
-        if (!x_staged)
-            for (int e = (la - 1) * j + t; e < lb * j; e += blockDim.x) cp_async8(Xs + e, Xg + e);
+        // the stage-term triangle (built before the wavefront) first: under PDL it
+        // overlaps the previous kernel's tail; X (this step's expand) after the wait
         const int ns = (L - 1) * L / 2;
         Sg = ws + lay.Stab + (int64_t)slot * ns;
-        // each stage term is used by j columns: for small j reading it from L2/L1
-        // once beats copying the whole triangle into shared memory first
         const int s0 = (la - 1) * L - (la - 1) * la / 2, s1 = lb * L - lb * (lb + 1) / 2;
         const uint64_t pol = l2_evict_last_policy();
         if (j > S_DIRECT_J)
             for (int e = s0 + t; e < s1; e += blockDim.x) cp_async8_hint(Stri + e, Sg + e, pol);
+        cp_async_commit();
+        pdl_wait();
+        const double* Xg = ws + lay.X + X_base(L, i, r);
+        if (!x_staged)
+            for (int e = (la - 1) * j + t; e < lb * j; e += blockDim.x) cp_async8(Xs + e, Xg + e);
         cp_async_commit();
         cp_async_wait<0>();
     }
@@ -1106,6 +1119,7 @@ __global__ void __launch_bounds__(256, 2) k_combine_s(pp_batch b, int j) {
     combine_item_s(b, I, j, blockIdx.y + 1, blockIdx.z, gridDim.z, cs_smem, s_hist, s_order, false);
 }
 __global__ void __launch_bounds__(256, 2) k_combine_s_p(const pp_batch* __restrict__ bp, int j) {
+    pdl_trigger();
     StepTrace tr;
     tr.begin();
     const pp_batch b = *bp;
