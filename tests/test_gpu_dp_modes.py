@@ -159,3 +159,26 @@ def test_cluster_per_instance_identical(persistent):
     a, b = _both(persistent, specs, modes=(4, 0))
     for s, x, y in zip(specs, a, b):
         assert x == y, s.name
+
+
+def test_graph_replay_across_batches(persistent):
+    """The per-step DP is replayed from a cached CUDA graph keyed on (workspace,
+    shape); batches of one shape with different data (and repeated runs) must
+    each give their own, exact results."""
+    from paper_2204_10562_b200 import _device, planner
+    specs_a = [W.c3_gpt96(M=m, nodes=2, per_node=8) for m in (8, 32, 128)]
+    specs_b = [W.c3_gpt96(M=m, jitter_seed=11, nodes=2, per_node=8) for m in (8, 32, 128)]
+    persistent(1)
+    want_a = P.spp_many([s.to_model() for s in specs_a])
+    want_b = P.spp_many([s.to_model() for s in specs_b])
+    persistent(0)
+    for specs, want in ((specs_a, want_a), (specs_b, want_b), (specs_a, want_a)):
+        models = [s.to_model() for s in specs]
+        items, packs = planner._items(models)
+        db = _device.DeviceBatch(items, capture_events=True)
+        for _ in range(2):   # first run may capture, second replays
+            db.run("spp")
+            h = db.fetch()
+            got = [planner._decode(db, h, k, items[k][1], packs[k]) for k in range(len(items))]
+            assert got == want
+        del db
