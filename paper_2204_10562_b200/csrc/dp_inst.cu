@@ -19,10 +19,9 @@ namespace pp {
 
 constexpr int DI_T = 256;
 
-template <int TX>
+template <int TX, int TL = 16 / TX>
 __device__ __forceinline__ void dp_inst_combine(const pp_batch& b, const pp_instance& I, int j, int ra, int rb,
                                                 double* smem, int* trio) {
-    constexpr int TL = 16 / TX;
     const int L = I.L, V = I.V;
     const WsLayout lay = ws_layout(L, V);
     double* ws = b.ws + I.ws_off;
@@ -38,8 +37,8 @@ __device__ __forceinline__ void dp_inst_combine(const pp_batch& b, const pp_inst
         const int slot = reinterpret_cast<const int*>(ws + lay.sidx)[(r - 1) * V + (i - 1)];
         const bool mono = g_combine_early_exit && reinterpret_cast<const int*>(ws + lay.smono)[slot];
         double acc[TL][TX];
-        if (mono) combine_tile_s_desc<TX>(Stri, trio, Xs, L, j, l0, xi0, 1, L - 1, acc);
-        else combine_tile_s<TX>(Stri, trio, Xs, L, j, l0, xi0, 1, L - 1, acc);
+        if (mono) combine_tile_s_desc<TX, TL>(Stri, trio, Xs, L, j, l0, xi0, 1, L - 1, acc);
+        else combine_tile_s<TX, TL>(Stri, trio, Xs, L, j, l0, xi0, 1, L - 1, acc);
         double* Wi = ws + lay.W + W_base(L, i);
 #pragma unroll
         for (int a = 0; a < TL; ++a) {

@@ -802,13 +802,15 @@ __global__ void __launch_bounds__(128) k_expand_s_p(const pp_batch* __restrict__
 // combine reads stage terms straight from global memory for j <= this (0 = always
 // stage them in shared memory; j <= 8 measured no better on B200)
 constexpr int S_DIRECT_J = 0;
+#ifndef COMBINE_TL4
+#define COMBINE_TL4 2   // combine register tile 2 l x 4 xi (8 accumulators: 3 CTAs / SM)
+#endif
 // combine stops scanning l' once no remaining candidate can lower a cell (needs a
 // certified monotone stage-term triangle, k_stab); pp_dp_set_early_exit toggles it
 __device__ int g_combine_early_exit = 1;
 
-template <int TX>
+template <int TX, int TL = 16 / TX>
 __device__ __forceinline__ int tile_nfast(int L, int l0, int xi0, int lA, int lB) {
-    constexpr int TL = 16 / TX;
     const int kb = max(max(1, xi0 - 1), lA), ke = min(min(L - 1, l0 + TL - 2), lB);
     return max(0, min(ke, l0 - 1) - kb + 1);
 }
@@ -817,10 +819,9 @@ __device__ __forceinline__ int tile_nfast(int L, int l0, int xi0, int lA, int lB
 // (row pointers advance incrementally through the packed triangle), so lanes
 // whose tiles have equal trip counts run in lockstep even though they start
 // at different l'.
-template <int TX>
+template <int TX, int TL = 16 / TX>
 __device__ __forceinline__ void combine_tile_s(const double* Stri, const int* trio, const double* Xs, int L, int j,
-                                               int l0, int xi0, int lA, int lB, double (&acc)[16 / TX][TX]) {
-    constexpr int TL = 16 / TX;
+                                               int l0, int xi0, int lA, int lB, double (&acc)[TL][TX]) {
 #pragma unroll
     for (int a = 0; a < TL; ++a)
 #pragma unroll
@@ -866,11 +867,10 @@ __device__ __forceinline__ void combine_tile_s(const double* Stri, const int* tr
 // candidates of row a at l'' < l' are >= S(l'', l0+a) >= S(l', l0+a) = p[a],
 // so once p[a] >= max_c acc[a][c] for every row, no remaining l' can lower any
 // cell and the fold stops (the min is unchanged, so the bits are too).
-template <int TX>
+template <int TX, int TL = 16 / TX>
 __device__ __forceinline__ void combine_tile_s_desc(const double* Stri, const int* trio, const double* Xs, int L,
                                                     int j, int l0, int xi0, int lA, int lB,
-                                                    double (&acc)[16 / TX][TX]) {
-    constexpr int TL = 16 / TX;
+                                                    double (&acc)[TL][TX]) {
 #pragma unroll
     for (int a = 0; a < TL; ++a)
 #pragma unroll
@@ -930,11 +930,10 @@ __device__ __forceinline__ void combine_tile_s_desc(const double* Stri, const in
 // each lane's own remaining candidates only grow in S and a certified-monotone
 // triangle lets the lane stop on its own partial minima; the caller
 // min-reduces the ks partials with shuffles (min is exact and order-free).
-template <int TX>
+template <int TX, int TL = 16 / TX>
 __device__ __forceinline__ void combine_tile_split(const double* Stri, const int* trio, const double* Xs, int L,
                                                    int j, int l0, int xi0, int lA, int lB, int sub, int ks,
-                                                   bool mono, double (&acc)[16 / TX][TX]) {
-    constexpr int TL = 16 / TX;
+                                                   bool mono, double (&acc)[TL][TX]) {
 #pragma unroll
     for (int a = 0; a < TL; ++a)
 #pragma unroll
@@ -983,11 +982,10 @@ __device__ __forceinline__ void combine_tile_split(const double* Stri, const int
     }
 }
 
-template <int TX>
+template <int TX, int TL = 16 / TX>
 __device__ __forceinline__ void combine_tiles_s(double* Wi, int i, int r, int L, int j, const double* Stri,
                                                 const int* trio, const double* Xs, int* hist, int* order,
                                                 int part, int nparts, int lA, int lB, bool atomic, bool mono) {
-    constexpr int TL = 16 / TX;
     const int t = threadIdx.x;
     const int ntl = (L + TL - 1) / TL, ntx = (j + TX - 1) / TX, ntiles = ntl * ntx;
     // the item is split over nparts CTAs: CTA `part` owns the tiles with id = part (mod nparts)
@@ -997,7 +995,7 @@ __device__ __forceinline__ void combine_tiles_s(double* Wi, int i, int r, int L,
     __syncthreads();
     for (int k = t; k < nmine; k += blockDim.x) {
         const int id = part + k * nparts;
-        atomicAdd(&hist[L - tile_nfast<TX>(L, 1 + TL * (id / ntx), 2 + TX * (id % ntx), lA, lB)], 1);
+        atomicAdd(&hist[L - tile_nfast<TX, TL>(L, 1 + TL * (id / ntx), 2 + TX * (id % ntx), lA, lB)], 1);
     }
     __syncthreads();
     if (t < 32) {   // exclusive prefix over the L + 2 bins: one warp, 5 bins per lane
@@ -1016,7 +1014,7 @@ __device__ __forceinline__ void combine_tiles_s(double* Wi, int i, int r, int L,
     __syncthreads();
     for (int k = t; k < nmine; k += blockDim.x) {
         const int id = part + k * nparts;
-        order[atomicAdd(&hist[L - tile_nfast<TX>(L, 1 + TL * (id / ntx), 2 + TX * (id % ntx), lA, lB)], 1)] = id;
+        order[atomicAdd(&hist[L - tile_nfast<TX, TL>(L, 1 + TL * (id / ntx), 2 + TX * (id % ntx), lA, lB)], 1)] = id;
     }
     __syncthreads();
     // few tiles: ks lanes per tile split its l' range (ks a power of two <= 32)
@@ -1029,10 +1027,10 @@ __device__ __forceinline__ void combine_tiles_s(double* Wi, int i, int r, int L,
         const int l0 = 1 + TL * (id / ntx), xi0 = 2 + TX * (id % ntx);
         double acc[TL][TX];
         if (ks == 1) {
-            if (mono) combine_tile_s_desc<TX>(Stri, trio, Xs, L, j, l0, xi0, lA, lB, acc);
-            else combine_tile_s<TX>(Stri, trio, Xs, L, j, l0, xi0, lA, lB, acc);
+            if (mono) combine_tile_s_desc<TX, TL>(Stri, trio, Xs, L, j, l0, xi0, lA, lB, acc);
+            else combine_tile_s<TX, TL>(Stri, trio, Xs, L, j, l0, xi0, lA, lB, acc);
         } else {
-            combine_tile_split<TX>(Stri, trio, Xs, L, j, l0, xi0, lA, lB, sub, ks, mono, acc);
+            combine_tile_split<TX, TL>(Stri, trio, Xs, L, j, l0, xi0, lA, lB, sub, ks, mono, acc);
             const unsigned gmask = (ks == 32 ? 0xffffffffu : ((1u << ks) - 1u)) << (lane & ~(ks - 1));
             for (int off = 1; off < ks; off <<= 1)
 #pragma unroll
@@ -1106,9 +1104,9 @@ __device__ __forceinline__ void combine_item_s(const pp_batch& b, const pp_insta
     __syncthreads();
     const double* S = j > S_DIRECT_J ? Stri : Sg;
     const bool mono = g_combine_early_exit && reinterpret_cast<const int*>(ws + lay.smono)[slot];
-    if (j >= 4) combine_tiles_s<4>(Wi, i, r, L, j, S, trio, Xs, s_hist, s_order, part, nparts, lA, lB, atomic, mono);
-    else if (j >= 2) combine_tiles_s<2>(Wi, i, r, L, j, S, trio, Xs, s_hist, s_order, part, nparts, lA, lB, atomic, mono);
-    else combine_tiles_s<1>(Wi, i, r, L, j, S, trio, Xs, s_hist, s_order, part, nparts, lA, lB, atomic, mono);
+    if (j >= 4) combine_tiles_s<4, COMBINE_TL4>(Wi, i, r, L, j, S, trio, Xs, s_hist, s_order, part, nparts, lA, lB, atomic, mono);
+    else if (j >= 2) combine_tiles_s<2, 4 * COMBINE_TL4 / 2>(Wi, i, r, L, j, S, trio, Xs, s_hist, s_order, part, nparts, lA, lB, atomic, mono);
+    else combine_tiles_s<1, 8 * COMBINE_TL4 / 2>(Wi, i, r, L, j, S, trio, Xs, s_hist, s_order, part, nparts, lA, lB, atomic, mono);
 }
 
 __global__ void __launch_bounds__(256, 2) k_combine_s(pp_batch b, int j) {
@@ -1118,7 +1116,7 @@ __global__ void __launch_bounds__(256, 2) k_combine_s(pp_batch b, int j) {
     __shared__ int s_order[1024];
     combine_item_s(b, I, j, blockIdx.y + 1, blockIdx.z, gridDim.z, cs_smem, s_hist, s_order, false);
 }
-__global__ void __launch_bounds__(256, 2) k_combine_s_p(const pp_batch* __restrict__ bp, int j) {
+__global__ void __launch_bounds__(256, COMBINE_TL4 == 2 ? 3 : 2) k_combine_s_p(const pp_batch* __restrict__ bp, int j) {
     pdl_trigger();
     StepTrace tr;
     tr.begin();
