@@ -424,6 +424,9 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 constexpr int KC = 32;   // K chunk staged per __syncthreads
+#ifndef EXPAND_TRW
+#define EXPAND_TRW 2        // expand register tile 4 xi x 2 r (8 accumulators)
+#endif
 
 // ----------------------------------------------------------------------------
 // k_expand(j), step j of the wavefront, once slice W_j is final:
@@ -724,7 +727,8 @@ __device__ __forceinline__ void expand_row_s(const pp_batch& b, const pp_instanc
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    const int ntx = (j + 3) >> 2, ntr = (nt + 3) >> 2, ntiles = ntx * ntr;
+    constexpr int TRW = EXPAND_TRW;   // target columns per register tile (4 xi x TRW r)
+    const int ntx = (j + 3) >> 2, ntr = (nt + TRW - 1) / TRW, ntiles = ntx * ntr;
     // split-K when the plane has few tiles: ks consecutive lanes share a tile,
     // fold interleaved r' subsets and min-reduce with shuffles
     int ks = 1;
@@ -734,36 +738,39 @@ __device__ __forceinline__ void expand_row_s(const pp_batch& b, const pp_instanc
     double* X = ws + lay.X;
     for (int id = t / ks; id < ntiles; id += blockDim.x / ks) {
         const int tx = id % ntx, tr = id / ntx;
-        const int xi0 = 2 + 4 * tx, r0 = rfirst + 4 * tr;
+        const int xi0 = 2 + 4 * tx, r0 = rfirst + TRW * tr;
         const int kend = j - xi0 + 2;   // W_j(l', xi-1, r') = inf for r' > j - xi + 2
-        double acc[4][4];
+        double acc[4][TRW];
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) acc[a][c] = PP_INF;
+            for (int c = 0; c < TRW; ++c) acc[a][c] = PP_INF;
         // padded columns read in-range garbage-free copies: clamp and mask at the end
         const int xa[4] = {min(xi0 - 1, j) - 1, min(xi0, j) - 1, min(xi0 + 1, j) - 1, min(xi0 + 2, j) - 1};
-        const int ra[4] = {min(r0, nr) - rfirst, min(r0 + 1, nr) - rfirst, min(r0 + 2, nr) - rfirst,
-                           min(r0 + 3, nr) - rfirst};
+        int ra[TRW];
+#pragma unroll
+        for (int c = 0; c < TRW; ++c) ra[c] = min(r0 + c, nr) - rfirst;
         for (int rp = 1 + sub; rp <= kend; rp += ks) {
             const double* Ar = A + (rp - 1) * j;
             const double* Br = B + (rp - 1) * nt;
-            double p[4], q[4];
+            double p[4], q[TRW];
 #pragma unroll
-            for (int a = 0; a < 4; ++a) { p[a] = Ar[xa[a]]; q[a] = Br[ra[a]]; }
+            for (int a = 0; a < 4; ++a) p[a] = Ar[xa[a]];
+#pragma unroll
+            for (int c = 0; c < TRW; ++c) q[c] = Br[ra[c]];
 #pragma unroll
             for (int a = 0; a < 4; ++a)
 #pragma unroll
-                for (int c = 0; c < 4; ++c) acc[a][c] = dmin(acc[a][c], dmax(p[a], q[c]));
+                for (int c = 0; c < TRW; ++c) acc[a][c] = dmin(acc[a][c], dmax(p[a], q[c]));
         }
         for (int off = 1; off < ks; off <<= 1)
 #pragma unroll
             for (int a = 0; a < 4; ++a)
 #pragma unroll
-                for (int c = 0; c < 4; ++c) acc[a][c] = dmin(acc[a][c], __shfl_xor_sync(gmask, acc[a][c], off));
+                for (int c = 0; c < TRW; ++c) acc[a][c] = dmin(acc[a][c], __shfl_xor_sync(gmask, acc[a][c], off));
         if (sub != 0) continue;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < TRW; ++c) {
             const int r = r0 + c;
             if (r > nr) continue;
             double* Xr = X + X_base(L, j + r, r) + (int64_t)(lp - 1) * j;
@@ -783,7 +790,7 @@ __global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
     extern __shared__ __align__(16) double ex_smem[];
     expand_row_s(b, I, j, lp, 1, ex_smem);
 }
-__global__ void __launch_bounds__(128) k_expand_s_p(const pp_batch* __restrict__ bp, int j) {
+__global__ void __launch_bounds__(128, EXPAND_TRW == 2 ? 5 : 4) k_expand_s_p(const pp_batch* __restrict__ bp, int j) {
     pdl_trigger();
     StepTrace tr;
     tr.begin();
