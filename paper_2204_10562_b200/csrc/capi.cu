@@ -273,7 +273,13 @@ static int prm_inst(const pp_batch* b, void* stream) {
     if (maxV > 1) {
         // smallest chunk: one expand row at j = V-1 or one combine item at j = V-1
         const int need = std::max((maxV - 1) * maxV, (maxL - 1) * maxL / 2 + std::max(maxL - 1, 0) * (maxV - 1));
-        const int sd = std::min(27000, std::max(need, 12000));
+        // enough for a whole step's rows / items when that is small (C4: ~8 K doubles,
+        // 3 CTAs per SM), else ~12 K doubles with chunking
+        int full = 0;
+        for (int j = 1; j < maxV; ++j)
+            full = std::max(full, std::max((maxL - 1) * j * maxV,
+                                           (maxV - j) * ((maxL - 1) * maxL / 2 + (maxL - 1) * j)));
+        const int sd = std::min(27000, std::max(need, std::min(full, 12000)));
         if (need > 27000) return fail(PP_EINVAL, "k_dp_inst: L=%d V=%d exceed shared memory", maxL, maxV);
         const size_t smem = sizeof(double) * (size_t)sd;
         cudaFuncSetAttribute(k_dp_inst, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

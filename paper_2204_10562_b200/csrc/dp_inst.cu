@@ -52,7 +52,7 @@ __device__ __forceinline__ void dp_inst_combine(const pp_batch& b, const pp_inst
     }
 }
 
-__global__ void __launch_bounds__(DI_T, 2) k_dp_inst(pp_batch b, int smem_doubles) {
+__global__ void __launch_bounds__(DI_T, 3) k_dp_inst(pp_batch b, int smem_doubles) {
     const pp_instance I = b.inst[blockIdx.x];
     const int L = I.L, V = I.V, M = I.M;
     if (L > SR_MAX || V > SR_MAX) return;
@@ -167,9 +167,9 @@ __global__ void __launch_bounds__(DI_T, 2) k_dp_inst(pp_batch b, int smem_double
             cp_async_commit();
             cp_async_wait<0>();
             __syncthreads();
-            if (j >= 4) dp_inst_combine<4>(b, I, j, ra, rb, di_smem, trio);
-            else if (j >= 2) dp_inst_combine<2>(b, I, j, ra, rb, di_smem, trio);
-            else dp_inst_combine<1>(b, I, j, ra, rb, di_smem, trio);
+            if (j >= 4) dp_inst_combine<4, 2>(b, I, j, ra, rb, di_smem, trio);
+            else if (j >= 2) dp_inst_combine<2, 4>(b, I, j, ra, rb, di_smem, trio);
+            else dp_inst_combine<1, 8>(b, I, j, ra, rb, di_smem, trio);
             __syncthreads();
         }
     }
