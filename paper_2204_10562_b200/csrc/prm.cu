@@ -220,7 +220,7 @@ __device__ __forceinline__ void base_body(const pp_batch& b, int full_rows) {
             }
         }
     }
-    if (y >= 1 && y < L) {
+    if (full_rows && y >= 1 && y < L) {   // T1 feeds the chunked path's S tables only
         const int lp = y, w = L - lp;
         double* T1 = ws + lay.T1;
         for (int e = t; e < (V - 1) * w; e += blockDim.x) {
@@ -285,71 +285,58 @@ __global__ void __launch_bounds__(128) k_sdedup_p(const pp_batch* __restrict__ b
     sdedup_body(b);
 }
 
-__device__ __forceinline__ void stab_fill(const pp_batch& b, const pp_instance& I, int r, int i) {
-    const int L = I.L, V = I.V;
+// One warp fills the triangle of item (r, i) if it is the canonical item of its
+// slot (the first i with that slot):
+//   S(l', l) = (M * span(l'+1, l)) / r (+ ((2 (r-1)) * P(l'+1..l)) / (r * minpair))
+// (partition.py:127-129, cost.py:99; the same expression as k_base's T1 + sync).
+__device__ __forceinline__ void stab_fill_warp(const pp_batch& b, const pp_instance& I, int r, int i) {
+    const int L = I.L, V = I.V, M = I.M;
     const WsLayout lay = ws_layout(L, V);
     double* ws = b.ws + I.ws_off;
     const int* sidx = reinterpret_cast<const int*>(ws + lay.sidx);
+    const int lane = threadIdx.x & 31;
     const int slot = sidx[(r - 1) * V + (i - 1)];
-    // only the canonical item of its slot (the first i with this slot) fills it
-    for (int q = r + 1; q < i; ++q)
-        if (sidx[(r - 1) * V + (q - 1)] == slot) return;
+    bool dup = false;
+    for (int q = r + 1 + lane; q < i; q += 32) dup |= sidx[(r - 1) * V + (q - 1)] == slot;
+    if (__any_sync(0xffffffffu, dup)) return;
     const int64_t tri = (int64_t)(L - 1) * L / 2;
     double* out = ws + lay.Stab + (int64_t)slot * tri;
-    const double* T1 = ws + lay.T1;
+    const double* prefix = ws + lay.prefix;
     const double* psum = ws + lay.psum;
     const double den = (double)r * ws[lay.minpair + (int64_t)(i - r) * V + (i - 1)];
     const uint64_t pol = l2_evict_last_policy();   // re-read by the combine of every step
     const double num = 2.0 * (double)(r - 1);
-    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, nw = blockDim.x >> 5;
-    int off = 0;
     for (int lp = 1; lp < L; ++lp) {
-        if ((lp - 1) % nw == warp) {
-            const double* t1 = T1 + stage_idx(L, r, lp, 1);
-            const double* ps = psum + (int64_t)lp * L;
-            double a[4], p[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int l = lp + 1 + lane + 32 * u;
-                a[u] = (l <= L) ? t1[l - 1] : 0.0;
-                p[u] = (l <= L && r > 1) ? ps[l - 1] : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int l = lp + 1 + lane + 32 * u;
-                if (l > L) continue;
-                double sv = a[u];
-                if (r > 1) sv += num * p[u] / den;   // partition.py:128-129, cost.py:99
-                st_evict_last(out + off + (l - lp - 1), sv, pol);
-            }
+        const int off = (lp - 1) * L - (lp - 1) * lp / 2;
+        const double pl = prefix[lp];
+        for (int l = lp + 1 + lane; l <= L; l += 32) {
+            double sv = (double)M * (prefix[l] - pl) / (double)r;
+            if (r > 1) sv += num * psum[(int64_t)lp * L + (l - 1)] / den;
+            st_evict_last(out + off + (l - lp - 1), sv, pol);
         }
-        off += L - lp;
     }
+    __syncwarp();
     // Is the triangle non-increasing in l' (S(l', l) >= S(l'+1, l) for every l)?
     // In exact arithmetic it is (span and parameter sums shrink as the stage
     // loses layers); the flag certifies it for these rounded values, and only a
     // certified triangle lets the combine stop scanning l' early.
-    __syncthreads();
-    __shared__ int s_bad;
-    if (t == 0) s_bad = 0;
-    __syncthreads();
-    int bad = 0;
-    for (int lp = 1 + warp; lp + 1 < L; lp += nw) {
+    bool bad = false;
+    for (int lp = 1; lp + 1 < L; ++lp) {
         const int o0 = (lp - 1) * L - (lp - 1) * lp / 2, o1 = lp * L - lp * (lp + 1) / 2;
         for (int l = lp + 2 + lane; l <= L; l += 32)
             bad |= !(out[o0 + (l - lp - 1)] >= out[o1 + (l - lp - 2)]);
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&s_bad, 1);
-    __syncthreads();
-    if (t == 0) reinterpret_cast<int*>(ws + lay.smono)[slot] = !s_bad;
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) reinterpret_cast<int*>(ws + lay.smono)[slot] = !bad;
 }
 
-// grid (n_inst, maxV - 1): CTA (instance, r) fills the canonical slots of width r
+// grid (n_inst, maxV - 1): CTA (instance, r); its warps take i = r+1.. round robin
 __device__ __forceinline__ void stab_body(const pp_batch& b) {
     const pp_instance I = b.inst[blockIdx.x];
     const int r = blockIdx.y + 1;
     if (I.L > SR_MAX || I.V > SR_MAX || r >= I.V) return;
-    for (int i = r + 1; i <= I.V; ++i) stab_fill(b, I, r, i);
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int i = r + 1 + warp; i <= I.V; i += nw) stab_fill_warp(b, I, r, i);
 }
 __global__ void __launch_bounds__(128) k_stab(pp_batch b) { stab_body(b); }
 __global__ void __launch_bounds__(128) k_stab_p(const pp_batch* __restrict__ bp) {
