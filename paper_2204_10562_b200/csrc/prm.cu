@@ -712,6 +712,8 @@ __device__ __forceinline__ void expand_row_s(const pp_batch& b, const pp_instanc
             else A[e] = PP_INF;
         }
     cp_async_commit();
+    __shared__ int64_t s_xb[SR_MAX];   // X_base of target r (the int64 index math once per CTA)
+    for (int q = t; q < nt; q += blockDim.x) s_xb[q] = X_base(L, j + rfirst + q, rfirst + q);
     cp_async_wait<0>();
     __syncthreads();
     constexpr int TRW = EXPAND_TRW;   // target columns per register tile (4 xi x TRW r)
@@ -760,7 +762,7 @@ __device__ __forceinline__ void expand_row_s(const pp_batch& b, const pp_instanc
         for (int c = 0; c < TRW; ++c) {
             const int r = r0 + c;
             if (r > nr) continue;
-            double* Xr = X + X_base(L, j + r, r) + (int64_t)(lp - 1) * j;
+            double* Xr = X + s_xb[r - rfirst] + (int64_t)(lp - 1) * j;
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
                 const int xi = xi0 + a;
