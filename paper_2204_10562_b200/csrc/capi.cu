@@ -39,6 +39,8 @@ template <bool SMEM> __global__ void k_rdo_cut(pp_batch b);
 template <bool SMEM>
 __global__ void k_min_cut(pp_batch b, int k, const int* verts, int n, unsigned char* in_a, double* weight);
 __global__ void k_pe_sweep(pp_batch b);
+__global__ void k_pe_sweep_w(pp_batch b);
+__global__ void k_replay_w(pp_batch b);
 __global__ void k_select(pp_batch b);
 __global__ void k_replay(pp_batch b);
 __global__ void k_sim_plans(pp_batch b, pp_sim_batch s);
@@ -626,9 +628,14 @@ static int sim_block(int maxN) {
 
 int pp_pe_sweep(const pp_batch* b, void* stream) {
     if (b->n_inst <= 0) return PP_OK;
+    dim3 g(b->n_inst, b->max_V);
+    if (b->max_V <= PE_WARP_MAXN) {   // one warp per plan: registers + shuffles per pass
+        k_pe_sweep_w<<<g, 32, 0, S(stream)>>>(*b);
+        PP_CHECK_LAUNCH("k_pe_sweep");
+        return PP_OK;
+    }
     const size_t smem = sim_smem(b->max_V);
     cudaFuncSetAttribute(k_pe_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 g(b->n_inst, b->max_V);
     k_pe_sweep<<<g, sim_block(b->max_V), smem, S(stream)>>>(*b);
     PP_CHECK_LAUNCH("k_pe_sweep");
     return PP_OK;
@@ -639,9 +646,13 @@ int pp_select(const pp_batch* b, void* stream) {
     k_select<<<b->n_inst, 32, 0, S(stream)>>>(*b);
     PP_CHECK_LAUNCH("k_select");
     if (b->ev_start) {
-        const size_t smem = sim_smem(b->max_V);
-        cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_replay<<<b->n_inst, sim_block(b->max_V), smem, S(stream)>>>(*b);
+        if (b->max_V <= PE_WARP_MAXN) {
+            k_replay_w<<<b->n_inst, 32, 0, S(stream)>>>(*b);
+        } else {
+            const size_t smem = sim_smem(b->max_V);
+            cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_replay<<<b->n_inst, sim_block(b->max_V), smem, S(stream)>>>(*b);
+        }
         PP_CHECK_LAUNCH("k_replay");
     }
     return PP_OK;

@@ -24,10 +24,26 @@ namespace pp {
 // ---- plan views -------------------------------------------------------------
 struct SppPlanView {   // xi-stage plan written by k_backtrack: device ranks are order slices
     const int *ls, *le, *dlo, *dhi, *order;
+    const double *minpair = nullptr, *cross = nullptr;   // k_prep's slice tables (optional)
+    int V = 0;
     __device__ int stage_ls(int n) const { return ls[n - 1]; }
     __device__ int stage_le(int n) const { return le[n - 1]; }
     __device__ int k(int n) const { return dhi[n - 1] - dlo[n - 1] + 1; }
     __device__ int dev(int n, int a) const { return order[dlo[n - 1] - 1 + a]; }
+    // min pairwise bandwidth of stage n's slice / min cross bandwidth between the
+    // slices of stages n and n+1 (cost.py:64-80): the exact minima k_prep tabulated
+    // over the same device sets (min is order-free, so the bits are the loop's);
+    // returns false when the tables are absent
+    __device__ bool table_min_pair(int n, double& mp) const {
+        if (!minpair) return false;
+        mp = minpair[(int64_t)(dlo[n - 1] - 1) * V + (dhi[n - 1] - 1)];
+        return true;
+    }
+    __device__ bool table_min_cross(int n, double& mc) const {
+        if (!cross) return false;
+        mc = cross[cross_idx(V, dhi[n], dhi[n] - dlo[n] + 1, dhi[n - 1] - dlo[n - 1] + 1)];
+        return true;
+    }
 };
 
 struct ExplicitPlanView {   // caller plan (pp_sim_batch)
@@ -36,6 +52,8 @@ struct ExplicitPlanView {   // caller plan (pp_sim_batch)
     __device__ int stage_le(int n) const { return le[n - 1]; }
     __device__ int k(int n) const { return doff[n] - doff[n - 1]; }
     __device__ int dev(int n, int a) const { return devs[doff[n - 1] + a]; }
+    __device__ bool table_min_pair(int, double&) const { return false; }   // arbitrary device sets
+    __device__ bool table_min_cross(int, double&) const { return false; }
 };
 
 struct InstView {
@@ -77,8 +95,9 @@ __device__ LaneCost lane_cost(const P& p, const InstView& I, int N, int lane) {
         if (k >= 2) {
             const double total = pysum(I.par + a - 1, e - a + 1, I.naive);
             double mp = PP_INF;
-            for (int x = 0; x < k; ++x)
-                for (int y = x + 1; y < k; ++y) mp = dmin(mp, I.w(p.dev(n, x), p.dev(n, y)));
+            if (!p.table_min_pair(n, mp))
+                for (int x = 0; x < k; ++x)
+                    for (int y = x + 1; y < k; ++y) mp = dmin(mp, I.w(p.dev(n, x), p.dev(n, y)));
             c.ar = 2.0 * (double)(k - 1) * total / ((double)k * mp);              // cost.py:99
             c.has_ar = true;
             c.mbw = mp;
@@ -86,8 +105,9 @@ __device__ LaneCost lane_cost(const P& p, const InstView& I, int N, int lane) {
     } else {
         const int kl = p.k(n), kr = p.k(n + 1);
         double mc = PP_INF;
-        for (int x = 0; x < kl; ++x)
-            for (int y = 0; y < kr; ++y) mc = dmin(mc, I.w(p.dev(n, x), p.dev(n + 1, y)));   // cost.py:74-80
+        if (!p.table_min_cross(n, mc))
+            for (int x = 0; x < kl; ++x)
+                for (int y = 0; y < kr; ++y) mc = dmin(mc, I.w(p.dev(n, x), p.dev(n + 1, y)));   // cost.py:74-80
         const double denom = (double)(kl * kr) * mc;                              // cost.py:121-122
         const int edge = p.stage_le(n);
         c.dA = I.efwd[edge - 1] / denom;
@@ -194,6 +214,141 @@ __device__ void pe_simulate(const P& p, const InstView& I, int N, int M, int nth
         for (int w = 0; w < nthr / 32; ++w) mk = dmax(mk, red[w]);
         *o_mk = mk;
     }
+}
+
+// ---- PE sweep, one WARP per plan (R = 2N-1 <= 32 S resources) ---------------
+// Lane L holds resources q = L*S + s (contiguous blocks): a predecessor on the
+// neighbouring resource is in the same lane's registers or one shuffle away, so
+// a pass is register work plus two shuffles instead of a shared-memory round
+// trip and a CTA barrier.  Same recurrence, same fp64 operations in the same
+// order per resource as pe_simulate (bit-identical).
+template <int S, class P>
+__device__ void pe_simulate_warp(const P& p, const InstView& I, int N, int M, double* o_mk, double* o_bound,
+                                 double* ev_s, double* ev_e, double* ar_s, double* ar_e) {
+    const unsigned FULL = 0xffffffffu;
+    const int R = 2 * N - 1, J = 4 * N - 3;
+    const int lane = threadIdx.x & 31;
+    double dA[S], dB[S], ar[S], fe[S], be[S], rf[S];
+    bool has_ar[S], act[S], from_left[S];
+    int p1[S], p2[S];
+    double cy = -PP_INF, am = -PP_INF;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int q = lane * S + s;
+        act[s] = q < R;
+        LaneCost c{0.0, 0.0, 0.0, 0.0, false, 0.0, 0.0, PP_INF};
+        if (act[s]) c = lane_cost(p, I, N, q);
+        dA[s] = c.dA; dB[s] = c.dB; ar[s] = c.ar; has_ar[s] = act[s] && c.has_ar;
+        if (act[s]) cy = dmax(cy, c.cyc);
+        if (has_ar[s]) am = dmax(am, c.ar);
+        const bool st = (q & 1) == 0;
+        const int n = q / 2 + 1;
+        if (st) {
+            if (n < N) { p1[s] = 4 * N - 1 - 2 * n; p2[s] = 2 * n - 1; }   // B_n, F_n
+            else { p1[s] = 2 * N - 1; p2[s] = 0; }                       // FB_N
+        } else { p1[s] = 4 * N - 2 - 2 * n; p2[s] = 2 * n; }              // Y_n, X_n
+        from_left[s] = st && n == N;
+        fe[s] = 0.0; be[s] = 0.0; rf[s] = 0.0;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        cy = dmax(cy, __shfl_xor_sync(FULL, cy, off));
+        am = dmax(am, __shfl_xor_sync(FULL, am, off));
+    }
+    if (lane == 0) *o_bound = (double)(M + 4 * N - 4) * cy + (am == -PP_INF ? 0.0 : am);   // scheduler.py:238
+    const int P_total = M + J - 1;
+    for (int pass = 1; pass <= P_total; ++pass) {
+        // neighbours' pass-1 ends: left fe of q-1, right be of q+1
+        const double fe_in = __shfl_up_sync(FULL, fe[S - 1], 1);
+        const double be_in = __shfl_down_sync(FULL, be[0], 1);
+        double fn[S], bn[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            fn[s] = fe[s]; bn[s] = be[s];
+            if (!act[s]) continue;
+            const int q = lane * S + s;
+            const double left = q == 0 ? 0.0 : (s > 0 ? fe[s - 1] : fe_in);
+            const double right = q + 1 >= R ? 0.0 : (s + 1 < S ? be[s + 1] : be_in);
+            int m = pass - p1[s] + 1;
+            if (m >= 1 && m <= M) {
+                const double st = dmax(rf[s], from_left[s] ? left : right);
+                const double en = st + dB[s];   // B / FB / Y
+                rf[s] = en;
+                bn[s] = en;
+                if (ev_s) { const int64_t x = (int64_t)(m - 1) * J + p1[s] - 1; ev_s[x] = st; ev_e[x] = en; }
+            }
+            if (p2[s]) {
+                m = pass - p2[s] + 1;
+                if (m >= 1 && m <= M) {
+                    const double st = dmax(rf[s], left);
+                    const double en = st + dA[s];   // F / X
+                    rf[s] = en;
+                    fn[s] = en;
+                    if (ev_s) { const int64_t x = (int64_t)(m - 1) * J + p2[s] - 1; ev_s[x] = st; ev_e[x] = en; }
+                }
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) { fe[s] = fn[s]; be[s] = bn[s]; }
+    }
+    // AllReduce windows start at the stage's last compute end (scheduler.py:195-198);
+    // makespan = max(last B_1 / FB_1 end, AllReduce ends)   (scheduler.py:216-220)
+    double arend = -PP_INF;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int q = lane * S + s;
+        if (act[s] && (q & 1) == 0 && has_ar[s]) {
+            const double e = rf[s] + ar[s];
+            arend = dmax(arend, e);
+            if (ar_s) { ar_s[q / 2] = rf[s]; ar_e[q / 2] = e; }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) arend = dmax(arend, __shfl_xor_sync(FULL, arend, off));
+    if (lane == 0) *o_mk = dmax(rf[0], arend);
+}
+
+template <class P>
+__device__ void pe_simulate_warp_any(const P& p, const InstView& I, int N, int M, double* o_mk, double* o_bound,
+                                     double* ev_s, double* ev_e, double* ar_s, double* ar_e) {
+    const int R = 2 * N - 1;
+    if (R <= 32) pe_simulate_warp<1>(p, I, N, M, o_mk, o_bound, ev_s, ev_e, ar_s, ar_e);
+    else if (R <= 64) pe_simulate_warp<2>(p, I, N, M, o_mk, o_bound, ev_s, ev_e, ar_s, ar_e);
+    else if (R <= 96) pe_simulate_warp<3>(p, I, N, M, o_mk, o_bound, ev_s, ev_e, ar_s, ar_e);
+    else pe_simulate_warp<4>(p, I, N, M, o_mk, o_bound, ev_s, ev_e, ar_s, ar_e);
+}
+
+// k_pe_sweep / k_replay with one warp per plan (every N of the batch <= PE_WARP_MAXN)
+constexpr int PE_WARP_MAXN = 64;
+__global__ void __launch_bounds__(32) k_pe_sweep_w(pp_batch b) {
+    const pp_instance I = b.inst[blockIdx.x];
+    const int xi = blockIdx.y + 1;
+    if (xi > I.V) return;
+    const int64_t so = I.sweep_off + xi - 1;
+    if (b.sweep_r[so] == 0) {   // infeasible: SweepEntry(makespan=None, bound=None)
+        if (threadIdx.x == 0) { b.sweep_mk[so] = PP_INF; b.sweep_bound[so] = PP_INF; }
+        return;
+    }
+    const int64_t st = I.stage_off + (int64_t)xi * (xi - 1) / 2;
+    SppPlanView p{b.stage_ls + st, b.stage_le + st, b.stage_dlo + st, b.stage_dhi + st, b.order + I.order_off};
+    const WsLayout lay = ws_layout(I.L, I.V);
+    p.minpair = b.ws + I.ws_off + lay.minpair; p.cross = b.ws + I.ws_off + lay.cross; p.V = I.V;
+    InstView iv(b, I);
+    pe_simulate_warp_any(p, iv, xi, I.M, b.sweep_mk + so, b.sweep_bound + so, nullptr, nullptr, nullptr, nullptr);
+}
+
+__global__ void __launch_bounds__(32) k_replay_w(pp_batch b) {
+    const pp_instance I = b.inst[blockIdx.x];
+    const int xi = b.best_xi[blockIdx.x];
+    if (xi <= 0) return;
+    __shared__ double s_mk, s_bd;
+    const int64_t st = I.stage_off + (int64_t)xi * (xi - 1) / 2;
+    SppPlanView p{b.stage_ls + st, b.stage_le + st, b.stage_dlo + st, b.stage_dhi + st, b.order + I.order_off};
+    const WsLayout lay = ws_layout(I.L, I.V);
+    p.minpair = b.ws + I.ws_off + lay.minpair; p.cross = b.ws + I.ws_off + lay.cross; p.V = I.V;
+    InstView iv(b, I);
+    pe_simulate_warp_any(p, iv, xi, I.M, &s_mk, &s_bd, b.ev_start + I.ev_off, b.ev_end + I.ev_off,
+                         b.ar_start + I.ar_off, b.ar_end + I.ar_off);
 }
 
 __host__ __device__ inline int sim_threads(int N) {
