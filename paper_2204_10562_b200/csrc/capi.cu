@@ -15,6 +15,8 @@ __global__ void k_prep_p(const pp_batch* bp);
 __global__ void k_base_p(const pp_batch* bp, int full_rows);
 __global__ void k_sdedup_p(const pp_batch* bp);
 __global__ void k_stab_p(const pp_batch* bp);
+__global__ void k_stab_big_p(const pp_batch* bp);
+__global__ void k_stab_big(pp_batch b);
 __global__ void k_expand_s_p(const pp_batch* bp, int j);
 __global__ void k_combine_s_p(const pp_batch* bp, int j);
 __global__ void k_backtrack_p(const pp_batch* bp);
@@ -495,7 +497,8 @@ static int prm_prep(const pp_batch* b, void* stream) {
         PP_CHECK_LAUNCH("k_sdedup");
         if (maxV > 1 && maxL > 1) {
             dim3 gs(b->n_inst, maxV - 1);
-            k_stab<<<gs, 128, 0, S(stream)>>>(*b);
+            if ((maxL - 1) * maxL / 2 >= STAB_BIG) k_stab_big<<<gs, 128, 0, S(stream)>>>(*b);
+            else k_stab<<<gs, 128, 0, S(stream)>>>(*b);
             PP_CHECK_LAUNCH("k_stab");
         }
     }
@@ -515,7 +518,8 @@ static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int 
     PP_CHECK_LAUNCH("k_sdedup");
     if (maxV > 1 && maxL > 1) {
         dim3 gs(b->n_inst, maxV - 1);
-        k_stab_p<<<gs, 128, 0, S(stream)>>>(db);
+        if ((maxL - 1) * maxL / 2 >= STAB_BIG) k_stab_big_p<<<gs, 128, 0, S(stream)>>>(db);
+        else k_stab_p<<<gs, 128, 0, S(stream)>>>(db);
         PP_CHECK_LAUNCH("k_stab");
     }
     const size_t ex_smem = sizeof(double) * (size_t)maxV * maxV;

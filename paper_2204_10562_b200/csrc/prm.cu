@@ -285,20 +285,18 @@ __global__ void __launch_bounds__(128) k_sdedup_p(const pp_batch* __restrict__ b
     sdedup_body(b);
 }
 
-// One warp fills the triangle of item (r, i) if it is the canonical item of its
-// slot (the first i with that slot):
+// Triangle of the canonical item (r, i) of its slot:
 //   S(l', l) = (M * span(l'+1, l)) / r (+ ((2 (r-1)) * P(l'+1..l)) / (r * minpair))
-// (partition.py:127-129, cost.py:99; the same expression as k_base's T1 + sync).
-__device__ __forceinline__ void stab_fill_warp(const pp_batch& b, const pp_instance& I, int r, int i) {
+// (partition.py:127-129, cost.py:99; the same expression as k_base's T1 + sync),
+// filled by `nw` warps starting at warp w0 (one warp for small triangles, the
+// whole CTA for large ones), plus its monotonicity flag.
+__device__ __forceinline__ void stab_fill(const pp_batch& b, const pp_instance& I, int r, int i, int w0, int nw,
+                                          int* s_bad) {
     const int L = I.L, V = I.V, M = I.M;
     const WsLayout lay = ws_layout(L, V);
     double* ws = b.ws + I.ws_off;
-    const int* sidx = reinterpret_cast<const int*>(ws + lay.sidx);
-    const int lane = threadIdx.x & 31;
-    const int slot = sidx[(r - 1) * V + (i - 1)];
-    bool dup = false;
-    for (int q = r + 1 + lane; q < i; q += 32) dup |= sidx[(r - 1) * V + (q - 1)] == slot;
-    if (__any_sync(0xffffffffu, dup)) return;
+    const int slot = reinterpret_cast<const int*>(ws + lay.sidx)[(r - 1) * V + (i - 1)];
+    const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) - w0;
     const int64_t tri = (int64_t)(L - 1) * L / 2;
     double* out = ws + lay.Stab + (int64_t)slot * tri;
     const double* prefix = ws + lay.prefix;
@@ -306,7 +304,7 @@ __device__ __forceinline__ void stab_fill_warp(const pp_batch& b, const pp_insta
     const double den = (double)r * ws[lay.minpair + (int64_t)(i - r) * V + (i - 1)];
     const uint64_t pol = l2_evict_last_policy();   // re-read by the combine of every step
     const double num = 2.0 * (double)(r - 1);
-    for (int lp = 1; lp < L; ++lp) {
+    for (int lp = 1 + warp; lp < L; lp += nw) {
         const int off = (lp - 1) * L - (lp - 1) * lp / 2;
         const double pl = prefix[lp];
         for (int l = lp + 1 + lane; l <= L; l += 32) {
@@ -315,33 +313,72 @@ __device__ __forceinline__ void stab_fill_warp(const pp_batch& b, const pp_insta
             st_evict_last(out + off + (l - lp - 1), sv, pol);
         }
     }
-    __syncwarp();
     // Is the triangle non-increasing in l' (S(l', l) >= S(l'+1, l) for every l)?
     // In exact arithmetic it is (span and parameter sums shrink as the stage
     // loses layers); the flag certifies it for these rounded values, and only a
     // certified triangle lets the combine stop scanning l' early.
+    if (nw == 1) __syncwarp();
+    else __syncthreads();
     bool bad = false;
-    for (int lp = 1; lp + 1 < L; ++lp) {
+    for (int lp = 1 + warp; lp + 1 < L; lp += nw) {
         const int o0 = (lp - 1) * L - (lp - 1) * lp / 2, o1 = lp * L - lp * (lp + 1) / 2;
         for (int l = lp + 2 + lane; l <= L; l += 32)
             bad |= !(out[o0 + (l - lp - 1)] >= out[o1 + (l - lp - 2)]);
     }
     bad = __any_sync(0xffffffffu, bad);
-    if (lane == 0) reinterpret_cast<int*>(ws + lay.smono)[slot] = !bad;
+    if (nw == 1) {
+        if (lane == 0) reinterpret_cast<int*>(ws + lay.smono)[slot] = !bad;
+        return;
+    }
+    if (lane == 0 && bad) atomicOr(s_bad, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) { reinterpret_cast<int*>(ws + lay.smono)[slot] = !*s_bad; *s_bad = 0; }
+    __syncthreads();
 }
 
-// grid (n_inst, maxV - 1): CTA (instance, r); its warps take i = r+1.. round robin
+// grid (n_inst, maxV - 1): CTA (instance, r).  The warps take i = r+1.. round
+// robin and skip non-canonical items (a slot is filled by its first i).  SMALL
+// triangles (C4: 496 entries, every item canonical): the warp fills its item at
+// once.  BIG ones (C3: 4560 entries, ~2 canonical items per r): the canonical
+// items are collected and each is filled by the whole CTA.
+template <bool BIG>
 __device__ __forceinline__ void stab_body(const pp_batch& b) {
     const pp_instance I = b.inst[blockIdx.x];
     const int r = blockIdx.y + 1;
-    if (I.L > SR_MAX || I.V > SR_MAX || r >= I.V) return;
-    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int i = r + 1 + warp; i <= I.V; i += nw) stab_fill_warp(b, I, r, i);
+    const int L = I.L, V = I.V;
+    if (L > SR_MAX || V > SR_MAX || r >= V) return;
+    __shared__ int s_can[SR_MAX];
+    __shared__ int s_nc, s_bad;
+    const int* sidx = reinterpret_cast<const int*>(b.ws + I.ws_off + ws_layout(L, V).sidx);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (BIG) {
+        if (threadIdx.x == 0) { s_nc = 0; s_bad = 0; }
+        __syncthreads();
+    }
+    for (int i = r + 1 + warp; i <= V; i += nw) {
+        const int slot = sidx[(r - 1) * V + (i - 1)];
+        bool dup = false;
+        for (int q = r + 1 + lane; q < i; q += 32) dup |= sidx[(r - 1) * V + (q - 1)] == slot;
+        if (__any_sync(0xffffffffu, dup)) continue;
+        if (!BIG) stab_fill(b, I, r, i, warp, 1, &s_bad);
+        else if (lane == 0) s_can[atomicAdd(&s_nc, 1)] = i;
+    }
+    if (!BIG) return;
+    __syncthreads();
+    const int nc = s_nc;
+    for (int c = 0; c < nc; ++c) stab_fill(b, I, r, s_can[c], 0, nw, &s_bad);
 }
-__global__ void __launch_bounds__(128) k_stab(pp_batch b) { stab_body(b); }
+// big triangles: (maxL - 1) maxL / 2 >= STAB_BIG
+constexpr int STAB_BIG = 1024;
+__global__ void __launch_bounds__(128) k_stab(pp_batch b) { stab_body<false>(b); }
+__global__ void __launch_bounds__(128) k_stab_big(pp_batch b) { stab_body<true>(b); }
 __global__ void __launch_bounds__(128) k_stab_p(const pp_batch* __restrict__ bp) {
     const pp_batch b = *bp;
-    stab_body(b);
+    stab_body<false>(b);
+}
+__global__ void __launch_bounds__(128) k_stab_big_p(const pp_batch* __restrict__ bp) {
+    const pp_batch b = *bp;
+    stab_body<true>(b);
 }
 
 // Debug timeline of the per-step kernels (tools/step_trace.py): one record of
