@@ -493,7 +493,7 @@ static int prm_prep(const pp_batch* b, void* stream) {
     k_base<<<gbase, 128, 0, S(stream)>>>(*b, !(maxL <= SR_MAX && maxV <= SR_MAX));
     PP_CHECK_LAUNCH("k_base");
     if (maxL <= SR_MAX && maxV <= SR_MAX) {
-        k_sdedup<<<b->n_inst, 128, 0, S(stream)>>>(*b);
+        k_sdedup<<<dim3(b->n_inst, (maxV - 1 + 7) / 8 > 0 ? (maxV - 1 + 7) / 8 : 1), 256, 0, S(stream)>>>(*b);
         PP_CHECK_LAUNCH("k_sdedup");
         if (maxV > 1 && maxL > 1) {
             dim3 gs(b->n_inst, maxV - 1);
@@ -514,7 +514,7 @@ static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int 
     PP_CHECK_LAUNCH("k_prep");
     k_base_p<<<gp, 128, 0, S(stream)>>>(db, 0);
     PP_CHECK_LAUNCH("k_base");
-    k_sdedup_p<<<b->n_inst, 128, 0, S(stream)>>>(db);
+    k_sdedup_p<<<dim3(b->n_inst, (maxV - 1 + 7) / 8 > 0 ? (maxV - 1 + 7) / 8 : 1), 256, 0, S(stream)>>>(db);
     PP_CHECK_LAUNCH("k_sdedup");
     if (maxV > 1 && maxL > 1) {
         dim3 gs(b->n_inst, maxV - 1);

@@ -239,48 +239,41 @@ __global__ void __launch_bounds__(128) k_base_p(const pp_batch* __restrict__ bp,
 // Stage-term tables for the shared-memory path.  S(l', l, r, i) depends on the
 // item (r, i) only through r and mp = minpair(i-r+1, i) (cost.py:99), so items
 // whose last-stage slices have bitwise-equal min-pair bandwidth share one
-// table.  k_sdedup: one thread per r assigns every (r, i) the slot of the
-// first i' with the same mp (sidx), slots numbered densely per instance.
-// k_stab: one CTA per canonical item fills its packed triangle
-//   row l' (1..L-1): S(l', l) = T1[r][l'][l] (+ sync if r > 1), l = l'+1..L.
+// table.  k_sdedup: one warp per r assigns every (r, i) the slot of the
+// first i' with the same mp (sidx; the slot id is that item's triangular index).
+// k_stab: the canonical items' packed triangles
+//   row l' (1..L-1): S(l', l) = T1(r, l', l) (+ sync if r > 1), l = l'+1..L.
 // ----------------------------------------------------------------------------
 __device__ __forceinline__ void sdedup_body(const pp_batch& b) {
+    // grid (n_inst, ceil((V-1)/8)), 8 warps: warp w owns width r = 8*y + w + 1.
+    // Items (r, i) whose last-stage slices have bitwise-equal min-pair bandwidth
+    // share a slot; the slot id is the triangular index of the FIRST such i
+    // (sparse ids inside the V(V-1)/2 slot budget, so no cross-r prefix).
     const pp_instance I = b.inst[blockIdx.x];
     const int L = I.L, V = I.V;
     if (L > SR_MAX || V > SR_MAX) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r = (int)blockIdx.y * (blockDim.x >> 5) + warp + 1;
+    if (r >= V) return;
     const WsLayout lay = ws_layout(L, V);
     double* ws = b.ws + I.ws_off;
     const double* minpair = ws + lay.minpair;
     int* sidx = reinterpret_cast<int*>(ws + lay.sidx);
-    __shared__ int s_cnt[SR_MAX + 1];
-    const int t = threadIdx.x;
-    for (int r = 1 + t; r < V; r += blockDim.x) {   // pass 1: distinct mp values per r
-        int nd = 0;
-        for (int i = r + 1; i <= V; ++i) {
-            const double m = minpair[(int64_t)(i - r) * V + (i - 1)];
-            int first = i;
-            for (int q = r + 1; q < i; ++q)
-                if (minpair[(int64_t)(q - r) * V + (q - 1)] == m) { first = q; break; }
-            sidx[(r - 1) * V + (i - 1)] = (first == i) ? nd++ : -(first);   // provisional
-        }
-        s_cnt[r] = nd;
-    }
-    __syncthreads();
-    if (t == 0) {
-        int o = 0;
-        for (int r = 1; r < V; ++r) { const int c = s_cnt[r]; s_cnt[r] = o; o += c; }
-    }
-    __syncthreads();
-    for (int r = 1 + t; r < V; r += blockDim.x) {   // pass 2: global slot ids
-        const int base = s_cnt[r];
-        for (int i = r + 1; i <= V; ++i) {
-            int* e = &sidx[(r - 1) * V + (i - 1)];
-            *e = (*e >= 0) ? base + *e : sidx[(r - 1) * V + (-*e - 1)];
-        }
+    __shared__ double s_mp[8][SR_MAX + 1];
+    double* mp = s_mp[warp];
+    for (int i = r + 1 + lane; i <= V; i += 32) mp[i] = minpair[(int64_t)(i - r) * V + (i - 1)];
+    __syncwarp();
+    const int base = (r - 1) * (2 * V - r) / 2 - r - 1;   // slot of (r, i) = base + i
+    for (int i = r + 1 + lane; i <= V; i += 32) {
+        const double m = mp[i];
+        int first = i;
+        for (int q = r + 1; q < i; ++q)
+            if (mp[q] == m) { first = q; break; }
+        sidx[(r - 1) * V + (i - 1)] = base + first;
     }
 }
-__global__ void __launch_bounds__(128) k_sdedup(pp_batch b) { sdedup_body(b); }
-__global__ void __launch_bounds__(128) k_sdedup_p(const pp_batch* __restrict__ bp) {
+__global__ void __launch_bounds__(256) k_sdedup(pp_batch b) { sdedup_body(b); }
+__global__ void __launch_bounds__(256) k_sdedup_p(const pp_batch* __restrict__ bp) {
     const pp_batch b = *bp;
     sdedup_body(b);
 }
