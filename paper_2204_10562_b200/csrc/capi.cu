@@ -487,7 +487,7 @@ static int prm_steps_graph(const pp_batch* b, void* stream) {
 static int prm_prep(const pp_batch* b, void* stream) {
     const int maxL = b->max_L, maxV = b->max_V;
     dim3 gp(b->n_inst, maxL > maxV ? maxL : maxV);
-    k_prep<<<gp, 128, 0, S(stream)>>>(*b);
+    k_prep<<<gp, 128, maxV <= PREP_CM_MAX ? sizeof(double) * maxV * maxV : 0, S(stream)>>>(*b);
     PP_CHECK_LAUNCH("k_prep");
     dim3 gbase(b->n_inst, maxL > maxV ? maxL : maxV);
     k_base<<<gbase, 128, 0, S(stream)>>>(*b, !(maxL <= SR_MAX && maxV <= SR_MAX));
@@ -510,7 +510,7 @@ static int prm_prep(const pp_batch* b, void* stream) {
 static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int total_inst) {
     const int maxL = b->max_L, maxV = b->max_V;
     dim3 gp(b->n_inst, maxL > maxV ? maxL : maxV);
-    k_prep_p<<<gp, 128, 0, S(stream)>>>(db);
+    k_prep_p<<<gp, 128, maxV <= PREP_CM_MAX ? sizeof(double) * maxV * maxV : 0, S(stream)>>>(db);
     PP_CHECK_LAUNCH("k_prep");
     k_base_p<<<gp, 128, 0, S(stream)>>>(db, 0);
     PP_CHECK_LAUNCH("k_base");

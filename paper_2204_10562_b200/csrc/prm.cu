@@ -40,6 +40,7 @@ __device__ __forceinline__ double W_at(const double* W, int L, int i, int l, int
 // grid (n_inst, max(maxL, maxV)); row y handles psum row ls=y+1, minpair row
 // lo=y+1 and the cross table of i=y+1.  Row 0 also computes prefix and phi.
 // ----------------------------------------------------------------------------
+constexpr int PREP_CM_MAX = 64;   // cross table via shared column minima up to this i
 __device__ __forceinline__ void prep_body(const pp_batch& b) {
     const pp_instance I = b.inst[blockIdx.x];
     const int L = I.L, V = I.V;
@@ -110,8 +111,34 @@ __device__ __forceinline__ void prep_body(const pp_batch& b) {
             ws[lay.minpair + (int64_t)(row - 1) * V + (hi - 1)] = m;
         }
     }
-    // cross table for i = row: thread per r in [1, i-1], sequential over rp
+    // cross table for i = row
     const int i = row;
+    if (b.max_V <= PREP_CM_MAX) {
+        // cm_r(x) = min bandwidth from rank x to the last r ranks (..i): thread per
+        // x, incremental in r; then cross(rp, r, i) = min over x in [i-r-rp+1, i-r]
+        // of cm_r(x): thread per r, incremental in rp.  Exact minima over the same
+        // pairs as the direct loop below.
+        extern __shared__ double s_cm[];   // [r-1][x-1], stride max_V (dynamic: max_V^2 doubles)
+        const int CM = b.max_V;
+        for (int x = 1 + t; x < i; x += blockDim.x) {
+            const double* bwr = bw + (int64_t)order[x - 1] * V;
+            double m = PP_INF;
+            for (int r = 1; r <= i - x; ++r) {
+                m = dmin(m, bwr[order[i - r]]);   // rank i - r + 1
+                s_cm[(r - 1) * CM + (x - 1)] = m;
+            }
+        }
+        __syncthreads();
+        for (int r = 1 + t; r < i; r += blockDim.x) {
+            double m = PP_INF;
+            for (int rp = 1; rp <= i - r; ++rp) {
+                m = dmin(m, s_cm[(r - 1) * CM + (i - r - rp)]);   // x = i - r - rp + 1
+                ws[lay.cross + cross_idx(V, i, r, rp)] = m;
+            }
+        }
+        return;
+    }
+    // thread per r in [1, i-1], sequential over rp
     for (int r = 1 + t; r < i; r += blockDim.x) {
         const int lo = i - r + 1;
         double m = PP_INF;
