@@ -1208,29 +1208,43 @@ __device__ void dp_walk(const pp_batch& b, const pp_instance& I, int l, int x, i
     const double* W = ws + lay.W;
     const bool allow = I.flags & PP_ALLOW_REPLICATION;
     const int lane = threadIdx.x & 31;
+    // shared-memory-path batches hold every stage term in the k_stab triangles and
+    // the chan quotients of multi-row payload classes in k_base's tables: the same
+    // expressions, so lookups give the bits the divisions would
+    const bool tables = b.max_L <= SR_MAX && b.max_V <= SR_MAX;
+    const int* sidx = reinterpret_cast<const int*>(ws + lay.sidx);
+    const int* rcls = reinterpret_cast<const int*>(ws + lay.chcls + CHAN_CLS);
+    const int64_t tri = (int64_t)(L - 1) * L / 2, tcls = (int64_t)V * ((int64_t)V * V - 1) / 6;
     while (x >= 2) {
         const int j = i - r;
         const double* X = ws + lay.X + X_base(L, i, r);
+        const double* St = tables ? ws + lay.Stab + (int64_t)sidx[(r - 1) * V + (i - 1)] * tri : nullptr;
         int lp = -1;
         for (int base = x - 1; base <= l - 1 && lp < 0; base += 32) {
             const int c = base + lane;
             bool match = false;
-            if (c <= l - 1)
-                match = dmax(X[(int64_t)(c - 1) * j + (x - 2)],
-                             stage_term(M, L, V, prefix, psum, minpair, c, l, r, i)) == w;
+            if (c <= l - 1) {
+                const double stc = St ? St[(c - 1) * L - (c - 1) * c / 2 + (l - c - 1)]
+                                      : stage_term(M, L, V, prefix, psum, minpair, c, l, r, i);
+                match = dmax(X[(int64_t)(c - 1) * j + (x - 2)], stc) == w;
+            }
             const int f = warp_first(match);
             if (f >= 0) lp = base + f;
         }
         int rp = -1;
         if (lp > 0) {
-            const double st = stage_term(M, L, V, prefix, psum, minpair, lp, l, r, i);
+            const double st = St ? St[(lp - 1) * L - (lp - 1) * lp / 2 + (l - lp - 1)]
+                                 : stage_term(M, L, V, prefix, psum, minpair, lp, l, r, i);
             const double Mp = (double)M * (b.efwd[I.layer_off + lp - 1] + b.ebwd[I.layer_off + lp - 1]);
+            const int cls = tables ? rcls[lp] : -1;
+            const double* Tj = cls >= 0 ? ws + lay.chan + cls * tcls + chan_step(V, j) : nullptr;
             for (int base = 1; base <= j && rp < 0; base += 32) {
                 const int c = base + lane;
                 bool match = false;
                 if (c <= j) {
                     const double sub = W_at(W, L, j, lp, c, x - 1, allow);
-                    const double chan = Mp / ((double)(c * r) * cross[cross_idx(V, i, r, c)]);
+                    const double chan = Tj ? Tj[(c - 1) * (V - j) + (r - 1)]
+                                           : Mp / ((double)(c * r) * cross[cross_idx(V, i, r, c)]);
                     match = dmax(dmax(sub, chan), st) == w;
                 }
                 const int f = warp_first(match);
