@@ -40,11 +40,6 @@ extern "C" {
 #define PP_SUM_NAIVE 2           /* CPython <= 3.11 float sum(); default is the 3.12+ Neumaier sum */
 #define PP_GIVEN_ORDER 4         /* order[] is an input (caller's DeviceOrdering); else RDO fills it */
 
-/* pp_layout reserves the first PP_WS_RESERVED doubles of the workspace for
- * library-internal device copies of pp_batch descriptors (the per-step DP is
- * replayed as a cached CUDA graph whose kernels read their batch from there). */
-#define PP_WS_RESERVED 512
-
 /* Build limits (checked by pp_layout). */
 #define PP_MAX_LAYERS 4096
 #define PP_MAX_GPUS 512
@@ -118,6 +113,9 @@ int pp_rdo_set_rounds(int32_t rounds);
 /* PartitionSolver over all cells + best_partition(xi) for every xi
  * (partition.py:41-162): fills sweep_w, sweep_r, stage_*. */
 int pp_prm(const pp_batch *b, void *stream);
+/* (The per-step schedule replays a CUDA graph cached per batch shape, per host
+ * thread; each cache entry owns 2.3 KB of device memory for the batch
+ * descriptors its kernels read.  Up to 8 shapes are cached.) */
 
 /* DP schedule for batches inside the shared-memory limits (L, V <= 128):
  * 0 = one launch pair per wavefront step (replayed as a cached CUDA graph),

@@ -119,7 +119,7 @@ int pp_device_count(void) {
 int pp_layout(int32_t n, const int32_t* L, const int32_t* V, const int32_t* M, const int32_t* flags,
               pp_instance* inst, int64_t* n_layer, int64_t* n_bw, int64_t* n_order, int64_t* n_sweep,
               int64_t* n_stage, int64_t* n_ev, int64_t* n_ar, int64_t* n_ws) {
-    int64_t lo = 0, bo = 0, oo = 0, so = 0, sto = 0, wo = PP_WS_RESERVED, eo = 0, ao = 0;
+    int64_t lo = 0, bo = 0, oo = 0, so = 0, sto = 0, wo = 0, eo = 0, ao = 0;
     for (int k = 0; k < n; ++k) {
         if (L[k] < 1 || L[k] > PP_MAX_LAYERS) return fail(PP_EINVAL, "instance %d: L=%d outside 1..%d", k, L[k], PP_MAX_LAYERS);
         if (V[k] < 1 || V[k] > PP_MAX_GPUS) return fail(PP_EINVAL, "instance %d: V=%d outside 1..%d", k, V[k], PP_MAX_GPUS);
@@ -413,25 +413,25 @@ static int prm_groups(const pp_batch* b, void* stream) { return prm_groups_impl(
 
 // The per-step schedule is ~2V dependent launches per instance group: launched
 // one by one the host's launch rate is the bound (~3.5 us per launch, measured:
-// the empty-kernel chain alone took 1.8 ms on C3).  It is captured once into a
-// CUDA graph and replayed; its kernels read their batch descriptor from the
-// reserved head of the workspace, so the graph stays valid for every batch of
-// the same shape in the same workspace (the descriptors are rewritten per call).
-struct GraphKey {   // what the captured launches bake in: descriptor location and grid shapes
-    const void* ws;
+// the empty-kernel chain alone took 1.8 ms on C3).  It is captured once per batch
+// SHAPE into a CUDA graph and replayed; its kernels read their batch descriptor
+// from a small library-owned device buffer of the cache entry (rewritten, stream
+// ordered, before every replay), so any workspace / buffers of that shape replay.
+struct GraphKey {   // what the captured launches bake in: grid shapes (descriptors live in the entry)
     int n_inst, max_L, max_V, G, dev;
     bool operator==(const GraphKey& o) const {
-        return ws == o.ws && n_inst == o.n_inst && max_L == o.max_L && max_V == o.max_V && G == o.G && dev == o.dev;
+        return n_inst == o.n_inst && max_L == o.max_L && max_V == o.max_V && G == o.G && dev == o.dev;
     }
 };
 struct GraphEntry {
     GraphKey key;
     cudaGraphExec_t exec;
+    pp_batch* d_desc;   // library-owned descriptor slots the graph's kernels read (256 B each)
+    cudaEvent_t done;   // last replay of this graph (the next one may rewrite the slots after it)
 };
 static thread_local std::vector<GraphEntry> g_graphs;
 static constexpr size_t PP_GRAPH_CACHE = 8;
 static_assert(sizeof(pp_batch) <= 256, "descriptor slot");
-static constexpr int PP_DESC_SLOT = 256 / sizeof(double);
 
 static int prm_steps_graph(const pp_batch* b, void* stream) {
     const int G = b->n_inst < g_dp_groups ? b->n_inst : g_dp_groups;
@@ -445,39 +445,49 @@ static int prm_steps_graph(const pp_batch* b, void* stream) {
         hd[1 + g].inst = b->inst + lo;
         hd[1 + g].n_inst = hi - lo;
     }
-    pp_batch* dev = reinterpret_cast<pp_batch*>(b->ws);
-    for (int g = 0; g <= ng; ++g)   // pageable source: staged by the driver, safe to reuse at once
-        if (cudaMemcpyAsync(b->ws + g * PP_DESC_SLOT, &hd[g], sizeof(pp_batch), cudaMemcpyHostToDevice, S(stream)) !=
-            cudaSuccess)
-            return fail(PP_ECUDA, "descriptor upload: %s", cudaGetErrorString(cudaGetLastError()));
     int d = 0;
     cudaGetDevice(&d);
-    const GraphKey key{b->ws, b->n_inst, b->max_L, b->max_V, G, d};
-    cudaGraphExec_t exec = nullptr;
+    const GraphKey key{b->n_inst, b->max_L, b->max_V, G, d};
+    GraphEntry* ent = nullptr;
     for (size_t k = 0; k < g_graphs.size(); ++k)
-        if (g_graphs[k].key == key) { exec = g_graphs[k].exec; break; }
-    if (!exec) {
+        if (g_graphs[k].key == key) { ent = &g_graphs[k]; break; }
+    if (!ent) {
         int rc;
         if ((rc = ensure_side_streams())) return rc;
+        if (g_graphs.size() >= PP_GRAPH_CACHE) {   // cudaFree waits for the evicted graph's last replay
+            GraphEntry& o = g_graphs.front();
+            cudaGraphExecDestroy(o.exec);
+            cudaFree(o.d_desc);
+            cudaEventDestroy(o.done);
+            g_graphs.erase(g_graphs.begin());
+        }
+        GraphEntry e{key, nullptr, nullptr, nullptr};
+        if (cudaMalloc(&e.d_desc, 256 * (1 + PP_DP_STREAMS)) != cudaSuccess ||
+            cudaEventCreateWithFlags(&e.done, cudaEventDisableTiming) != cudaSuccess)
+            return fail(PP_ECUDA, "graph descriptors: %s", cudaGetErrorString(cudaGetLastError()));
         cudaGraph_t graph;
-        cudaStream_t cs = g_side.capture;
+        cudaStream_t cs = g_side.capture;   // the caller's stream may be the (uncapturable) legacy stream
         if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
             return fail(PP_ECUDA, "graph capture: %s", cudaGetErrorString(cudaGetLastError()));
-        rc = prm_groups_impl(b, cs, dev);
+        rc = prm_groups_impl(b, cs, e.d_desc);
         const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
         if (rc) return rc;
         if (ce != cudaSuccess) return fail(PP_ECUDA, "graph capture: %s", cudaGetErrorString(ce));
-        const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+        const cudaError_t ie = cudaGraphInstantiate(&e.exec, graph, 0);
         cudaGraphDestroy(graph);
         if (ie != cudaSuccess) return fail(PP_ECUDA, "graph instantiate: %s", cudaGetErrorString(ie));
-        if (g_graphs.size() >= PP_GRAPH_CACHE) {
-            cudaGraphExecDestroy(g_graphs.front().exec);
-            g_graphs.erase(g_graphs.begin());
-        }
-        g_graphs.push_back({key, exec});
+        g_graphs.push_back(e);
+        ent = &g_graphs.back();
+    } else {
+        cudaStreamWaitEvent(S(stream), ent->done, 0);   // a replay on another stream may still read the slots
     }
-    if (cudaGraphLaunch(exec, S(stream)) != cudaSuccess)
+    for (int g = 0; g <= ng; ++g)   // pageable source: staged by the driver, safe to reuse at once
+        if (cudaMemcpyAsync(reinterpret_cast<char*>(ent->d_desc) + 256 * g, &hd[g], sizeof(pp_batch),
+                            cudaMemcpyHostToDevice, S(stream)) != cudaSuccess)
+            return fail(PP_ECUDA, "descriptor upload: %s", cudaGetErrorString(cudaGetLastError()));
+    if (cudaGraphLaunch(ent->exec, S(stream)) != cudaSuccess)
         return fail(PP_ECUDA, "graph launch: %s", cudaGetErrorString(cudaGetLastError()));
+    cudaEventRecord(ent->done, S(stream));
     g_launches.fetch_add(1 + 2 * (int64_t)ng * (b->max_V - 1) + 5 * ng, std::memory_order_relaxed);
     return PP_OK;
 }

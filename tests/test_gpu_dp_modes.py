@@ -162,9 +162,10 @@ def test_cluster_per_instance_identical(persistent):
 
 
 def test_graph_replay_across_batches(persistent):
-    """The per-step DP is replayed from a cached CUDA graph keyed on (workspace,
-    shape); batches of one shape with different data (and repeated runs) must
-    each give their own, exact results."""
+    """The per-step DP is replayed from a CUDA graph cached per batch shape (its
+    descriptors rewritten before each replay); batches of one shape with
+    different data and buffers (and repeated runs) must each give their own,
+    exact results."""
     from paper_2204_10562_b200 import _device, planner
     specs_a = [W.c3_gpt96(M=m, nodes=2, per_node=8) for m in (8, 32, 128)]
     specs_b = [W.c3_gpt96(M=m, jitter_seed=11, nodes=2, per_node=8) for m in (8, 32, 128)]
