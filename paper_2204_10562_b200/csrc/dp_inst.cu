@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(DI_T, 3) k_dp_inst(pp_batch b, int smem_double
                 // (copied from the row's payload-class table when it has one: same bits)
                 const int* rcls = reinterpret_cast<const int*>(ws + lay.chcls + CHAN_CLS);
                 const double* T0 = ws + lay.chan + chan_step(V, j);
-                const int64_t tcls = (int64_t)V * ((int64_t)V * V - 1) / 6;
+                const int64_t tcls = (int64_t)tet(V);
                 const bool any_cls = rcls[0] > 0;
                 for (int e = t; e < nrow * j * nr; e += blockDim.x) {
                     int k, o, rp, q;

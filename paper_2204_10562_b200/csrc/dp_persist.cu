@@ -133,7 +133,7 @@ __device__ void expand_r1(const pp_batch& b, const pp_instance& I, int j, int la
         const double Mp = (double)M * (b.efwd[I.layer_off + lp - 1] + b.ebwd[I.layer_off + lp - 1]);
         const double* Wsrc = ws + lay.W + W_idx(L, j, lp, 1, 1);   // [r'-1][xi'-1], stride j
         const int cls = reinterpret_cast<const int*>(ws + lay.chcls + CHAN_CLS)[lp];
-        const double* Tj = ws + lay.chan + (int64_t)max(cls, 0) * V * ((int64_t)V * V - 1) / 6 + chan_step(V, j);
+        const double* Tj = ws + lay.chan + (int64_t)max(cls, 0) * tet(V) + chan_step(V, j);
         for (int rp = 1 + lane; rp <= j; rp += 32)   // the class table holds the same quotient
             ch[rp - 1] = cls >= 0 ? Tj[(rp - 1) * (V - j)] : Mp / ((double)(rp * 1) * cross[cross_idx(V, j + 1, 1, rp)]);
         __syncwarp();

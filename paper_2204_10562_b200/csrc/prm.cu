@@ -239,7 +239,7 @@ __device__ __forceinline__ void base_body(const pp_batch& b, int full_rows) {
         const int ncls = reinterpret_cast<const int*>(cv + CHAN_CLS)[0];
         const double* cross = ws + lay.cross;
         for (int c = 0; c < ncls; ++c) {
-            double* Tj = ws + lay.chan + (int64_t)c * V * ((int64_t)V * V - 1) / 6 + chan_step(V, j);
+            double* Tj = ws + lay.chan + (int64_t)c * tet(V) + chan_step(V, j);
             const double Mp = cv[c];
             for (int e = t; e < j * nr; e += blockDim.x) {
                 const int rp = 1 + e / nr, r = 1 + e % nr;
@@ -403,14 +403,18 @@ __global__ void __launch_bounds__(128) k_stab_big_p(const pp_batch* __restrict__
 
 // Debug timeline of the per-step kernels (tools/step_trace.py): one record of
 // 4 x u64 per CTA when g_step_trace is set: (kind << 56 | j << 40 | smid << 32 | block
-// linear id), start, end, 0 (globaltimer ns).
+// linear id), start, end, end of the PDL wait (0 if none) (globaltimer ns).
 __device__ unsigned long long* g_step_trace = nullptr;
 __device__ int g_step_trace_cap = 0;
 __device__ int g_step_trace_n = 0;
+__shared__ unsigned long long s_trace_wait;
 struct StepTrace {
     unsigned long long t0 = 0;
     __device__ __forceinline__ void begin() {
-        if (g_step_trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        if (g_step_trace && threadIdx.x == 0) {
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            s_trace_wait = 0;
+        }
     }
     __device__ __forceinline__ void end(int kind, int j) {
         if (!g_step_trace) return;
@@ -425,7 +429,7 @@ struct StepTrace {
         const unsigned long long bid = blockIdx.x + (unsigned long long)gridDim.x * (blockIdx.y + (unsigned long long)gridDim.y * blockIdx.z);
         unsigned long long* r = g_step_trace + 4 * (int64_t)k;
         r[0] = ((unsigned long long)kind << 56) | ((unsigned long long)j << 40) | ((unsigned long long)smid << 32) | (bid & 0xffffffffu);
-        r[1] = t0; r[2] = t1; r[3] = 0;
+        r[1] = t0; r[2] = t1; r[3] = s_trace_wait;
     }
 };
 
@@ -433,7 +437,20 @@ struct StepTrace {
 // lets its successor launch as soon as all its CTAs run, and the successor
 // stages its producer-independent operands before waiting (no-ops without PDL).
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// where the per-step kernels let their successor launch: 0 = at entry,
+// 1 = once the CTA's operands are staged, 2 = after its compute (measured
+// best: n = 1 C3 DP 1.42 -> 1.33 ms; early-launched successors only occupy slots)
+#ifndef PDL_TRIGGER_AT
+#define PDL_TRIGGER_AT 2
+#endif
+template <int AT>
+__device__ __forceinline__ void pdl_trigger_at() {
+    if constexpr (AT == PDL_TRIGGER_AT) pdl_trigger();
+}
+__device__ __forceinline__ void pdl_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (g_step_trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(s_trace_wait));
+}
 
 // (min, max) micro-kernel: a thread owns a TA x TB register tile and folds one
 // K index per step, acc[a][c] = min(acc[a][c], max(p[a], q[c])).
@@ -747,7 +764,7 @@ __device__ __forceinline__ void expand_row_s(const pp_batch& b, const pp_instanc
     // table (same expression, same bits), else divided here
     const int cls = reinterpret_cast<const int*>(ws + lay.chcls + CHAN_CLS)[lp];
     if (cls >= 0) {
-        const double* Tj = ws + lay.chan + (int64_t)cls * V * ((int64_t)V * V - 1) / 6 + chan_step(V, j);
+        const double* Tj = ws + lay.chan + (int64_t)cls * tet(V) + chan_step(V, j);
         for (int rp = 1 + warp; rp <= j; rp += nw)
             for (int q = lane; q < nt; q += 32) cp_async8(B + (rp - 1) * nt + q, Tj + (rp - 1) * nr + (q + rfirst - 1));
         cp_async_commit();
@@ -773,6 +790,7 @@ __device__ __forceinline__ void expand_row_s(const pp_batch& b, const pp_instanc
     for (int q = t; q < nt; q += blockDim.x) s_xb[q] = X_base(L, j + rfirst + q, rfirst + q);
     cp_async_wait<0>();
     __syncthreads();
+    pdl_trigger_at<1>();
     constexpr int TRW = EXPAND_TRW;   // target columns per register tile (4 xi x TRW r)
     const int ntx = (j + 3) >> 2, ntr = (nt + TRW - 1) / TRW, ntiles = ntx * ntr;
     // split-K when the plane has few tiles: ks consecutive lanes share a tile,
@@ -837,7 +855,7 @@ __global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
     expand_row_s(b, I, j, lp, 1, ex_smem);
 }
 __global__ void __launch_bounds__(128, EXPAND_TRW == 2 ? 5 : 4) k_expand_s_p(const pp_batch* __restrict__ bp, int j) {
-    pdl_trigger();
+    pdl_trigger_at<0>();
     StepTrace tr;
     tr.begin();
     const pp_batch b = *bp;
@@ -846,6 +864,7 @@ __global__ void __launch_bounds__(128, EXPAND_TRW == 2 ? 5 : 4) k_expand_s_p(con
     if (j >= I.V || lp > I.L - 1) return;
     extern __shared__ __align__(16) double ex_smem[];
     expand_row_s(b, I, j, lp, 1, ex_smem);
+    pdl_trigger_at<2>();
     tr.end(1, j);
 }
 
@@ -1155,6 +1174,7 @@ __device__ __forceinline__ void combine_item_s(const pp_batch& b, const pp_insta
         cp_async_wait<0>();
     }
     __syncthreads();
+    pdl_trigger_at<1>();
     const double* S = j > S_DIRECT_J ? Stri : Sg;
     const bool mono = g_combine_early_exit && reinterpret_cast<const int*>(ws + lay.smono)[slot];
     if (j >= 4) combine_tiles_s<4, COMBINE_TL4>(Wi, i, r, L, j, S, trio, Xs, s_hist, s_order, part, nparts, lA, lB, atomic, mono);
@@ -1170,7 +1190,7 @@ __global__ void __launch_bounds__(256, 2) k_combine_s(pp_batch b, int j) {
     combine_item_s(b, I, j, blockIdx.y + 1, blockIdx.z, gridDim.z, cs_smem, s_hist, s_order, false);
 }
 __global__ void __launch_bounds__(256, COMBINE_TL4 == 2 ? 3 : 2) k_combine_s_p(const pp_batch* __restrict__ bp, int j) {
-    pdl_trigger();
+    pdl_trigger_at<0>();
     StepTrace tr;
     tr.begin();
     const pp_batch b = *bp;
@@ -1179,6 +1199,7 @@ __global__ void __launch_bounds__(256, COMBINE_TL4 == 2 ? 3 : 2) k_combine_s_p(c
     __shared__ int s_hist[SR_MAX + 2];
     __shared__ int s_order[1024];
     combine_item_s(b, I, j, blockIdx.y + 1, blockIdx.z, gridDim.z, cs_smem, s_hist, s_order, false);
+    pdl_trigger_at<2>();
     tr.end(2, j);
 }
 
@@ -1214,7 +1235,7 @@ __device__ void dp_walk(const pp_batch& b, const pp_instance& I, int l, int x, i
     const bool tables = b.max_L <= SR_MAX && b.max_V <= SR_MAX;
     const int* sidx = reinterpret_cast<const int*>(ws + lay.sidx);
     const int* rcls = reinterpret_cast<const int*>(ws + lay.chcls + CHAN_CLS);
-    const int64_t tri = (int64_t)(L - 1) * L / 2, tcls = (int64_t)V * ((int64_t)V * V - 1) / 6;
+    const int64_t tri = (int64_t)(L - 1) * L / 2, tcls = (int64_t)tet(V);
     while (x >= 2) {
         const int j = i - r;
         const double* X = ws + lay.X + X_base(L, i, r);

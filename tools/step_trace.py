@@ -23,18 +23,21 @@ print(f"prm {a.elapsed_time(b):.3f} ms")
 tr = buf.view(-1, 4).cpu().numpy().astype(np.uint64)
 tr = tr[tr[:, 2] != 0].astype(np.int64)
 kind = (tr[:, 0] >> 56) & 0xff; j = (tr[:, 0] >> 40) & 0xffff
-t0 = tr[:, 1]; t1 = tr[:, 2]; base = t0.min()
+t0 = tr[:, 1]; t1 = tr[:, 2]; tw = tr[:, 3]; base = t0.min()
 s, e = (t0 - base) / 1e3, (t1 - base) / 1e3
+w = np.where(tw > 0, (tw - base) / 1e3, s)   # end of the PDL wait
 print(f"{len(tr)} CTAs, span {e.max():.1f} us")
 for k, nm in ((1, "expand"), (2, "combine")):
     m = kind == k
     d = e[m] - s[m]
     print(f"{nm}: {m.sum()} CTAs, CTA time mean {d.mean():.2f} us p50 {np.median(d):.2f} p90 {np.percentile(d, 90):.2f} max {d.max():.1f}; total CTA-us {d.sum() / 1e3:.1f} ms")
+    dw = w[m] - s[m]
+    print(f"    of which PDL wait mean {dw.mean():.2f} us (total {dw.sum() / 1e3:.1f} ms), after wait mean {(e[m] - w[m]).mean():.2f} us")
 for jj in (1, 8, 16, 32, 48, 62):
     for k, nm in ((1, "E"), (2, "C")):
         m = (kind == k) & (j == jj)
         if m.any():
-            print(f"  j={jj:2d} {nm}: CTAs {m.sum():5d}  window [{s[m].min():8.1f}, {e[m].max():8.1f}] = {e[m].max() - s[m].min():6.1f} us  CTA mean {np.mean(e[m] - s[m]):5.2f} max {np.max(e[m] - s[m]):5.2f}")
+            print(f"  j={jj:2d} {nm}: CTAs {m.sum():5d}  window [{s[m].min():8.1f}, {e[m].max():8.1f}] = {e[m].max() - s[m].min():6.1f} us  CTA mean {np.mean(e[m] - s[m]):5.2f} max {np.max(e[m] - s[m]):5.2f} post-wait {np.mean(e[m] - w[m]):5.2f}")
 # per-step window: first CTA start of E(j) to last end of C(j), and gaps
 ws = []
 for jj in range(1, int(j.max()) + 1):
