@@ -84,6 +84,11 @@ typedef struct {
     double *ar_start, *ar_end;
     double *ws;                       /* fp64 workspace, pp_layout() doubles                      */
     double *gamma;                    /* [n_inst] cost.py:126-128, written by pp_phi; NULL skips  */
+    /* schedule order of the selected plan's events (optional, needs ev_start):
+     * ev_order[ev_off + k] = (m-1)*(4N-3) + pos-1 of the k-th event of the
+     * reference's Schedule.events order (start, resource key, microbatch,
+     * position; scheduler.py:227-231); NULL skips */
+    int32_t *ev_order;
 } pp_batch;
 
 /* ---- host helpers (no device work) ------------------------------------ */

@@ -172,8 +172,8 @@ class DeviceBatch:
         ev = n_ev if capture_events else 0
         self.f_off = np.cumsum([0, n_sweep, n_sweep, n_sweep, n, n, n, n_ar, n_ar, ev, ev])
         self.d_fout = torch.empty(int(self.f_off[-1]), dtype=F64, device=dev)
-        # int32 outputs: [sweep_r | ls | le | dlo | dhi | best_xi]
-        self.i_off = np.cumsum([0, n_sweep, n_stage, n_stage, n_stage, n_stage, n])
+        # int32 outputs: [sweep_r | ls | le | dlo | dhi | best_xi | ev_order]
+        self.i_off = np.cumsum([0, n_sweep, n_stage, n_stage, n_stage, n_stage, n, ev])
         self.d_iout = torch.empty(int(self.i_off[-1]), dtype=I32, device=dev)
         self.d_ws = torch.empty(max(n_ws, 1), dtype=F64, device=dev)
         self.capture_events = capture_events
@@ -201,6 +201,7 @@ class DeviceBatch:
         io = self.d_iout.data_ptr()
         io_ = [io + 4 * int(x) for x in self.i_off]
         b.sweep_r, b.stage_ls, b.stage_le, b.stage_dlo, b.stage_dhi, b.best_xi = io_[:6]
+        b.ev_order = io_[6] if capture_events else None
         b.ws = self.d_ws.data_ptr()
         self.batch = b
         self.lib = lib
@@ -225,7 +226,7 @@ class DeviceBatch:
              for i, k in enumerate(("sweep_w", "sweep_mk", "sweep_bound", "best_mk", "phi", "gamma",
                                     "ar_start", "ar_end", "ev_start", "ev_end"))}
         g = {k: io[int(self.i_off[i]):int(self.i_off[i + 1])]
-             for i, k in enumerate(("sweep_r", "ls", "le", "dlo", "dhi", "best_xi"))}
+             for i, k in enumerate(("sweep_r", "ls", "le", "dlo", "dhi", "best_xi", "ev_order"))}
         f.update(g)
         f["order"] = order
         return f

@@ -43,6 +43,8 @@ __global__ void k_min_cut(pp_batch b, int k, const int* verts, int n, unsigned c
 __global__ void k_pe_sweep(pp_batch b);
 __global__ void k_pe_sweep_w(pp_batch b);
 __global__ void k_replay_w(pp_batch b);
+__global__ void k_event_merge(pp_batch b);
+__global__ void k_event_rank(pp_batch b);
 __global__ void k_select(pp_batch b);
 __global__ void k_replay(pp_batch b);
 __global__ void k_sim_plans(pp_batch b, pp_sim_batch s);
@@ -85,10 +87,12 @@ static const int g_max_parts = read_max_parts();
 // PP_COMBINE_WAVES x SMs CTAs
 static int read_combine_waves() {
     const char* e = getenv("PP_COMBINE_WAVES");
-    const int v = e ? atoi(e) : 1;
+    const int v = e ? atoi(e) : 2;   // n = 1 C3 DP: 1.25 ms at 1 wave, 1.21 at 2, 1.24 at 3
     return v < 1 ? 1 : (v > 16 ? 16 : v);
 }
 static const int g_combine_waves = read_combine_waves();
+// expand CTAs get 256 threads when a step has <= this many rows per SM (PP_EXPAND_WIDE env)
+static const int g_expand_wide = getenv("PP_EXPAND_WIDE") ? atoi(getenv("PP_EXPAND_WIDE")) : 2;
 // programmatic dependent launch in the per-step chain (PP_PDL=0 disables)
 static const int g_pdl = getenv("PP_PDL") ? atoi(getenv("PP_PDL")) : 1;
 
@@ -546,7 +550,9 @@ static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int 
         if (maxL > 1) {
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(b->n_inst, maxL - 1);
-            cfg.blockDim = dim3(128);
+            // a step with fewer rows than SMs runs one CTA per SM: twice the warps
+            // per row (split-K over r') hides the issue latency of its (min, max) chain
+            cfg.blockDim = dim3((int64_t)total_inst * (maxL - 1) <= g_expand_wide * num_sms() ? 256 : 128);
             cfg.dynamicSmemBytes = sizeof(double) * (size_t)j * maxV;
             cfg.stream = S(stream);
             cfg.attrs = pdl;
@@ -668,6 +674,13 @@ int pp_select(const pp_batch* b, void* stream) {
             k_replay<<<b->n_inst, sim_block(b->max_V), smem, S(stream)>>>(*b);
         }
         PP_CHECK_LAUNCH("k_replay");
+        if (b->ev_order) {
+            cudaFuncSetAttribute(k_event_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, EM_SMEM);
+            k_event_merge<<<b->n_inst, EM_T, EM_SMEM, S(stream)>>>(*b);
+            PP_CHECK_LAUNCH("k_event_merge");
+            k_event_rank<<<dim3(b->n_inst, 16), 256, 0, S(stream)>>>(*b);
+            PP_CHECK_LAUNCH("k_event_rank");
+        }
     }
     return PP_OK;
 }

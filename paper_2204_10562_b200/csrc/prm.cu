@@ -854,7 +854,7 @@ __global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
     extern __shared__ __align__(16) double ex_smem[];
     expand_row_s(b, I, j, lp, 1, ex_smem);
 }
-__global__ void __launch_bounds__(128, EXPAND_TRW == 2 ? 5 : 4) k_expand_s_p(const pp_batch* __restrict__ bp, int j) {
+__global__ void __launch_bounds__(256, EXPAND_TRW == 2 ? 2 : 2) k_expand_s_p(const pp_batch* __restrict__ bp, int j) {
     pdl_trigger_at<0>();
     StepTrace tr;
     tr.begin();

@@ -351,6 +351,116 @@ __global__ void __launch_bounds__(32) k_replay_w(pp_batch b) {
                          b.ar_start + I.ar_off, b.ar_end + I.ar_off);
 }
 
+// Resource sort key of block position p in an N-stage plan (scheduler.py:115-118
+// via model.py:148-158): compute blocks sort by stage, channels after all
+// stages by channel index.
+__device__ __forceinline__ int ev_key(int N, int p) {
+    if (p & 1) return p <= 2 * N - 1 ? (p + 1) >> 1 : (4 * N - 1 - p) >> 1;
+    return (1 << 20) + (p <= 2 * N - 2 ? p >> 1 : (4 * N - 2 - p) >> 1);
+}
+
+// The reference's event order of the selected plan's schedule: events sorted by
+// (start, resource key, microbatch, position) (scheduler.py:227-231), a strict
+// total order.  Each position q is served by one resource in increasing
+// microbatch order, so its column start(., q) is non-decreasing in m: the J
+// columns are already-sorted runs and ordering the events is a merge.
+__device__ __forceinline__ uint64_t ev_tie(int N, int J, int e) {
+    const int m = e / J, p = e - m * J + 1;   // m 0-based
+    return ((uint64_t)ev_key(N, p) << 43) | ((uint64_t)m << 12) | (uint64_t)p;
+}
+
+// k_event_merge: one CTA per instance, start times staged in shared memory, the
+// J runs merged pairwise (ceil(log2 J) levels, merge-path split per thread,
+// 16-bit event indices ping-ponged in shared memory).  n = M (4N-3) <= EM_MAXN.
+constexpr int EM_T = 1024;
+constexpr int EM_SMEM = 216 * 1024;
+constexpr int EM_MAXN = EM_SMEM / 12 < 65536 ? EM_SMEM / 12 : 65536;
+__global__ void __launch_bounds__(EM_T) k_event_merge(pp_batch b) {
+    const pp_instance I = b.inst[blockIdx.x];
+    const int N = b.best_xi[blockIdx.x];
+    if (N <= 0) return;
+    const int M = I.M, J = 4 * N - 3, n = M * J;
+    if (n > EM_MAXN) return;   // k_event_rank orders it
+    extern __shared__ __align__(16) double em_key[];
+    unsigned short* A = reinterpret_cast<unsigned short*>(em_key + n);
+    unsigned short* B = A + n;
+    const double* st = b.ev_start + I.ev_off;
+    const int t = threadIdx.x;
+    for (int k = t; k < n; k += EM_T) {
+        em_key[k] = st[k];
+        const int q = k / M, m = k - q * M;   // run q = column q+1, in microbatch order
+        A[k] = (unsigned short)(m * J + q);
+    }
+    __syncthreads();
+    auto less = [&](int x, int y) {
+        const double u = em_key[x], v = em_key[y];
+        return u != v ? u < v : ev_tie(N, J, x) < ev_tie(N, J, y);
+    };
+    const int per = (n + EM_T - 1) / EM_T;
+    for (int R = M; R < n; R *= 2) {
+        int o = t * per;
+        const int oend = min(n, o + per);
+        while (o < oend) {
+            const int base = o / (2 * R) * (2 * R);
+            const int la = min(R, n - base), lb = max(0, min(R, n - base - R));
+            const unsigned short* X = A + base;
+            const unsigned short* Y = X + la;
+            const int d = o - base;
+            int lo = max(0, d - lb), hi = min(d, la);   // merge path: X elements among the first d
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (less(X[mid], Y[d - 1 - mid])) lo = mid + 1; else hi = mid;
+            }
+            int xi = lo, yi = d - lo;
+            const int stop = min(oend, base + la + lb);
+            // the two heads (index + start) stay in registers: one shared load per output
+            int ex = xi < la ? X[xi] : 0, ey = yi < lb ? Y[yi] : 0;
+            double kx = em_key[ex], ky = em_key[ey];
+            for (; o < stop; ++o) {
+                const bool takeX = yi >= lb || (xi < la && (kx != ky ? kx < ky : ev_tie(N, J, ex) < ev_tie(N, J, ey)));
+                if (takeX) {
+                    B[o] = (unsigned short)ex;
+                    if (++xi < la) { ex = X[xi]; kx = em_key[ex]; }
+                } else {
+                    B[o] = (unsigned short)ey;
+                    if (++yi < lb) { ey = Y[yi]; ky = em_key[ey]; }
+                }
+            }
+        }
+        __syncthreads();
+        unsigned short* T = A; A = B; B = T;
+    }
+    for (int k = t; k < n; k += EM_T) b.ev_order[I.ev_off + k] = A[k];
+}
+
+// k_event_rank: instances too large for k_event_merge.  One thread per event,
+// its rank = sum over columns of a binary search for the events below it
+// (O(J log M) loads per event); ranks are a permutation.
+__global__ void __launch_bounds__(256) k_event_rank(pp_batch b) {
+    const pp_instance I = b.inst[blockIdx.x];
+    const int N = b.best_xi[blockIdx.x];
+    if (N <= 0) return;
+    const int M = I.M, J = 4 * N - 3, n = M * J;
+    if (n <= EM_MAXN) return;
+    const double* st = b.ev_start + I.ev_off;
+    for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < n; e += gridDim.y * blockDim.x) {
+        const double s = st[e];
+        const uint64_t te = ev_tie(N, J, e);
+        int rank = 0;
+        for (int q = 1; q <= J; ++q) {
+            const double* col = st + (q - 1);
+            int a = 0, c = M;   // #{m' : (start, tie)(m', q) < (s, te)}: the column is sorted by it
+            while (a < c) {
+                const int mid = (a + c) >> 1;
+                const double v = col[(int64_t)mid * J];
+                if (v < s || (v == s && ev_tie(N, J, mid * J + q - 1) < te)) a = mid + 1; else c = mid;
+            }
+            rank += a;
+        }
+        b.ev_order[I.ev_off + rank] = e;
+    }
+}
+
 __host__ __device__ inline int sim_threads(int N) {
     const int R = 2 * N - 1;
     const int t = (R + 31) / 32 * 32;

@@ -121,7 +121,6 @@ def _labels(N: int):
 
 
 @functools.lru_cache(maxsize=256)
-@functools.lru_cache(maxsize=256)
 def _pe_tiebreak_order(N: int, M: int):
     """Permutation of the (m, pos) grid sorted by (resource key, microbatch, position): a
     stable sort by start time on top of it yields the reference's event order.
@@ -186,7 +185,12 @@ def _build_schedule(plan: Plan, rec, tiebreak=None) -> Schedule:
     start = rec["ev_start"]
     end = rec["ev_end"]
     # stable order of the reference: (start, resource key, microbatch), ties in queue order
-    if tiebreak is None:
+    if tiebreak is None and rec.get("ev_order") is not None:
+        # ordered on the device (k_event_order): rank k holds event (m-1)*J + pos-1
+        o = rec["ev_order"]
+        mo, po = np.divmod(o, J)
+        events = LazyEvents(res, lab, mo + 1, po + 1, start[o], end[o])
+    elif tiebreak is None:
         # PE queues: same-resource, same-microbatch ties are in position order
         order, mo, po = _pe_tiebreak_order(N, M)
         so = start[order]

@@ -192,6 +192,38 @@ def test_wider_random_instances_vs_oracle():
     _check_vs_oracle(specs, res)
 
 
+def test_event_order_ties_vs_oracle():
+    """Equal costs and zero-byte edges: many events share a start time, so the
+    device event order (k_event_order) is decided by the (resource key,
+    microbatch, position) tie rule."""
+    rng = random.Random(5)
+    specs = []
+    for L, V, M in ((6, 4, 5), (12, 8, 16), (9, 6, 7), (24, 16, 32), (1, 3, 4), (5, 1, 9)):
+        ids = rng.sample(range(1, 1000), V)
+        e = [0.0] * (L - 1) if L % 2 == 0 else [1e6] * (L - 1)
+        specs.append(_spec([1.0] * L, [2.0] * L, [1e6] * L, e, list(e), ids,
+                           [(a, b, 1e9) for k, a in enumerate(ids) for b in ids[k + 1:]], M))
+    res = P.spp_many([model_of(s) for s in specs])
+    _check_vs_oracle(specs, res)
+    starts = [ev.start for r in res for ev in r.schedule.events]
+    assert len(starts) > len(set(starts))   # the cases do tie
+
+
+def test_event_order_large_schedules_vs_oracle():
+    """Schedules beyond the shared-memory merge (M (4N-3) > 18432 events) are
+    ordered by the per-event rank kernel."""
+    rng = random.Random(11)
+    fwd, bwd, par, ef, eb, ids, links, _ = _random_instance(rng, Lmax=20, Vmax=12, Mmax=2)
+    specs = [_spec(fwd, bwd, par, ef, eb, ids, links, 700)]
+    ids = rng.sample(range(1, 1000), 12)
+    # heavy parameters on slow links: replication loses, the plan pipelines deep
+    specs.append(_spec([1.0] * 24, [2.0] * 24, [1e12] * 24, [1e3] * 23, [1e3] * 23, ids,
+                       [(a, b, 1e9) for k, a in enumerate(ids) for b in ids[k + 1:]], 1500))
+    res = P.spp_many([model_of(s) for s in specs])
+    _check_vs_oracle(specs, res)
+    assert max(len(r.schedule.events) for r in res) > 18432
+
+
 def _spec_from_workload(w):
     return _spec(w.fwd, w.bwd, w.param, w.efwd, w.ebwd, list(w.gpu_ids), w.links, w.M)
 

@@ -22,3 +22,12 @@ for _ in range(3):
     t5 = time.perf_counter()
     print(f"validate+pack {1e3*(t1-t0):.1f} ms | DeviceBatch (H2D+alloc) {1e3*(t2-t1):.1f} | enqueue {1e3*(t3-t2):.1f} "
           f"| fetch (sync+D2H) {1e3*(t4-t3):.1f} | decode {1e3*(t5-t4):.1f} | total {1e3*(t5-t0):.1f}")
+
+if "--profile" in sys.argv:
+    import cProfile, pstats
+    pr = cProfile.Profile()
+    pr.enable()
+    for _ in range(5):
+        planner.spp_many(models)
+    pr.disable()
+    pstats.Stats(pr).sort_stats("tottime").print_stats(25)
