@@ -18,6 +18,7 @@ __global__ void k_stab_p(const pp_batch* bp);
 __global__ void k_stab_big_p(const pp_batch* bp);
 __global__ void k_stab_big(pp_batch b);
 __global__ void k_expand_s_p(const pp_batch* bp, int j);
+__global__ void k_expand_m_p(const pp_batch* bp, int j, int rb);
 __global__ void k_combine_s_p(const pp_batch* bp, int j);
 __global__ void k_backtrack_p(const pp_batch* bp);
 __global__ void k_phi(pp_batch b);
@@ -93,6 +94,11 @@ static int read_combine_waves() {
 static const int g_combine_waves = read_combine_waves();
 // expand CTAs get 256 threads when a step has <= this many rows per SM (PP_EXPAND_WIDE env)
 static const int g_expand_wide = getenv("PP_EXPAND_WIDE") ? atoi(getenv("PP_EXPAND_WIDE")) : 2;
+// rows per expand CTA when a step has more than PP_EXPAND_RB_MIN rows per SM
+// (PP_EXPAND_RB env, default 4; the chan block is shared by the CTA's rows)
+static const int g_expand_rb = getenv("PP_EXPAND_RB") ? std::max(1, atoi(getenv("PP_EXPAND_RB"))) : 4;
+static const int g_expand_rb_min = getenv("PP_EXPAND_RB_MIN") ? atoi(getenv("PP_EXPAND_RB_MIN")) : 4;
+static constexpr int64_t EX_SMEM_DOUBLES = 12288;   // 96 KB: two 256-thread CTAs per SM
 // programmatic dependent launch in the per-step chain (PP_PDL=0 disables)
 static const int g_pdl = getenv("PP_PDL") ? atoi(getenv("PP_PDL")) : 1;
 
@@ -540,6 +546,8 @@ static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int 
     const size_t cs_smem = sizeof(double) * ((maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 +
                                              (size_t)(maxL > 1 ? maxL - 1 : 0) * maxV);
     cudaFuncSetAttribute(k_expand_s_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ex_smem);
+    cudaFuncSetAttribute(k_expand_m_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max(ex_smem, sizeof(double) * (size_t)EX_SMEM_DOUBLES));
     cudaFuncSetAttribute(k_combine_s_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs_smem);
     // programmatic dependent launch between consecutive wavefront kernels: each
     // stages its producer-independent operands while its predecessor drains
@@ -549,15 +557,24 @@ static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int 
     for (int j = 1; j < maxV; ++j) {
         if (maxL > 1) {
             cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(b->n_inst, maxL - 1);
             // a step with fewer rows than SMs runs one CTA per SM: twice the warps
-            // per row (split-K over r') hides the issue latency of its (min, max) chain
-            cfg.blockDim = dim3((int64_t)total_inst * (maxL - 1) <= g_expand_wide * num_sms() ? 256 : 128);
-            cfg.dynamicSmemBytes = sizeof(double) * (size_t)j * maxV;
+            // per row (split-K over r') hides the issue latency of its (min, max) chain;
+            // with many rows, rb rows per 256-thread CTA share their chan block
+            const int64_t rows = (int64_t)total_inst * (maxL - 1);
+            int rb = 1;
+            if (rows > (int64_t)g_expand_rb_min * num_sms()) {
+                rb = g_expand_rb;
+                const int64_t cap = (EX_SMEM_DOUBLES - (int64_t)j * (maxV - j)) / ((int64_t)j * j);
+                if (rb > cap) rb = cap < 1 ? 1 : (int)cap;
+            }
+            cfg.gridDim = dim3(b->n_inst, ceil_div(maxL - 1, rb));
+            cfg.blockDim = dim3(rb > 1 || rows <= g_expand_wide * num_sms() ? 256 : 128);
+            cfg.dynamicSmemBytes = sizeof(double) * std::max((size_t)j * maxV, (size_t)rb * j * j + (size_t)j * (maxV - j));
             cfg.stream = S(stream);
             cfg.attrs = pdl;
             cfg.numAttrs = 1;
-            if (cudaLaunchKernelEx(&cfg, k_expand_s_p, db, j) != cudaSuccess)
+            if ((rb > 1 ? cudaLaunchKernelEx(&cfg, k_expand_m_p, db, j, rb) : cudaLaunchKernelEx(&cfg, k_expand_s_p, db, j)) !=
+                cudaSuccess)
                 return fail(PP_ECUDA, "k_expand_s launch: %s", cudaGetErrorString(cudaGetLastError()));
             PP_CHECK_LAUNCH("k_expand_s");
         }

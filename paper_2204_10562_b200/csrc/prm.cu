@@ -847,6 +847,97 @@ __device__ __forceinline__ void expand_row_s(const pp_batch& b, const pp_instanc
     }
 }
 
+// expand, step j, for nrows consecutive rows l' that share one chan payload
+// class (every row of a transformer stack): the chan block B = chan(cls, r', r)
+// is staged ONCE for all rows and the rows' W_j blocks side by side, so the
+// block is a (min, max) product of the stacked (row, xi) x r' operand with one
+// r' x r operand.  smem: B (j x (V-j)) then nrows A blocks (j x j each).
+__device__ __forceinline__ void expand_rows_cls(const pp_batch& b, const pp_instance& I, int j, int lp0, int nrows,
+                                                int cls, double* ex_smem) {
+    const int L = I.L, V = I.V;
+    const int nr = V - j;
+    const WsLayout lay = ws_layout(L, V);
+    double* ws = b.ws + I.ws_off;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+    const bool allow = I.flags & PP_ALLOW_REPLICATION;
+    double* B = ex_smem;              // [r'-1][r-1], stride nr
+    double* A0 = ex_smem + j * nr;    // row k: A0 + k j^2, [r'-1][xi'-1]
+    const double* Tj = ws + lay.chan + (int64_t)cls * tet(V) + chan_step(V, j);
+    for (int e = t; e < j * nr; e += blockDim.x) cp_async8(B + e, Tj + e);
+    cp_async_commit();
+    pdl_wait();
+    const double* Wsrc = ws + lay.W + W_idx(L, j, lp0, 1, 1);   // rows are consecutive j x j blocks
+    for (int rp = 1 + warp; rp <= j; rp += nw)
+        for (int xip = 1 + lane; xip <= j; xip += 32) {
+            const int e = (rp - 1) * j + (xip - 1);
+            if (W_structural(j, rp, xip, allow)) {
+                for (int k = 0; k < nrows; ++k) cp_async8(A0 + k * j * j + e, Wsrc + (int64_t)k * j * j + e);
+            } else {
+                for (int k = 0; k < nrows; ++k) A0[k * j * j + e] = PP_INF;
+            }
+        }
+    cp_async_commit();
+    __shared__ int64_t s_xb[SR_MAX];
+    for (int q = t; q < nr; q += blockDim.x) s_xb[q] = X_base(L, j + 1 + q, 1 + q);
+    cp_async_wait<0>();
+    __syncthreads();
+    pdl_trigger_at<1>();
+    constexpr int TRW = EXPAND_TRW;
+    const int ntx = (j + 3) >> 2, ntr = (nr + TRW - 1) / TRW, per_row = ntx * ntr, ntiles = nrows * per_row;
+    int ks = 1;
+    while (ks < 8 && ntiles * ks * 2 <= (int)blockDim.x) ks *= 2;
+    const int sub = t % ks;
+    const unsigned gmask = (ks == 32 ? 0xffffffffu : ((1u << ks) - 1u)) << (lane & ~(ks - 1));
+    double* X = ws + lay.X;
+    for (int id = t / ks; id < ntiles; id += blockDim.x / ks) {
+        const int k = id / per_row, rem = id - k * per_row;
+        const int tx = rem % ntx, tr = rem / ntx;
+        const int xi0 = 2 + 4 * tx, r0 = 1 + TRW * tr;
+        const int kend = j - xi0 + 2;
+        double acc[4][TRW];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < TRW; ++c) acc[a][c] = PP_INF;
+        const int xa[4] = {min(xi0 - 1, j) - 1, min(xi0, j) - 1, min(xi0 + 1, j) - 1, min(xi0 + 2, j) - 1};
+        int ra[TRW];
+#pragma unroll
+        for (int c = 0; c < TRW; ++c) ra[c] = min(r0 + c, nr) - 1;
+        const double* A = A0 + k * j * j;
+        for (int rp = 1 + sub; rp <= kend; rp += ks) {
+            const double* Ar = A + (rp - 1) * j;
+            const double* Br = B + (rp - 1) * nr;
+            double p[4], q[TRW];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) p[a] = Ar[xa[a]];
+#pragma unroll
+            for (int c = 0; c < TRW; ++c) q[c] = Br[ra[c]];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int c = 0; c < TRW; ++c) acc[a][c] = dmin(acc[a][c], dmax(p[a], q[c]));
+        }
+        for (int off = 1; off < ks; off <<= 1)
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int c = 0; c < TRW; ++c) acc[a][c] = dmin(acc[a][c], __shfl_xor_sync(gmask, acc[a][c], off));
+        if (sub != 0) continue;
+        const int lp = lp0 + k;
+#pragma unroll
+        for (int c = 0; c < TRW; ++c) {
+            const int r = r0 + c;
+            if (r > nr) continue;
+            double* Xr = X + s_xb[r - 1] + (int64_t)(lp - 1) * j;
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int xi = xi0 + a;
+                if (xi <= j + 1) Xr[xi - 2] = acc[a][c];
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
     const pp_instance I = b.inst[blockIdx.x];
     const int lp = blockIdx.y + 1;
@@ -854,7 +945,8 @@ __global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
     extern __shared__ __align__(16) double ex_smem[];
     expand_row_s(b, I, j, lp, 1, ex_smem);
 }
-__global__ void __launch_bounds__(256, EXPAND_TRW == 2 ? 2 : 2) k_expand_s_p(const pp_batch* __restrict__ bp, int j) {
+// one row l' per CTA (steps with few rows: every SM gets work)
+__global__ void __launch_bounds__(256, 2) k_expand_s_p(const pp_batch* __restrict__ bp, int j) {
     pdl_trigger_at<0>();
     StepTrace tr;
     tr.begin();
@@ -864,6 +956,33 @@ __global__ void __launch_bounds__(256, EXPAND_TRW == 2 ? 2 : 2) k_expand_s_p(con
     if (j >= I.V || lp > I.L - 1) return;
     extern __shared__ __align__(16) double ex_smem[];
     expand_row_s(b, I, j, lp, 1, ex_smem);
+    pdl_trigger_at<2>();
+    tr.end(1, j);
+}
+// rb rows per CTA (host: rb * j^2 + j (V-j) doubles of shared memory): rows of one
+// payload class share their chan block (expand_rows_cls), others go row by row.
+__global__ void __launch_bounds__(256, 2) k_expand_m_p(const pp_batch* __restrict__ bp, int j, int rb) {
+    pdl_trigger_at<0>();
+    StepTrace tr;
+    tr.begin();
+    const pp_batch b = *bp;
+    const pp_instance I = b.inst[blockIdx.x];
+    const int lp0 = blockIdx.y * rb + 1;
+    if (j >= I.V || lp0 > I.L - 1) return;
+    extern __shared__ __align__(16) double ex_smem[];
+    const int nrows = min(rb, I.L - lp0);
+    const int* rcls = reinterpret_cast<const int*>(b.ws + I.ws_off + ws_layout(I.L, I.V).chcls + CHAN_CLS);
+    int cls = rcls[lp0];
+    for (int k = 1; k < nrows && cls >= 0; ++k)
+        if (rcls[lp0 + k] != cls) cls = -1;
+    if (cls >= 0) {
+        expand_rows_cls(b, I, j, lp0, nrows, cls, ex_smem);
+    } else {
+        for (int k = 0; k < nrows; ++k) {
+            if (k) __syncthreads();   // the previous row's tiles are done with the shared operands
+            expand_row_s(b, I, j, lp0 + k, 1, ex_smem);
+        }
+    }
     pdl_trigger_at<2>();
     tr.end(1, j);
 }
