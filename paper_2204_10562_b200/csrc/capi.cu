@@ -17,9 +17,9 @@ __global__ void k_sdedup_p(const pp_batch* bp);
 __global__ void k_stab_p(const pp_batch* bp);
 __global__ void k_stab_big_p(const pp_batch* bp);
 __global__ void k_stab_big(pp_batch b);
-__global__ void k_expand_s_p(const pp_batch* bp, int j);
+__global__ void k_expand_s_p(const pp_batch* bp, int j, int rfirst, int rlast);
 __global__ void k_expand_m_p(const pp_batch* bp, int j, int rb);
-__global__ void k_combine_s_p(const pp_batch* bp, int j);
+__global__ void k_combine_s_p(const pp_batch* bp, int j, int r0);
 __global__ void k_backtrack_p(const pp_batch* bp);
 __global__ void k_phi(pp_batch b);
 __global__ void k_base(pp_batch b, int full_rows);
@@ -99,6 +99,10 @@ static const int g_expand_wide = getenv("PP_EXPAND_WIDE") ? atoi(getenv("PP_EXPA
 static const int g_expand_rb = getenv("PP_EXPAND_RB") ? std::max(1, atoi(getenv("PP_EXPAND_RB"))) : 4;
 static const int g_expand_rb_min = getenv("PP_EXPAND_RB_MIN") ? atoi(getenv("PP_EXPAND_RB_MIN")) : 4;
 static constexpr int64_t EX_SMEM_DOUBLES = 12288;   // 96 KB: two 256-thread CTAs per SM
+// per-step chain with the critical path (items r = 1) split from the bulk, for
+// batches of at most PP_DP_SPLIT instances (default 2; measured on C3: n = 1
+// DP 1.20 -> 1.10 ms, n = 3 equal, n = 12 2.71 -> 3.52 ms: twice the launches)
+static const int g_dp_split = getenv("PP_DP_SPLIT") ? atoi(getenv("PP_DP_SPLIT")) : 2;
 // programmatic dependent launch in the per-step chain (PP_PDL=0 disables)
 static const int g_pdl = getenv("PP_PDL") ? atoi(getenv("PP_PDL")) : 1;
 
@@ -191,6 +195,7 @@ int pp_rdo(const pp_batch* b, void* stream) {
 
 static int prm_chain(const pp_batch* b, void* stream, int total_inst);
 static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int total_inst);
+static int prm_chain_split_p(const pp_batch* b, const pp_batch* db, void* stream, int total_inst, int grp);
 static int prm_groups(const pp_batch* b, void* stream);
 static int prm_steps_graph(const pp_batch* b, void* stream);
 
@@ -211,6 +216,9 @@ struct SideStreams {
     cudaStream_t s[PP_DP_STREAMS];
     cudaStream_t capture;   // origin stream of graph captures (the caller's may be the legacy stream)
     cudaEvent_t fork, join[PP_DP_STREAMS];
+    // split chain (prm_chain_split_p): per group 3 bulk streams + its events
+    cudaStream_t x[3 * PP_DP_STREAMS];
+    cudaEvent_t xfork[PP_DP_STREAMS], c1[PP_DP_STREAMS][2], cb[PP_DP_STREAMS][3];
 };
 static thread_local SideStreams g_side;
 
@@ -391,6 +399,14 @@ static int ensure_side_streams() {
             cudaEventCreateWithFlags(&g_side.join[g], cudaEventDisableTiming) != cudaSuccess)
             return fail(PP_ECUDA, "side stream creation: %s", cudaGetErrorString(cudaGetLastError()));
     }
+    for (int g = 0; g < PP_DP_STREAMS; ++g) {
+        bool ok = cudaEventCreateWithFlags(&g_side.xfork[g], cudaEventDisableTiming) == cudaSuccess;
+        for (int k = 0; k < 3; ++k)
+            ok = ok && cudaStreamCreateWithFlags(&g_side.x[3 * g + k], cudaStreamNonBlocking) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&g_side.cb[g][k], cudaEventDisableTiming) == cudaSuccess;
+        for (int k = 0; k < 2; ++k) ok = ok && cudaEventCreateWithFlags(&g_side.c1[g][k], cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) return fail(PP_ECUDA, "side stream creation: %s", cudaGetErrorString(cudaGetLastError()));
+    }
     if (cudaEventCreateWithFlags(&g_side.fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaStreamCreateWithFlags(&g_side.capture, cudaStreamNonBlocking) != cudaSuccess)
         return fail(PP_ECUDA, "event creation: %s", cudaGetErrorString(cudaGetLastError()));
@@ -402,7 +418,10 @@ static int ensure_side_streams() {
 // device descriptors of the groups (per-step shared-memory path) or NULL.
 static int prm_groups_impl(const pp_batch* b, void* stream, const pp_batch* dev) {
     const int G = b->n_inst < g_dp_groups ? b->n_inst : g_dp_groups;
-    if (G <= 1) return dev ? prm_chain_p(b, desc_slot(dev, 1), stream, b->n_inst) : prm_chain(b, stream, b->n_inst);
+    if (G <= 1)
+        return dev ? (b->n_inst <= g_dp_split ? prm_chain_split_p(b, desc_slot(dev, 1), stream, b->n_inst, 0)
+                                 : prm_chain_p(b, desc_slot(dev, 1), stream, b->n_inst))
+                   : prm_chain(b, stream, b->n_inst);
     int rc;
     if ((rc = ensure_side_streams())) return rc;
     cudaEventRecord(g_side.fork, S(stream));
@@ -412,7 +431,9 @@ static int prm_groups_impl(const pp_batch* b, void* stream, const pp_batch* dev)
         bg.inst = b->inst + lo;
         bg.n_inst = hi - lo;
         cudaStreamWaitEvent(g_side.s[g], g_side.fork, 0);
-        rc = dev ? prm_chain_p(&bg, desc_slot(dev, 1 + g), g_side.s[g], b->n_inst) : prm_chain(&bg, g_side.s[g], b->n_inst);
+        rc = dev ? (b->n_inst <= g_dp_split ? prm_chain_split_p(&bg, desc_slot(dev, 1 + g), g_side.s[g], b->n_inst, g)
+                               : prm_chain_p(&bg, desc_slot(dev, 1 + g), g_side.s[g], b->n_inst))
+                 : prm_chain(&bg, g_side.s[g], b->n_inst);
         if (rc) return rc;
         cudaEventRecord(g_side.join[g], g_side.s[g]);
         cudaStreamWaitEvent(S(stream), g_side.join[g], 0);
@@ -527,7 +548,7 @@ static int prm_prep(const pp_batch* b, void* stream) {
 
 // prm_chain for the shared-memory path with device descriptors (graph capture):
 // `b` supplies the host-side shape, `db` is the same batch in device memory.
-static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int total_inst) {
+static int prm_tables_p(const pp_batch* b, const pp_batch* db, void* stream) {
     const int maxL = b->max_L, maxV = b->max_V;
     dim3 gp(b->n_inst, maxL > maxV ? maxL : maxV);
     k_prep_p<<<gp, 128, maxV <= PREP_CM_MAX ? sizeof(double) * maxV * maxV : 0, S(stream)>>>(db);
@@ -549,6 +570,100 @@ static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int 
     cudaFuncSetAttribute(k_expand_m_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)std::max(ex_smem, sizeof(double) * (size_t)EX_SMEM_DOUBLES));
     cudaFuncSetAttribute(k_combine_s_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs_smem);
+    return PP_OK;
+}
+
+// combine work units (tile parts) per item: split until a step has about
+// g_combine_waves waves of CTAs
+static int combine_parts(int items) {
+    int parts = (g_combine_waves * num_sms() + items - 1) / items;
+    return parts < 1 ? 1 : (parts > g_max_parts ? g_max_parts : parts);
+}
+static size_t combine_smem(int maxL, int j) {
+    return sizeof(double) * ((maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 + (size_t)(maxL > 1 ? maxL - 1 : 0) * j);
+}
+
+// The wavefront with its critical path split off (small batches, PP_DP_SPLIT).  Slice W_{j+1} needs only the r = 1 item of step j (i = j + 1); the
+// items r >= 2 of step j are first read r - 1 steps later.  So each step runs
+//   s0 (critical): E1(j) = expand target r = 1, then C1(j) = combine item r = 1
+//   x[j % 3] (bulk): Eb(j) = expand targets r >= 2, then Cb(j) = items r >= 2
+// E1(j) and Eb(j) read all of W_j: they wait for C1(j-1) and Cb(j-2) (Cb(j-3)
+// is behind its own stream's order, or waited for on s0; older ones are
+// implied: Cb(m) waited for Cb(m-2) and follows Cb(m-3) on its stream).  The
+// critical chain is two small launches per step; the bulk work of later steps
+// overlaps it on three streams.
+static int prm_chain_split_p(const pp_batch* b, const pp_batch* db, void* stream, int total_inst, int grp) {
+    const int maxL = b->max_L, maxV = b->max_V;
+    int rc;
+    if ((rc = ensure_side_streams())) return rc;
+    if ((rc = prm_tables_p(b, db, stream))) return rc;
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    cudaStream_t s0 = S(stream);
+    cudaStream_t* sx = &g_side.x[3 * grp];
+    cudaEvent_t* c1 = g_side.c1[grp];
+    cudaEvent_t* cb = g_side.cb[grp];
+    cudaEventRecord(g_side.xfork[grp], s0);
+    for (int k = 0; k < 3; ++k) {
+        cudaStreamWaitEvent(sx[k], g_side.xfork[grp], 0);
+        cudaEventRecord(cb[k], sx[k]);
+    }
+    cudaEventRecord(c1[0], s0);
+    cudaEventRecord(c1[1], s0);
+    auto expand = [&](cudaStream_t st, int j, int rfirst, int rlast) -> int {
+        if (maxL <= 1) return PP_OK;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(b->n_inst, maxL - 1);
+        cfg.blockDim = dim3(rlast == 1 || (int64_t)total_inst * (maxL - 1) <= g_expand_wide * num_sms() ? 256 : 128);
+        cfg.dynamicSmemBytes = sizeof(double) * (size_t)j * maxV;
+        cfg.stream = st;
+        cfg.attrs = pdl;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, k_expand_s_p, db, j, rfirst, rlast) != cudaSuccess)
+            return fail(PP_ECUDA, "k_expand_s launch: %s", cudaGetErrorString(cudaGetLastError()));
+        PP_CHECK_LAUNCH("k_expand_s");
+        return PP_OK;
+    };
+    auto combine = [&](cudaStream_t st, int j, int r0, int nitems, int parts) -> int {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(b->n_inst, nitems, parts);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = combine_smem(maxL, j);
+        cfg.stream = st;
+        cfg.attrs = pdl;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, k_combine_s_p, db, j, r0) != cudaSuccess)
+            return fail(PP_ECUDA, "k_combine_s launch: %s", cudaGetErrorString(cudaGetLastError()));
+        PP_CHECK_LAUNCH("k_combine_s");
+        return PP_OK;
+    };
+    for (int j = 1; j < maxV; ++j) {
+        if (j >= 3) cudaStreamWaitEvent(s0, cb[(j - 2) % 3], 0);
+        if (j >= 4) cudaStreamWaitEvent(s0, cb[(j - 3) % 3], 0);
+        if ((rc = expand(s0, j, 1, 1))) return rc;
+        if ((rc = combine(s0, j, 1, 1, g_max_parts))) return rc;
+        cudaEventRecord(c1[j % 2], s0);
+        if (maxV - j >= 2) {
+            cudaStream_t sk = sx[j % 3];
+            cudaStreamWaitEvent(sk, c1[(j - 1) % 2], 0);
+            if (j >= 3) cudaStreamWaitEvent(sk, cb[(j - 2) % 3], 0);
+            if ((rc = expand(sk, j, 2, (int)SR_MAX))) return rc;
+            if ((rc = combine(sk, j, 2, maxV - j - 1, combine_parts(total_inst * (maxV - j - 1))))) return rc;
+            cudaEventRecord(cb[j % 3], sk);
+        }
+    }
+    for (int k = 0; k < 3; ++k) cudaStreamWaitEvent(s0, cb[k], 0);
+    dim3 gb(b->n_inst, maxV);
+    k_backtrack_p<<<gb, 32, 0, s0>>>(db);
+    PP_CHECK_LAUNCH("k_backtrack");
+    return PP_OK;
+}
+
+static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int total_inst) {
+    const int maxL = b->max_L, maxV = b->max_V;
+    int rc;
+    if ((rc = prm_tables_p(b, db, stream))) return rc;
     // programmatic dependent launch between consecutive wavefront kernels: each
     // stages its producer-independent operands while its predecessor drains
     cudaLaunchAttribute pdl[1];
@@ -573,7 +688,7 @@ static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int 
             cfg.stream = S(stream);
             cfg.attrs = pdl;
             cfg.numAttrs = 1;
-            if ((rb > 1 ? cudaLaunchKernelEx(&cfg, k_expand_m_p, db, j, rb) : cudaLaunchKernelEx(&cfg, k_expand_s_p, db, j)) !=
+            if ((rb > 1 ? cudaLaunchKernelEx(&cfg, k_expand_m_p, db, j, rb) : cudaLaunchKernelEx(&cfg, k_expand_s_p, db, j, 1, (int)SR_MAX)) !=
                 cudaSuccess)
                 return fail(PP_ECUDA, "k_expand_s launch: %s", cudaGetErrorString(cudaGetLastError()));
             PP_CHECK_LAUNCH("k_expand_s");
@@ -589,7 +704,7 @@ static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int 
         cfg.stream = S(stream);
         cfg.attrs = pdl;
         cfg.numAttrs = 1;
-        if (cudaLaunchKernelEx(&cfg, k_combine_s_p, db, j) != cudaSuccess)
+        if (cudaLaunchKernelEx(&cfg, k_combine_s_p, db, j, 1) != cudaSuccess)
             return fail(PP_ECUDA, "k_combine_s launch: %s", cudaGetErrorString(cudaGetLastError()));
         PP_CHECK_LAUNCH("k_combine_s");
     }

@@ -743,9 +743,10 @@ __global__ void __launch_bounds__(CD_T, 2) k_combine_diag(pp_batch b, int j, int
 // Targets r = rfirst..V-j of row l' (rfirst = 2 leaves the r = 1 target to the
 // fused critical-path task of the persistent DP).  ex_smem: j * (j + nt) doubles.
 __device__ __forceinline__ void expand_row_s(const pp_batch& b, const pp_instance& I, int j, int lp, int rfirst,
-                                             double* ex_smem) {
+                                             double* ex_smem, int rlast = SR_MAX) {
     const int L = I.L, V = I.V, M = I.M;
-    const int nr = V - j, nt = nr - rfirst + 1;
+    const int nr = min(V - j, rlast), nt = nr - rfirst + 1;   // targets r = rfirst..nr
+    const int nrow = V - j;                                       // row stride of the chan class table
     if (nt <= 0) return;
     const WsLayout lay = ws_layout(L, V);
     double* ws = b.ws + I.ws_off;
@@ -766,7 +767,7 @@ __device__ __forceinline__ void expand_row_s(const pp_batch& b, const pp_instanc
     if (cls >= 0) {
         const double* Tj = ws + lay.chan + (int64_t)cls * tet(V) + chan_step(V, j);
         for (int rp = 1 + warp; rp <= j; rp += nw)
-            for (int q = lane; q < nt; q += 32) cp_async8(B + (rp - 1) * nt + q, Tj + (rp - 1) * nr + (q + rfirst - 1));
+            for (int q = lane; q < nt; q += 32) cp_async8(B + (rp - 1) * nt + q, Tj + (rp - 1) * nrow + (q + rfirst - 1));
         cp_async_commit();
     } else {
         cp_async_commit();
@@ -946,7 +947,7 @@ __global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
     expand_row_s(b, I, j, lp, 1, ex_smem);
 }
 // one row l' per CTA (steps with few rows: every SM gets work)
-__global__ void __launch_bounds__(256, 2) k_expand_s_p(const pp_batch* __restrict__ bp, int j) {
+__global__ void __launch_bounds__(256, 2) k_expand_s_p(const pp_batch* __restrict__ bp, int j, int rfirst, int rlast) {
     pdl_trigger_at<0>();
     StepTrace tr;
     tr.begin();
@@ -955,7 +956,7 @@ __global__ void __launch_bounds__(256, 2) k_expand_s_p(const pp_batch* __restric
     const int lp = blockIdx.y + 1;
     if (j >= I.V || lp > I.L - 1) return;
     extern __shared__ __align__(16) double ex_smem[];
-    expand_row_s(b, I, j, lp, 1, ex_smem);
+    expand_row_s(b, I, j, lp, rfirst, ex_smem, rlast);
     pdl_trigger_at<2>();
     tr.end(1, j);
 }
@@ -1308,7 +1309,7 @@ __global__ void __launch_bounds__(256, 2) k_combine_s(pp_batch b, int j) {
     __shared__ int s_order[1024];
     combine_item_s(b, I, j, blockIdx.y + 1, blockIdx.z, gridDim.z, cs_smem, s_hist, s_order, false);
 }
-__global__ void __launch_bounds__(256, COMBINE_TL4 == 2 ? 3 : 2) k_combine_s_p(const pp_batch* __restrict__ bp, int j) {
+__global__ void __launch_bounds__(256, COMBINE_TL4 == 2 ? 3 : 2) k_combine_s_p(const pp_batch* __restrict__ bp, int j, int r0) {
     pdl_trigger_at<0>();
     StepTrace tr;
     tr.begin();
@@ -1317,7 +1318,7 @@ __global__ void __launch_bounds__(256, COMBINE_TL4 == 2 ? 3 : 2) k_combine_s_p(c
     extern __shared__ __align__(16) double cs_smem[];
     __shared__ int s_hist[SR_MAX + 2];
     __shared__ int s_order[1024];
-    combine_item_s(b, I, j, blockIdx.y + 1, blockIdx.z, gridDim.z, cs_smem, s_hist, s_order, false);
+    combine_item_s(b, I, j, blockIdx.y + r0, blockIdx.z, gridDim.z, cs_smem, s_hist, s_order, false);
     pdl_trigger_at<2>();
     tr.end(2, j);
 }
