@@ -110,7 +110,7 @@ int pp_layout(int32_t n, const int32_t *L, const int32_t *V, const int32_t *M, c
 int pp_rdo(const pp_batch *b, void *stream);
 
 /* Number of speculative rounds pp_rdo runs before its sequential finisher
- * (default 2; 0 = the sequential recursion only).  The order is the
+ * (default 1; 0 = the sequential recursion only).  The order is the
  * reference's either way; this is a performance / test knob.  Returns the
  * previous value, or PP_EINVAL outside 0..64.  Process-wide. */
 int pp_rdo_set_rounds(int32_t rounds);

@@ -154,7 +154,7 @@ int pp_layout(int32_t n, const int32_t* L, const int32_t* V, const int32_t* M, c
 }
 
 // Speculative rounds before the sequential finisher (rdo.cu); 0 = sequential only.
-static std::atomic<int> g_rdo_rounds{2};
+static std::atomic<int> g_rdo_rounds{1};
 
 int pp_rdo_set_rounds(int32_t rounds) {
     if (rounds < 0 || rounds > 64) return fail(PP_EINVAL, "rdo rounds %d outside 0..64", rounds);

@@ -18,4 +18,4 @@ for n in [int(x) for x in sys.argv[1:]] or [12, 1]:
             a.record(); db.run("rdo"); b.record(); torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))
         print(f"n={n:3d} rounds={rounds}: rdo {min(ts):.3f} ms")
-    _lib.rdo_rounds(2)
+    _lib.rdo_rounds(1)
