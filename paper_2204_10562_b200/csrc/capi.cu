@@ -410,6 +410,10 @@ static int ensure_side_streams() {
     if (cudaEventCreateWithFlags(&g_side.fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaStreamCreateWithFlags(&g_side.capture, cudaStreamNonBlocking) != cudaSuccess)
         return fail(PP_ECUDA, "event creation: %s", cudaGetErrorString(cudaGetLastError()));
+    if (const char* e = getenv("PP_BULK")) {   // A/B knob: 0 stages the combine with per-element cp.async
+        const int v = atoi(e);
+        cudaMemcpyToSymbol(g_combine_bulk, &v, sizeof(v));
+    }
     g_side.dev = dev;
     return PP_OK;
 }
@@ -564,7 +568,7 @@ static int prm_tables_p(const pp_batch* b, const pp_batch* db, void* stream) {
         PP_CHECK_LAUNCH("k_stab");
     }
     const size_t ex_smem = sizeof(double) * (size_t)maxV * maxV;
-    const size_t cs_smem = sizeof(double) * ((maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 +
+    const size_t cs_smem = sizeof(double) * ((maxL + 1) / 2 + 3 + (size_t)(maxL - 1) * maxL / 2 +
                                              (size_t)(maxL > 1 ? maxL - 1 : 0) * maxV);
     cudaFuncSetAttribute(k_expand_s_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ex_smem);
     cudaFuncSetAttribute(k_expand_m_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -580,7 +584,7 @@ static int combine_parts(int items) {
     return parts < 1 ? 1 : (parts > g_max_parts ? g_max_parts : parts);
 }
 static size_t combine_smem(int maxL, int j) {
-    return sizeof(double) * ((maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 + (size_t)(maxL > 1 ? maxL - 1 : 0) * j);
+    return sizeof(double) * ((maxL + 1) / 2 + 3 + (size_t)(maxL - 1) * maxL / 2 + (size_t)(maxL > 1 ? maxL - 1 : 0) * j);
 }
 
 // The wavefront with its critical path split off (small batches, PP_DP_SPLIT).  Slice W_{j+1} needs only the r = 1 item of step j (i = j + 1); the
@@ -699,7 +703,7 @@ static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int 
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(b->n_inst, maxV - j, parts);
         cfg.blockDim = dim3(256);
-        cfg.dynamicSmemBytes = sizeof(double) * ((maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 +
+        cfg.dynamicSmemBytes = sizeof(double) * ((maxL + 1) / 2 + 3 + (size_t)(maxL - 1) * maxL / 2 +
                                                  (size_t)(maxL > 1 ? maxL - 1 : 0) * j);
         cfg.stream = S(stream);
         cfg.attrs = pdl;

@@ -481,6 +481,46 @@ __device__ __forceinline__ void cp_async8_hint(double* dst, const double* src, u
     asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "l"(pol) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+
+// TMA 1-D bulk copies (cp.async.bulk) completing on an mbarrier: one thread
+// moves a whole contiguous span, no per-element instructions.  Spans are split
+// into a 16-byte-aligned body (bulk) and at most one head / tail double (plain
+// loads); the shared destination is placed at the same 16-byte phase as the
+// source so the body is aligned on both sides.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(uint64_t* bar) {   // phase 0 (single-use barrier)
+    unsigned ok = 0;
+    while (!ok)
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(ok) : "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(double* dst, const double* src, unsigned bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ int dphase(const void* p) { return (int)((reinterpret_cast<uintptr_t>(p) >> 3) & 1); }
+// dst[e] = src[e] for e in [e0, e1): thread 0 issues the aligned body (arming
+// `bar` with its bytes, possibly 0), threads 0/1 copy the head / tail double.
+// dst and src must have the same 16-byte phase.
+__device__ __forceinline__ void stage_span(double* dst, const double* src, int e0, int e1, uint64_t* bar, uint64_t pol) {
+    const int n = e1 - e0;
+    const int head = n > 0 ? dphase(src + e0) : 0;
+    const int body = max(0, n - head) & ~1;
+    const int tail = max(0, n - head - body);
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(bar, 8u * body);
+        if (body) bulk_g2s(dst + e0 + head, src + e0 + head, 8u * body, bar, pol);
+        if (head) dst[e0] = src[e0];
+    }
+    if (threadIdx.x == 1 && tail) dst[e1 - 1] = src[e1 - 1];
+}
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
@@ -994,6 +1034,8 @@ __global__ void __launch_bounds__(256, 2) k_expand_m_p(const pp_batch* __restric
 // combine reads stage terms straight from global memory for j <= this (0 = always
 // stage them in shared memory; j <= 8 measured no better on B200)
 constexpr int S_DIRECT_J = 0;
+// k_combine_s_p stages with TMA bulk copies (pp_dp_set_bulk / PP_BULK; same bits)
+__device__ int g_combine_bulk = 1;
 #ifndef COMBINE_TL4
 #define COMBINE_TL4 2   // combine register tile 2 l x 4 xi (8 accumulators: 3 CTAs / SM)
 #endif
@@ -1255,7 +1297,8 @@ __device__ __forceinline__ void combine_tiles_s(double* Wi, int i, int r, int L,
 // smem: trio (L+1)/2+1, Stri (L-1)L/2, Xs (L-1) x j doubles; hist/order scratch.
 __device__ __forceinline__ void combine_item_s(const pp_batch& b, const pp_instance& I, int j, int r, int part,
                                                int nparts, double* cs_smem, int* s_hist, int* s_order,
-                                               bool x_staged, int lA = 1, int lB = PP_MAX_LAYERS, bool atomic = false) {
+                                               bool x_staged, int lA = 1, int lB = PP_MAX_LAYERS, bool atomic = false,
+                                               bool bulk = false) {
     const int L = I.L, V = I.V;
     if (j >= V || r > V - j) return;
     const int i = j + r;
@@ -1276,7 +1319,27 @@ __device__ __forceinline__ void combine_item_s(const pp_batch& b, const pp_insta
     const int la = max(lA, 1), lb = min(lB, L - 1);
     const double* Sg;
     const int slot = reinterpret_cast<const int*>(ws + lay.sidx)[(r - 1) * V + (i - 1)];
-    {
+    if (bulk) {
+        // TMA bulk path (one call per CTA): the triangle and X spans each one
+        // cp.async.bulk; shared bases shifted (1 spare double each) to the
+        // 16-byte phase of their global source
+        __shared__ uint64_t s_bar[2];
+        const int ns = (L - 1) * L / 2;
+        Sg = ws + lay.Stab + (int64_t)slot * ns;
+        const double* Xg = ws + lay.X + X_base(L, i, r);
+        Stri = cs_smem + (L + 1) / 2 + 1;
+        Stri += dphase(Stri) ^ dphase(Sg);
+        Xs = cs_smem + (L + 1) / 2 + 2 + ns;
+        Xs += dphase(Xs) ^ dphase(Xg);
+        if (t == 0) { mbar_init(&s_bar[0]); mbar_init(&s_bar[1]); }
+        __syncthreads();
+        const int s0 = (la - 1) * L - (la - 1) * la / 2, s1 = lb * L - lb * (lb + 1) / 2;
+        stage_span(Stri, Sg, s0, s1, &s_bar[0], l2_evict_last_policy());
+        pdl_wait();
+        stage_span(Xs, Xg, (la - 1) * j, lb * j, &s_bar[1], l2_evict_last_policy());
+        mbar_wait0(&s_bar[0]);
+        mbar_wait0(&s_bar[1]);
+    } else {
         // the stage-term triangle (built before the wavefront) first: under PDL it
         // overlaps the previous kernel's tail; X (this step's expand) after the wait
         const int ns = (L - 1) * L / 2;
@@ -1318,7 +1381,8 @@ __global__ void __launch_bounds__(256, COMBINE_TL4 == 2 ? 3 : 2) k_combine_s_p(c
     extern __shared__ __align__(16) double cs_smem[];
     __shared__ int s_hist[SR_MAX + 2];
     __shared__ int s_order[1024];
-    combine_item_s(b, I, j, blockIdx.y + r0, blockIdx.z, gridDim.z, cs_smem, s_hist, s_order, false);
+    combine_item_s(b, I, j, blockIdx.y + r0, blockIdx.z, gridDim.z, cs_smem, s_hist, s_order, false, 1, PP_MAX_LAYERS,
+                   false, g_combine_bulk);
     pdl_trigger_at<2>();
     tr.end(2, j);
 }
