@@ -1336,7 +1336,7 @@ __device__ __forceinline__ void combine_item_s(const pp_batch& b, const pp_insta
         const int s0 = (la - 1) * L - (la - 1) * la / 2, s1 = lb * L - lb * (lb + 1) / 2;
         stage_span(Stri, Sg, s0, s1, &s_bar[0], l2_evict_last_policy());
         pdl_wait();
-        stage_span(Xs, Xg, (la - 1) * j, lb * j, &s_bar[1], l2_evict_last_policy());
+        stage_span(Xs, Xg, (la - 1) * j, lb * j, &s_bar[1], l2_evict_normal_policy());
         mbar_wait0(&s_bar[0]);
         mbar_wait0(&s_bar[1]);
     } else {
