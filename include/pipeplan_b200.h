@@ -89,6 +89,8 @@ typedef struct {
      * reference's Schedule.events order (start, resource key, microbatch,
      * position; scheduler.py:227-231); NULL skips */
     int32_t *ev_order;
+    int32_t max_M;                    /* host copy: max microbatch count over the batch (0 = unknown;
+                                         sizes the event-order launch)                        */
 } pp_batch;
 
 /* ---- host helpers (no device work) ------------------------------------ */

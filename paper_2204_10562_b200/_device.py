@@ -182,6 +182,7 @@ class DeviceBatch:
         b.n_inst = n
         b.max_L = self.max_L
         b.max_V = self.max_V
+        b.max_M = int(Ms.max())
         fp = self.d_fin.data_ptr()
         b.inst = self.d_iin.data_ptr()
         b.fwd = fp

@@ -63,7 +63,8 @@ class PPBatch(C.Structure):
                 ("best_xi", C.c_void_p), ("best_mk", C.c_void_p), ("phi", C.c_void_p),
                 ("ev_start", C.c_void_p), ("ev_end", C.c_void_p),
                 ("ar_start", C.c_void_p), ("ar_end", C.c_void_p),
-                ("ws", C.c_void_p), ("gamma", C.c_void_p), ("ev_order", C.c_void_p)]
+                ("ws", C.c_void_p), ("gamma", C.c_void_p), ("ev_order", C.c_void_p),
+                ("max_M", C.c_int32)]
 
 
 class PPPlan(C.Structure):

@@ -811,11 +811,19 @@ int pp_select(const pp_batch* b, void* stream) {
         }
         PP_CHECK_LAUNCH("k_replay");
         if (b->ev_order) {
-            cudaFuncSetAttribute(k_event_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, EM_SMEM);
-            k_event_merge<<<b->n_inst, EM_T, EM_SMEM, S(stream)>>>(*b);
+            // events per plan <= max_M (4 max_V - 3): shared memory and block sized to
+            // it (small plans: several CTAs per SM); max_M = 0 (unknown) sizes for EM_MAXN
+            const int64_t nmax = b->max_M > 0 ? (int64_t)b->max_M * (4 * b->max_V - 3) : (int64_t)EM_MAXN + 1;
+            const int64_t nm = std::min<int64_t>(nmax, EM_MAXN);
+            const size_t smem = (size_t)(12 * nm + 16 + 15) & ~(size_t)15;
+            const int thr = nm <= 2048 ? 256 : (nm <= 8192 ? 512 : EM_T);
+            cudaFuncSetAttribute(k_event_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, EM_SMEM + 32);
+            k_event_merge<<<b->n_inst, thr, smem, S(stream)>>>(*b);
             PP_CHECK_LAUNCH("k_event_merge");
-            k_event_rank<<<dim3(b->n_inst, 16), 256, 0, S(stream)>>>(*b);
-            PP_CHECK_LAUNCH("k_event_rank");
+            if (nmax > EM_MAXN) {
+                k_event_rank<<<dim3(b->n_inst, 16), 256, 0, S(stream)>>>(*b);
+                PP_CHECK_LAUNCH("k_event_rank");
+            }
         }
     }
     return PP_OK;

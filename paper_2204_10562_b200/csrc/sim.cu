@@ -371,7 +371,8 @@ __device__ __forceinline__ uint64_t ev_tie(int N, int J, int e) {
 
 // k_event_merge: one CTA per instance, start times staged in shared memory, the
 // J runs merged pairwise (ceil(log2 J) levels, merge-path split per thread,
-// 16-bit event indices ping-ponged in shared memory).  n = M (4N-3) <= EM_MAXN.
+// 16-bit event indices ping-ponged in shared memory).  n = M (4N-3) <= EM_MAXN;
+// the host sizes shared memory and the block (<= EM_T) from the batch's max_M.
 constexpr int EM_T = 1024;
 constexpr int EM_SMEM = 216 * 1024;
 constexpr int EM_MAXN = EM_SMEM / 12 < 65536 ? EM_SMEM / 12 : 65536;
@@ -386,7 +387,8 @@ __global__ void __launch_bounds__(EM_T) k_event_merge(pp_batch b) {
     unsigned short* B = A + n;
     const double* st = b.ev_start + I.ev_off;
     const int t = threadIdx.x;
-    for (int k = t; k < n; k += EM_T) {
+    const int T = blockDim.x;
+    for (int k = t; k < n; k += T) {
         em_key[k] = st[k];
         const int q = k / M, m = k - q * M;   // run q = column q+1, in microbatch order
         A[k] = (unsigned short)(m * J + q);
@@ -396,7 +398,7 @@ __global__ void __launch_bounds__(EM_T) k_event_merge(pp_batch b) {
         const double u = em_key[x], v = em_key[y];
         return u != v ? u < v : ev_tie(N, J, x) < ev_tie(N, J, y);
     };
-    const int per = (n + EM_T - 1) / EM_T;
+    const int per = (n + T - 1) / T;
     for (int R = M; R < n; R *= 2) {
         int o = t * per;
         const int oend = min(n, o + per);
@@ -430,7 +432,7 @@ __global__ void __launch_bounds__(EM_T) k_event_merge(pp_batch b) {
         __syncthreads();
         unsigned short* T = A; A = B; B = T;
     }
-    for (int k = t; k < n; k += EM_T) b.ev_order[I.ev_off + k] = A[k];
+    for (int k = t; k < n; k += T) b.ev_order[I.ev_off + k] = A[k];
 }
 
 // k_event_rank: instances too large for k_event_merge.  One thread per event,
