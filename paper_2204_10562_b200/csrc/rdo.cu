@@ -79,6 +79,7 @@ __device__ __forceinline__ double warp_min_cut_t(double* wl, const double* bw, i
             for (int s = 0; s < SLOTS; ++s) side[s] = (grp[s] == tv);
         }
         const int merged = min(sv, tv), other = max(sv, tv);   // ordering.py:77-85
+        __syncwarp();   // every lane's reads of row nk precede the merge's writes
 #pragma unroll
         for (int s = 0; s < SLOTS; ++s) {
             const int u = lane + 32 * s;
@@ -394,6 +395,9 @@ __global__ void __launch_bounds__(32 * RDO_WARPS) k_rdo(pp_batch b, int resume) 
             int o = 0;
             for (int gi = 0; gi < ng; ++gi) { goff[gi] = o; const int c = cnt[glist[gi] - 1]; o += c * c; }
         }
+        // new labels go to `first` (free now) and are copied back after every
+        // group of this round is split: warps read lo while others relabel
+        for (int v = t; v < V; v += blockDim.x) first[v] = lo[v];
         __syncthreads();
         for (int gi = warp; gi < ng; gi += RDO_WARPS) {
             const int g = glist[gi];
@@ -414,10 +418,11 @@ __global__ void __launch_bounds__(32 * RDO_WARPS) k_rdo(pp_batch b, int resume) 
                 const int k = k0 + lane;
                 na += __popc(__ballot_sync(0xffffffffu, k < n && side[k]));
             }
-            for (int k = lane; k < n; k += 32) lo[mem[k]] = side[k] ? g : g + na;
+            for (int k = lane; k < n; k += 32) first[mem[k]] = side[k] ? g : g + na;
             __syncwarp();
         }
         __syncthreads();
+        for (int v = t; v < V; v += blockDim.x) lo[v] = first[v];   // same thread resets first[v] next round
     }
     int* order = b.order + I.order_off;
     for (int v = t; v < V; v += blockDim.x) order[lo[v] - 1] = v;
