@@ -270,7 +270,7 @@ __device__ void pe_simulate_warp(const P& p, const InstView& I, int N, int M, do
             const double left = q == 0 ? 0.0 : (s > 0 ? fe[s - 1] : fe_in);
             const double right = q + 1 >= R ? 0.0 : (s + 1 < S ? be[s + 1] : be_in);
             int m = pass - p1[s] + 1;
-            if (m >= 1 && m <= M) {
+            if ((unsigned)(m - 1) < (unsigned)M) {   // 1 <= m <= M
                 const double st = dmax(rf[s], from_left[s] ? left : right);
                 const double en = st + dB[s];   // B / FB / Y
                 rf[s] = en;
@@ -279,7 +279,7 @@ __device__ void pe_simulate_warp(const P& p, const InstView& I, int N, int M, do
             }
             if (p2[s]) {
                 m = pass - p2[s] + 1;
-                if (m >= 1 && m <= M) {
+                if ((unsigned)(m - 1) < (unsigned)M) {
                     const double st = dmax(rf[s], left);
                     const double en = st + dA[s];   // F / X
                     rf[s] = en;
