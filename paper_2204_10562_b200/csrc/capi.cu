@@ -103,6 +103,8 @@ static constexpr int64_t EX_SMEM_DOUBLES = 12288;   // 96 KB: two 256-thread CTA
 // batches of at most PP_DP_SPLIT instances (default 2; measured on C3: n = 1
 // DP 1.20 -> 1.10 ms, n = 3 equal, n = 12 2.71 -> 3.52 ms: twice the launches)
 static const int g_dp_split = getenv("PP_DP_SPLIT") ? atoi(getenv("PP_DP_SPLIT")) : 2;
+// CTAs (tile parts) of the critical item r = 1 in the split chain (PP_C1_PARTS env)
+static const int g_c1_parts = getenv("PP_C1_PARTS") ? std::max(1, std::min(64, atoi(getenv("PP_C1_PARTS")))) : 32;
 // programmatic dependent launch in the per-step chain (PP_PDL=0 disables)
 static const int g_pdl = getenv("PP_PDL") ? atoi(getenv("PP_PDL")) : 1;
 
@@ -646,7 +648,7 @@ static int prm_chain_split_p(const pp_batch* b, const pp_batch* db, void* stream
         if (j >= 3) cudaStreamWaitEvent(s0, cb[(j - 2) % 3], 0);
         if (j >= 4) cudaStreamWaitEvent(s0, cb[(j - 3) % 3], 0);
         if ((rc = expand(s0, j, 1, 1))) return rc;
-        if ((rc = combine(s0, j, 1, 1, g_max_parts))) return rc;
+        if ((rc = combine(s0, j, 1, 1, g_c1_parts))) return rc;
         cudaEventRecord(c1[j % 2], s0);
         if (maxV - j >= 2) {
             cudaStream_t sk = sx[j % 3];
