@@ -1,4 +1,7 @@
-for lib in main build/ab_tl4.so build/ab_trw4.so; do
+#!/bin/bash
+# Same-box A/B of the in-tree library against variant builds: tools/ab_quick.sh "<dp_ab args>" build/a.so ...
+args=$1; shift
+for lib in main "$@"; do
   if [ "$lib" = main ]; then unset PP_LIB_OVERRIDE; else export PP_LIB_OVERRIDE=$PWD/$lib; fi
-  echo "== $lib"; MODES=0 python tools/dp_ab.py 1 12 24 2>&1 | grep early_exit=True
+  echo "== $lib"; MODES=${MODES:-0} python tools/dp_ab.py $args 2>&1 | grep early_exit=True
 done
