@@ -574,7 +574,7 @@ static int prm_tables_p(const pp_batch* b, const pp_batch* db, void* stream) {
                                              (size_t)(maxL > 1 ? maxL - 1 : 0) * maxV);
     cudaFuncSetAttribute(k_expand_s_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ex_smem);
     cudaFuncSetAttribute(k_expand_m_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)std::max(ex_smem, sizeof(double) * (size_t)EX_SMEM_DOUBLES));
+                         (int)std::max(ex_smem, sizeof(double) * (size_t)(EX_SMEM_DOUBLES + 2)));
     cudaFuncSetAttribute(k_combine_s_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs_smem);
     return PP_OK;
 }
@@ -690,7 +690,7 @@ static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int 
             }
             cfg.gridDim = dim3(b->n_inst, ceil_div(maxL - 1, rb));
             cfg.blockDim = dim3(rb > 1 || rows <= g_expand_wide * num_sms() ? 256 : 128);
-            cfg.dynamicSmemBytes = sizeof(double) * std::max((size_t)j * maxV, (size_t)rb * j * j + (size_t)j * (maxV - j));
+            cfg.dynamicSmemBytes = sizeof(double) * (2 + std::max((size_t)j * maxV, (size_t)rb * j * j + (size_t)j * (maxV - j)));
             cfg.stream = S(stream);
             cfg.attrs = pdl;
             cfg.numAttrs = 1;

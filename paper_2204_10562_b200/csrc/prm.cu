@@ -901,26 +901,31 @@ __device__ __forceinline__ void expand_rows_cls(const pp_batch& b, const pp_inst
     double* ws = b.ws + I.ws_off;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
     const bool allow = I.flags & PP_ALLOW_REPLICATION;
-    double* B = ex_smem;              // [r'-1][r-1], stride nr
-    double* A0 = ex_smem + j * nr;    // row k: A0 + k j^2, [r'-1][xi'-1]
+    // TMA bulk: the chan block and the rows' W_j blocks (consecutive in W) are
+    // each one cp.async.bulk (2 spare doubles of shared memory for the 16-byte
+    // phase); the never-written structural cells are set to +inf afterwards
+    __shared__ uint64_t s_mbar[2];
     const double* Tj = ws + lay.chan + (int64_t)cls * tet(V) + chan_step(V, j);
-    for (int e = t; e < j * nr; e += blockDim.x) cp_async8(B + e, Tj + e);
-    cp_async_commit();
-    pdl_wait();
     const double* Wsrc = ws + lay.W + W_idx(L, j, lp0, 1, 1);   // rows are consecutive j x j blocks
-    for (int rp = 1 + warp; rp <= j; rp += nw)
-        for (int xip = 1 + lane; xip <= j; xip += 32) {
-            const int e = (rp - 1) * j + (xip - 1);
-            if (W_structural(j, rp, xip, allow)) {
-                for (int k = 0; k < nrows; ++k) cp_async8(A0 + k * j * j + e, Wsrc + (int64_t)k * j * j + e);
-            } else {
-                for (int k = 0; k < nrows; ++k) A0[k * j * j + e] = PP_INF;
-            }
-        }
-    cp_async_commit();
+    double* B = ex_smem + (dphase(ex_smem) ^ dphase(Tj));             // [r'-1][r-1], stride nr
+    double* A0 = ex_smem + 1 + j * nr;                                // row k: A0 + k j^2
+    A0 += dphase(A0) ^ dphase(Wsrc);
+    if (t == 0) { mbar_init(&s_mbar[0]); mbar_init(&s_mbar[1]); }
+    __syncthreads();
+    stage_span(B, Tj, 0, j * nr, &s_mbar[0], l2_evict_last_policy());
+    pdl_wait();
+    stage_span(A0, Wsrc, 0, nrows * j * j, &s_mbar[1], l2_evict_normal_policy());
     __shared__ int64_t s_xb[SR_MAX];
     for (int q = t; q < nr; q += blockDim.x) s_xb[q] = X_base(L, j + 1 + q, 1 + q);
-    cp_async_wait<0>();
+    mbar_wait0(&s_mbar[0]);
+    mbar_wait0(&s_mbar[1]);
+    __syncthreads();   // head / tail copies land before the +inf pass
+    for (int rp = 1 + warp; rp <= j; rp += nw)
+        for (int xip = 1 + lane; xip <= j; xip += 32)
+            if (!W_structural(j, rp, xip, allow)) {
+                const int e = (rp - 1) * j + (xip - 1);
+                for (int k = 0; k < nrows; ++k) A0[k * j * j + e] = PP_INF;
+            }
     __syncthreads();
     pdl_trigger_at<1>();
     constexpr int TRW = EXPAND_TRW;
