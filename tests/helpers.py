@@ -65,3 +65,25 @@ def block_labels(N):
         out[pos + 1] = (f"stage{n}", f"bwd{n}")
         pos += 2
     return out
+
+
+def oracle_spp_parallel(specs, threads=None):
+    """O.spp over fixture-style specs on a thread pool (the ctypes call
+    releases the GIL; the oracle has no global state).  Returns [(want, ids)]."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle as O
+    insts = [oracle_instance(s) for s in specs]
+    n = threads or max(1, min(len(insts), len(os.sched_getaffinity(0)), 32))
+    with ThreadPoolExecutor(n) as ex:
+        outs = list(ex.map(lambda t: O.spp(t[0]), insts))
+    return [(w, ids) for w, (_, ids) in zip(outs, insts)]
+
+
+def spec_from_workload(w):
+    """Fixture-style input dict (floats as hex) from a workloads.InstanceSpec."""
+    h = lambda xs: [float(x).hex() for x in xs]
+    return {"name": w.name, "fwd": h(w.fwd), "bwd": h(w.bwd), "param": h(w.param), "efwd": h(w.efwd),
+            "ebwd": h(w.ebwd), "gpu_ids": list(w.gpu_ids), "links": [[a, b, float(x).hex()] for a, b, x in w.links],
+            "M": w.M}

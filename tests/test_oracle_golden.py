@@ -97,7 +97,11 @@ def stall_message(res, names, M, N):
 
 
 def test_sim_golden():
-    for case in load("sim")["cases"]:
+    check_sim_cases(load("sim")["cases"])
+
+
+def check_sim_cases(cases):
+    for case in cases:
         inst, ids = oracle_instance(case["input"])
         pos = {g: k for k, g in enumerate(ids)}
         stages = [(a, b, tuple(pos[d] for d in devs)) for a, b, devs in case["plan"]["stages"]]
@@ -129,7 +133,18 @@ def check_spp(res, case, ids):
 
 
 def test_spp_golden():
-    for case in load("spp")["cases"]:
+    check_spp_cases(load("spp")["cases"])
+
+
+def test_edge_semantics_golden():
+    """-0.0 inputs and zero-duration blocks (tests/golden/edge.json)."""
+    data = load("edge")
+    check_spp_cases(data["spp"])
+    check_sim_cases(data["sim"])
+
+
+def check_spp_cases(cases):
+    for case in cases:
         inst, ids = oracle_instance(case["input"])
         res = O.spp(inst)
         check_spp(res, case, ids)
