@@ -1,0 +1,6 @@
+"""pipeplan.model → paper_2204_10562_b200.model (see pipeplan/__init__.py)."""
+import sys as _sys
+
+from paper_2204_10562_b200 import model as _m
+
+_sys.modules[__name__] = _m

@@ -168,6 +168,44 @@ def _check_costed_plan(plan: Plan, profile: ModelProfile, cluster: ClusterGraph)
                 raise ValidationError(f"unknown device {d}")
 
 
+def _stage_time(profile: ModelProfile, layer_start: int, layer_end: int, k, which: str) -> float:
+    """sum(layer times of [layer_start, layer_end]) / k (cost.py:44-61) on the
+    device cost pass: a one-stage plan on a k-GPU probe clique whose profile
+    keeps only the requested time column (``cyc = sf + sb`` with the other
+    sum exactly 0.0, so the record's cycle time IS ``sum / k`` bit for bit)."""
+    _check_interval(profile, layer_start, layer_end)
+    if k == 0:
+        raise ZeroDivisionError("float division by zero")
+    kk = abs(int(k))
+    keep_f, keep_b = which in ("f", "fb"), which in ("b", "fb")
+    layers = tuple(LayerProfile(l.id, l.fwd_time if keep_f else 0.0, l.bwd_time if keep_b else 0.0, 0.0)
+                   for l in profile.layers)
+    edges = tuple(InterLayerEdge(e.src, e.dst, 0.0, 0.0) for e in profile.edges)
+    probe = ModelProfile(profile.name, profile.microbatch_size, layers, edges)
+    ids = list(range(1, kk + 1))
+    clu = ClusterGraph(gpu_ids=tuple(ids), bandwidth={(a, b): 1.0 for a in ids for b in ids if a < b})
+    rec = _plan_costs([[(layer_start, layer_end, ids)]], probe, clu)[0]
+    v = float(rec["lane_cost"][0, _CYC])
+    return -v if k < 0 else v   # x / (-k) == -(x / k) in IEEE round-to-nearest
+
+
+def stage_fwd_time(profile: ModelProfile, layer_start: int, layer_end: int, k: int) -> float:
+    """Per-microbatch forward time of a stage on k replicas (cost.py:44-48), on the GPU."""
+    return _stage_time(profile, layer_start, layer_end, k, "f")
+
+
+def stage_bwd_time(profile: ModelProfile, layer_start: int, layer_end: int, k: int) -> float:
+    """Per-microbatch backward time of a stage on k replicas (cost.py:51-54), on the GPU."""
+    return _stage_time(profile, layer_start, layer_end, k, "b")
+
+
+def stage_compute_time(profile: ModelProfile, layer_start: int, layer_end: int, k: int) -> float:
+    """stage_fwd_time + stage_bwd_time (cost.py:56-61), on the GPU."""
+    if k < 1:
+        raise ValidationError("replication factor must be >= 1")
+    return _stage_time(profile, layer_start, layer_end, k, "fb")
+
+
 def cost_summary(plan: Plan, profile: ModelProfile, cluster: ClusterGraph) -> CostSummary:
     """Every planning-cost quantity of a plan (cost.py:172-202) from one device pass."""
     if not plan.stages:
@@ -237,3 +275,8 @@ def _gamma_phi(profile: ModelProfile, cluster: ClusterGraph) -> Tuple[float, flo
 def gamma(profile: ModelProfile, cluster: ClusterGraph) -> float:
     """sum(f + b over layers) / V (cost.py:126-128), on the GPU."""
     return _gamma_phi(profile, cluster)[0]
+
+
+def phi(profile: ModelProfile, cluster: ClusterGraph) -> float:
+    """cost.py:131-142 (also exported as planner.phi), evaluated on the GPU."""
+    return _gamma_phi(profile, cluster)[1]

@@ -188,3 +188,24 @@ def test_lazy_sweep_behaves_like_the_reference_tuple():
     assert lz[:2] == want[:2] and list(lz) == list(want) and hash(lz) == hash(want)
     assert lz == LazySweep([1, 0, 2], [1.5, 0.0, 2.5], [3.0, 0.0, 4.0], [5.0, 0.0, 6.0])
     assert lz != LazySweep([1, 0, 2], [1.5, 0.0, 2.5], [3.0, 0.0, 4.5], [5.0, 0.0, 6.0])
+
+
+def test_pipeplan_alias_exposes_the_reference_names():
+    """dropin/pipeplan: `import pipeplan` gives the drop-in with every public
+    name of the reference package (reference __init__.py:96-174)."""
+    import ast
+    import subprocess
+    import sys
+    ref_init = os.path.join(REPO, "baseline", "_ref", "pipeplan", "__init__.py")
+    if not os.path.isfile(ref_init):
+        pytest.skip("reference not staged under baseline/_ref")
+    tree = ast.parse(open(ref_init).read())
+    names = next(ast.literal_eval(n.value) for n in tree.body
+                 if isinstance(n, ast.Assign) and getattr(n.targets[0], "id", "") == "__all__")
+    env = dict(os.environ, PYTHONPATH=os.path.join(REPO, "dropin"))
+    code = ("import pipeplan, json, sys; from pipeplan.model import FWD; from pipeplan.cli import main; "
+            "import pipeplan.oracle as o; assert o.Plan is pipeplan.Plan; "
+            "print(json.dumps([n for n in sys.argv[1:] if not hasattr(pipeplan, n)]), pipeplan.IMPLEMENTATION)")
+    r = subprocess.run([sys.executable, "-c", code] + names, env=env, capture_output=True, text=True, cwd="/tmp")
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.split() == ["[]", "paper_2204_10562_b200"]
