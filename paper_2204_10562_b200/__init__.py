@@ -22,6 +22,8 @@ from .planner import BoundReport, SppResult, SweepEntry, bound_factor, phi, spp,
 from .scheduler import (ExecutionOrder, SchedulingError, build_block_list, compute_execution_order, lemma1_bound,
                         simulate_cycle_schedule, simulate_pe, simulate_pe_many, simulate_with_order)
 
+from .warm import warmup
+
 __version__ = "0.1.0"
 
 __all__ = [
@@ -37,4 +39,5 @@ __all__ = [
     "save_cluster", "save_plan", "save_profile", "trace_to_schedule", "write_trace",
     "CostSummary", "allreduce_time", "block_duration", "block_durations", "channel_times", "cost_summary", "gamma",
     "interstage_comm_time", "min_cross_bandwidth", "min_pairwise_bandwidth", "simulate_cycle_schedule", "validate_schedule",
+    "warmup",
 ]

@@ -38,7 +38,7 @@ def _cuda():
 
 def _env():
     env = dict(os.environ)
-    env["PYTHONPATH"] = os.pathsep.join([os.path.join(REPO, "dropin"), REPO] +
+    env["PYTHONPATH"] = os.pathsep.join([os.path.join(REPO, "dropin"), REPO, os.path.join(REPO, "tests")] +
                                         ([env["PYTHONPATH"]] if env.get("PYTHONPATH") else []))
     env["PYTHONDONTWRITEBYTECODE"] = "1"
     return env
@@ -52,7 +52,8 @@ def test_suite_imports_the_dropin(tmp_path):
 
 @pytest.mark.parametrize("module", MODULES)
 def test_reference_module_passes_on_dropin(module, tmp_path):
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider",
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-p", "refsuite_plugin",
+                        "--durations=5",
                         os.path.join(SUITE, module)], cwd=tmp_path, env=_env(), capture_output=True, text=True,
                        timeout=1800)
     tail = "\n".join(r.stdout.splitlines()[-30:])
