@@ -284,6 +284,14 @@ typedef struct {
     double *part;                     /* [3*M + N] per-microbatch partials scratch  */
     double *scal;                     /* [4] */
     int32_t *stat;                    /* [3] */
+    /* overlap-check sort scratch, needed only when 2*M > 8192 (the shared-memory
+     * sort's capacity): per resource lane sort_cap keys, i.e. (2N-1)*sort_cap
+     * doubles in each of sort_ks / sort_ke and int32 in sort_ki, sort_cap = the
+     * next power of two >= 2*M.  NULL / 0 otherwise. */
+    double *sort_ks;
+    double *sort_ke;
+    int32_t *sort_ki;
+    int64_t sort_cap;
 } pp_validate_args;
 
 int pp_validate_schedule(const pp_validate_args *a, int32_t phase, void *stream);

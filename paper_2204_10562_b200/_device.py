@@ -11,6 +11,8 @@ import ctypes as C
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
+import threading
+
 import numpy as np
 import torch
 
@@ -98,8 +100,15 @@ class _Staging:
     def __init__(self):
         self.buf = {}
         self.evt = {}
+        # fill + async copy + event record are one critical section: two threads
+        # planning concurrently must not refill a buffer whose copy is queued
+        self.lock = threading.Lock()
 
     def to_device(self, arr: np.ndarray, dev):
+        with self.lock:
+            return self._to_device(arr, dev)
+
+    def _to_device(self, arr: np.ndarray, dev):
         key = arr.dtype.str
         n = arr.size
         buf = self.buf.get(key)
@@ -276,7 +285,7 @@ class SimPlan:
 class SimRun:
     """Run pp_simulate for plans over a DeviceBatch's instances."""
 
-    def __init__(self, db: DeviceBatch, plans: Sequence[SimPlan], capture_events=True, costs=False):
+    def __init__(self, db: DeviceBatch, plans: Sequence[SimPlan], capture_events=True, costs=False, launch=True):
         lib = db.lib
         dev = db.d_fin.device
         n = len(plans)
@@ -352,7 +361,13 @@ class SimRun:
         self.n = n
         self.capture_events = capture_events
         self.costs = costs
-        _lib.check(lib.pp_simulate(C.byref(db.batch), C.byref(s), _stream()))
+        self.db = db
+        if launch:
+            self.launch()
+
+    def launch(self):
+        """(Re-)run pp_simulate over the uploaded plans on the current stream."""
+        _lib.check(self.db.lib.pp_simulate(C.byref(self.db.batch), C.byref(self.sim), _stream()))
 
     def fetch(self):
         f = self.d_f.cpu().numpy()

@@ -35,7 +35,8 @@ class PPValidateArgs(C.Structure):
                 ("slot_first", C.c_void_p), ("slot_last", C.c_void_p), ("slot_count", C.c_void_p),
                 ("ev_flags", C.c_void_p), ("slot_flags", C.c_void_p), ("mn_flags", C.c_void_p),
                 ("ar_flags", C.c_void_p), ("ov_flags", C.c_void_p), ("ov_idx", C.c_void_p),
-                ("res_off", C.c_void_p), ("part", C.c_void_p), ("scal", C.c_void_p), ("stat", C.c_void_p)]
+                ("res_off", C.c_void_p), ("part", C.c_void_p), ("scal", C.c_void_p), ("stat", C.c_void_p),
+                ("sort_ks", C.c_void_p), ("sort_ke", C.c_void_p), ("sort_ki", C.c_void_p), ("sort_cap", C.c_int64)]
 
 
 def _expected(N: int, merged: bool):
@@ -213,9 +214,11 @@ def validate_schedule(schedule: Schedule, plan: Plan, profile: ModelProfile, clu
         return problems
 
     # ---------------- phase 2 (scheduler.py:361-437)
-    if 2 * M > _VAL_SORT_MAX:
-        raise ValidationError(f"validate_schedule: {2 * M} events per resource exceed this build's capacity "
-                              f"{_VAL_SORT_MAX}")
+    if 2 * M > _VAL_SORT_MAX:   # global-memory sort scratch for the overlap check
+        cap = 1 << (2 * M - 1).bit_length()
+        lanes = 2 * N - 1
+        sk, se, si = f64(lanes * cap), f64(lanes * cap), i32(lanes * cap)
+        a.sort_ks, a.sort_ke, a.sort_ki, a.sort_cap = sk.data_ptr(), se.data_ptr(), si.data_ptr(), cap
     _lib.check(lib.pp_validate_schedule(C.byref(a), 2, stream))
     stat = out["stat"].cpu().numpy()
     scal = out["scal"].cpu().numpy()

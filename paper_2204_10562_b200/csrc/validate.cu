@@ -229,6 +229,56 @@ __global__ void __launch_bounds__(1024) k_val_overlap(pp_validate_args a) {
     }
 }
 
+// Large-M overlap check (2M > VAL_SORT_MAX): the same (start, end, event index)
+// order, bitonic-sorted in global scratch, one launch per (size, stride) pass
+// over all lanes at once; then the neighbour check.
+__global__ void k_val_ov_fill(pp_validate_args a) {
+    const ValLayout V(a);
+    const int lane = blockIdx.y, N = a.N, M = a.M;
+    const int n = lane / 2 + 1;
+    int es[2], ne = 0;
+    if ((lane & 1) == 0) {
+        es[ne++] = V.fwd(n);
+        if (!(V.merged && n == N)) es[ne++] = V.bwd(n);
+    } else { es[ne++] = V.cf(n); es[ne++] = V.cb(n); }
+    const int64_t cnt = (int64_t)ne * M, P2 = a.sort_cap, base = (int64_t)lane * P2;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < P2; j += (int64_t)gridDim.x * blockDim.x) {
+        if (j < cnt) {
+            const int e = es[j / M], m = (int)(j % M) + 1;
+            const int k = a.slot_last[(int64_t)(m - 1) * a.n_exp + e];
+            a.sort_ks[base + j] = a.ev_start[k]; a.sort_ke[base + j] = a.ev_end[k]; a.sort_ki[base + j] = k;
+        } else { a.sort_ks[base + j] = PP_INF; a.sort_ke[base + j] = PP_INF; a.sort_ki[base + j] = INT_MAX; }
+    }
+}
+__global__ void k_val_ov_pass(pp_validate_args a, int64_t size, int64_t stride) {
+    const int64_t P2 = a.sort_cap, base = (int64_t)blockIdx.y * P2;
+    double* ks = a.sort_ks + base;
+    double* ke = a.sort_ke + base;
+    int32_t* ki = a.sort_ki + base;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < P2; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = j ^ stride;
+        if (p > j) {
+            const bool up = (j & size) == 0;
+            const bool gt = ks[j] > ks[p] || (ks[j] == ks[p] && (ke[j] > ke[p] || (ke[j] == ke[p] && ki[j] > ki[p])));
+            if (gt == up) {
+                double t = ks[j]; ks[j] = ks[p]; ks[p] = t;
+                t = ke[j]; ke[j] = ke[p]; ke[p] = t;
+                const int32_t u = ki[j]; ki[j] = ki[p]; ki[p] = u;
+            }
+        }
+    }
+}
+__global__ void k_val_ov_check(pp_validate_args a) {
+    const int lane = blockIdx.y, N = a.N, M = a.M;
+    const int ne = ((lane & 1) == 0 && a.flags & 1 && lane / 2 + 1 == N) ? 1 : 2;
+    const int64_t cnt = (int64_t)ne * M, base = (int64_t)lane * a.sort_cap, off = a.res_off[lane];
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cnt; j += (int64_t)gridDim.x * blockDim.x) {
+        a.ov_idx[off + j] = a.sort_ki[base + j];
+        a.ov_flags[off + j] = (j > 0 && a.sort_ks[base + j] < a.sort_ke[base + j - 1] - vtol1(a.sort_ke[base + j - 1]))
+                                  ? 1 : 0;
+    }
+}
+
 }  // namespace pp
 
 extern "C" int pp_validate_schedule(const pp_validate_args* a, int32_t phase, void* stream) {
@@ -250,13 +300,28 @@ extern "C" int pp_validate_schedule(const pp_validate_args* a, int32_t phase, vo
         PP_CHECK_LAUNCH("k_val_slots");
         return PP_OK;
     }
-    if (2 * a->M > VAL_SORT_MAX)
-        return fail(PP_EINVAL, "validate: %d events per resource exceed this build's sort capacity %d", 2 * a->M,
-                    VAL_SORT_MAX);
+    int64_t P2g = 1;
+    while (P2g < 2 * (int64_t)a->M) P2g <<= 1;
+    if (2 * a->M > VAL_SORT_MAX && (!a->sort_ks || !a->sort_ke || !a->sort_ki || a->sort_cap < P2g))
+        return fail(PP_EINVAL, "validate: %d events per resource need sort scratch of %lld keys per lane", 2 * a->M,
+                    (long long)P2g);
     k_val_order<<<(a->M + 127) / 128, 128, 0, st>>>(*a);
     PP_CHECK_LAUNCH("k_val_order");
     k_val_final<<<1, 256, 0, st>>>(*a);
     PP_CHECK_LAUNCH("k_val_final");
+    if (2 * a->M > VAL_SORT_MAX) {
+        const dim3 g((unsigned)std::min<int64_t>((a->sort_cap + 255) / 256, 1024), 2 * a->N - 1);
+        k_val_ov_fill<<<g, 256, 0, st>>>(*a);
+        PP_CHECK_LAUNCH("k_val_ov_fill");
+        for (int64_t size = 2; size <= a->sort_cap; size <<= 1)
+            for (int64_t stride = size >> 1; stride > 0; stride >>= 1) {
+                k_val_ov_pass<<<g, 256, 0, st>>>(*a, size, stride);
+                PP_CHECK_LAUNCH("k_val_ov_pass");
+            }
+        k_val_ov_check<<<g, 256, 0, st>>>(*a);
+        PP_CHECK_LAUNCH("k_val_ov_check");
+        return PP_OK;
+    }
     int P2 = 1;
     while (P2 < 2 * a->M) P2 <<= 1;
     const size_t smem = (size_t)P2 * (2 * sizeof(double) + sizeof(int));

@@ -224,12 +224,18 @@ def simulate_with_order(plan: Plan, profile: ModelProfile, cluster: ClusterGraph
     for r, q in enumerate(lists):
         for k, item in enumerate(q):
             mm, pp = int(item[0]), int(item[1])
-            if not (1 <= mm <= M and 1 <= pp <= J):
-                raise ValidationError(f"queue item {item} outside microbatches 1..{M} / positions 1..{J}")
+            # Malformed queues: the reference looks the
+            # position up in its block dict (KeyError, scheduler.py:167) and
+            # plays the rest out as given; here they are rejected up front
+            # with the reference's simulation error class.
+            if not 1 <= pp <= J:
+                raise KeyError(pp)
+            if not 1 <= mm <= M:
+                raise SchedulingError(f"queue item {item} outside microbatches 1..{M}")
             if _pos_lane(N, pp) != r:
-                raise ValidationError(f"queue item {item} is not a block of resource {names[r]}")
+                raise SchedulingError(f"queue item {item} is not a block of resource {names[r]}")
             if (mm, pp) in seen:
-                raise ValidationError(f"queue item {item} appears twice")
+                raise SchedulingError(f"queue item {item} appears twice")
             seen.add((mm, pp))
             qidx[(mm - 1) * J + pp - 1] = k
     rec = _sim(plan, profile, cluster, lists, forward_barrier)

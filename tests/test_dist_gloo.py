@@ -53,6 +53,44 @@ def test_sharded_min_loc_world2():
         assert got == (3.0, 2, 3)
 
 
+def _worker_uneven(rank, world, port, n, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mine = shard(n, rank, world)
+        mk = [float((7 * k) % 5) + (0.5 if k % 3 else 0.0) for k in range(n)]
+        xi = [1 + (k * 5) % 4 for k in range(n)]
+        got = global_best([mk[k] for k in mine], [xi[k] for k in mine], mine)
+        q.put((rank, mine, got))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [10, 2, 0])
+def test_uneven_and_empty_shards_world3(n):
+    """10 items over 3 ranks (4/3/3), 2 items (one rank empty), 0 items (all
+    empty): counts are gathered first and short shards padded with +inf rows."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_uneven, args=(r, 3, port, n, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    shards = {r: m for r, m, _ in res}
+    assert sorted(sum(shards.values(), [])) == list(range(n))
+    mk = [float((7 * k) % 5) + (0.5 if k % 3 else 0.0) for k in range(n)]
+    xi = [1 + (k * 5) % 4 for k in range(n)]
+    want = min_loc(np.array([[mk[k], xi[k], k] for k in range(n)])) if n else None
+    for _, _, got in res:
+        assert got == want
+
+
 def test_min_loc_single_process():
+    assert min_loc(np.zeros((0, 3))) is None
+    assert global_best([], [], []) is None
     assert min_loc(np.array([[2.0, 3, 0], [2.0, 1, 5], [1.5, 9, 2]])) == (1.5, 9, 2)
     assert global_best([1.0, 1.0], [2, 2], [7, 3]) == (1.0, 2, 3)

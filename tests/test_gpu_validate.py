@@ -65,3 +65,34 @@ def test_spp_schedules_validate_at_scale():
         r = P.spp(prof, clu, M)
         assert P.validate_schedule(r.schedule, r.plan, prof, clu) == []
         assert r.makespan <= P.lemma1_bound(r.plan, prof, clu) * (1 + 1e-12)
+
+
+def test_large_m_overlap_check_uses_global_sort():
+    """2M > 8192 events per resource: the overlap check sorts in global
+    scratch (k_val_ov_*).  Clean PE schedule -> []; the same schedule with one
+    stage-1 forward moved onto its predecessor's interval -> the overlap (and
+    the dependency messages it causes) are reported, exactly as for a
+    shared-memory-sized M with the same corruption."""
+    import dataclasses
+
+    def corrupt(sched, M):
+        evs = list(sched.events)
+        k1 = next(k for k, e in enumerate(evs) if e.resource == "stage1" and e.block == "fwd1" and e.microbatch == 3)
+        k0 = next(k for k, e in enumerate(evs) if e.resource == "stage1" and e.block == "fwd1" and e.microbatch == 2)
+        d = evs[k1].end - evs[k1].start
+        evs[k1] = dataclasses.replace(evs[k1], start=evs[k0].start, end=evs[k0].start + d)
+        return P.Schedule(events=tuple(evs), allreduce=sched.allreduce, makespan=sched.makespan)
+
+    layers = tuple(P.LayerProfile(k, 1.0, 2.0, 1e8) for k in (1, 2, 3))
+    edges = (P.InterLayerEdge(1, 2, 1e8, 1e8), P.InterLayerEdge(2, 3, 1e8, 1e8))
+    prof = P.ModelProfile("bigM", 1, layers, edges)
+    clu = P.make_cluster([1, 2, 3], [(1, 2, 1e9), (1, 3, 1e9), (2, 3, 1e9)])
+    msgs = {}
+    for M in (64, 5000):
+        plan = P.Plan((P.Stage(1, 1, 1, (1,)), P.Stage(2, 2, 3, (2, 3))), M)
+        s = P.simulate_pe(plan, prof, clu)
+        assert P.validate_schedule(s, plan, prof, clu) == []
+        msgs[M] = P.validate_schedule(corrupt(s, M), plan, prof, clu)
+        assert any(m.startswith("overlap on stage1: (2,fwd1) and (3,fwd1)") or
+                   m.startswith("overlap on stage1: (3,fwd1) and (2,fwd1)") for m in msgs[M]), msgs[M]
+    assert msgs[64] == msgs[5000]
