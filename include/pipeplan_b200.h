@@ -139,6 +139,12 @@ int pp_dp_set_persistent(int32_t mode);
  * Returns the previous value (needs a device: the flag is device state). */
 int pp_dp_set_early_exit(int32_t on);
 
+/* Combine kernel of the per-step DP schedule: 1 (default) = crossing search
+ * (combine_bis.cu: bisection for the valley of max(X, S) under certified
+ * monotonicity, exhaustive fold otherwise), 0 = exhaustive register tiles.
+ * Identical results; a performance / test knob.  Returns the previous kind. */
+int pp_dp_set_combine(int32_t kind);
+
 /* Debug: record the persistent DP's per-task timeline (4 x u64 per task:
  * smid << 32 | kind, fetch, inputs-ready, end; globaltimer ns) into the device
  * buffer d_buf of 4 * cap entries; NULL disables.  Not on the planning path. */

@@ -88,7 +88,7 @@ EXPORTS = ("pp_version", "pp_last_error", "pp_device_count", "pp_layout", "pp_rd
            "pp_pe_sweep", "pp_select", "pp_spp", "pp_prm_query", "pp_simulate", "pp_min_cut",
            "pp_launch_count", "pp_phi", "pp_peak_minmax", "pp_format_trace", "pp_validate_schedule",
            "pp_rdo_set_rounds", "pp_dp_set_persistent", "pp_dp_trace",
-           "pp_dp_set_early_exit", "pp_step_trace")
+           "pp_dp_set_early_exit", "pp_step_trace", "pp_dp_set_combine")
 
 _lib = None
 
@@ -140,6 +140,8 @@ def _declare(L):
     L.pp_dp_set_persistent.restype = C.c_int
     L.pp_dp_set_early_exit.argtypes = [i32]
     L.pp_dp_set_early_exit.restype = C.c_int
+    L.pp_dp_set_combine.argtypes = [i32]
+    L.pp_dp_set_combine.restype = C.c_int
     L.pp_step_trace.argtypes = [vp, i32]
     L.pp_step_trace.restype = C.c_int
     L.pp_dp_trace.argtypes = [vp, i32]
@@ -159,6 +161,12 @@ def dp_early_exit(on: bool) -> bool:
     if prev < 0:
         check(prev)
     return bool(prev)
+
+
+def dp_combine(kind: int) -> int:
+    """Per-step combine kernel: 1 crossing search (default), 0 exhaustive
+    register tiles.  Returns the previous kind; results are identical."""
+    return int(load(require_device=False).pp_dp_set_combine(int(kind)))
 
 
 def rdo_rounds(rounds: int) -> int:

@@ -20,6 +20,7 @@ __global__ void k_stab_big(pp_batch b);
 __global__ void k_expand_s_p(const pp_batch* bp, int j, int rfirst, int rlast);
 __global__ void k_expand_m_p(const pp_batch* bp, int j, int rb);
 __global__ void k_combine_s_p(const pp_batch* bp, int j, int r0);
+__global__ void k_combine_bis_p(const pp_batch* bp, int j, int r0);
 __global__ void k_backtrack_p(const pp_batch* bp);
 __global__ void k_phi(pp_batch b);
 __global__ void k_base(pp_batch b, int full_rows);
@@ -107,6 +108,9 @@ static const int g_dp_split = getenv("PP_DP_SPLIT") ? atoi(getenv("PP_DP_SPLIT")
 static const int g_c1_parts = getenv("PP_C1_PARTS") ? std::max(1, std::min(64, atoi(getenv("PP_C1_PARTS")))) : 32;
 // programmatic dependent launch in the per-step chain (PP_PDL=0 disables)
 static const int g_pdl = getenv("PP_PDL") ? atoi(getenv("PP_PDL")) : 1;
+// combine kernel of the per-step schedule: 1 = crossing search (combine_bis.cu),
+// 0 = exhaustive register tiles (k_combine_s_p); same bits either way
+static std::atomic<int> g_combine_kind{getenv("PP_COMBINE_BIS") ? atoi(getenv("PP_COMBINE_BIS")) : 1};
 
 static int num_sms() {
     static thread_local int dev = -1, sms = 148;
@@ -316,6 +320,8 @@ static int prm_inst(const pp_batch* b, void* stream) {
     return PP_OK;
 }
 
+int pp_dp_set_combine(int32_t kind) { return g_combine_kind.exchange(kind ? 1 : 0); }
+
 int pp_dp_set_early_exit(int32_t on) {
     int prev = 1, v = on ? 1 : 0;
     if (cudaMemcpyFromSymbol(&prev, g_combine_early_exit, sizeof(int)) != cudaSuccess ||
@@ -455,9 +461,10 @@ static int prm_groups(const pp_batch* b, void* stream) { return prm_groups_impl(
 // from a small library-owned device buffer of the cache entry (rewritten, stream
 // ordered, before every replay), so any workspace / buffers of that shape replay.
 struct GraphKey {   // what the captured launches bake in: grid shapes (descriptors live in the entry)
-    int n_inst, max_L, max_V, G, dev;
+    int n_inst, max_L, max_V, G, dev, combine;
     bool operator==(const GraphKey& o) const {
-        return n_inst == o.n_inst && max_L == o.max_L && max_V == o.max_V && G == o.G && dev == o.dev;
+        return n_inst == o.n_inst && max_L == o.max_L && max_V == o.max_V && G == o.G && dev == o.dev &&
+               combine == o.combine;
     }
 };
 struct GraphEntry {
@@ -484,7 +491,7 @@ static int prm_steps_graph(const pp_batch* b, void* stream) {
     }
     int d = 0;
     cudaGetDevice(&d);
-    const GraphKey key{b->n_inst, b->max_L, b->max_V, G, d};
+    const GraphKey key{b->n_inst, b->max_L, b->max_V, G, d, g_combine_kind.load()};
     GraphEntry* ent = nullptr;
     for (size_t k = 0; k < g_graphs.size(); ++k)
         if (g_graphs[k].key == key) { ent = &g_graphs[k]; break; }
@@ -576,6 +583,33 @@ static int prm_tables_p(const pp_batch* b, const pp_batch* db, void* stream) {
     cudaFuncSetAttribute(k_expand_m_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)std::max(ex_smem, sizeof(double) * (size_t)(EX_SMEM_DOUBLES + 2)));
     cudaFuncSetAttribute(k_combine_s_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs_smem);
+    cudaFuncSetAttribute(k_combine_bis_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double) * ((size_t)(maxL - 1) * maxL / 2 + (size_t)(maxL > 1 ? maxL - 1 : 0) * maxV + 4)));
+    return PP_OK;
+}
+
+// one combine launch of the per-step schedule: items r0 .. r0 + nitems - 1 of step j
+static int launch_combine(const pp_batch* b, const pp_batch* db, cudaStream_t st, cudaLaunchAttribute* attrs, int j,
+                          int r0, int nitems, int parts) {
+    const int maxL = b->max_L;
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    cudaError_t e;
+    if (g_combine_kind == 1) {
+        cfg.gridDim = dim3(b->n_inst, nitems, 1);
+        cfg.dynamicSmemBytes = sizeof(double) * ((size_t)(maxL - 1) * maxL / 2 + (size_t)(maxL > 1 ? maxL - 1 : 0) * j + 4);
+        e = cudaLaunchKernelEx(&cfg, k_combine_bis_p, db, j, r0);
+    } else {
+        cfg.gridDim = dim3(b->n_inst, nitems, parts);
+        cfg.dynamicSmemBytes = sizeof(double) * ((maxL + 1) / 2 + 3 + (size_t)(maxL - 1) * maxL / 2 +
+                                                 (size_t)(maxL > 1 ? maxL - 1 : 0) * j);
+        e = cudaLaunchKernelEx(&cfg, k_combine_s_p, db, j, r0);
+    }
+    if (e != cudaSuccess) return fail(PP_ECUDA, "combine launch: %s", cudaGetErrorString(cudaGetLastError()));
+    PP_CHECK_LAUNCH("k_combine");
     return PP_OK;
 }
 
@@ -632,17 +666,7 @@ static int prm_chain_split_p(const pp_batch* b, const pp_batch* db, void* stream
         return PP_OK;
     };
     auto combine = [&](cudaStream_t st, int j, int r0, int nitems, int parts) -> int {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(b->n_inst, nitems, parts);
-        cfg.blockDim = dim3(256);
-        cfg.dynamicSmemBytes = combine_smem(maxL, j);
-        cfg.stream = st;
-        cfg.attrs = pdl;
-        cfg.numAttrs = 1;
-        if (cudaLaunchKernelEx(&cfg, k_combine_s_p, db, j, r0) != cudaSuccess)
-            return fail(PP_ECUDA, "k_combine_s launch: %s", cudaGetErrorString(cudaGetLastError()));
-        PP_CHECK_LAUNCH("k_combine_s");
-        return PP_OK;
+        return launch_combine(b, db, st, pdl, j, r0, nitems, parts);
     };
     for (int j = 1; j < maxV; ++j) {
         if (j >= 3) cudaStreamWaitEvent(s0, cb[(j - 2) % 3], 0);
@@ -699,20 +723,8 @@ static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int 
                 return fail(PP_ECUDA, "k_expand_s launch: %s", cudaGetErrorString(cudaGetLastError()));
             PP_CHECK_LAUNCH("k_expand_s");
         }
-        const int items = total_inst * (maxV - j);
-        int parts = (g_combine_waves * num_sms() + items - 1) / items;
-        parts = parts < 1 ? 1 : (parts > g_max_parts ? g_max_parts : parts);
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(b->n_inst, maxV - j, parts);
-        cfg.blockDim = dim3(256);
-        cfg.dynamicSmemBytes = sizeof(double) * ((maxL + 1) / 2 + 3 + (size_t)(maxL - 1) * maxL / 2 +
-                                                 (size_t)(maxL > 1 ? maxL - 1 : 0) * j);
-        cfg.stream = S(stream);
-        cfg.attrs = pdl;
-        cfg.numAttrs = 1;
-        if (cudaLaunchKernelEx(&cfg, k_combine_s_p, db, j, 1) != cudaSuccess)
-            return fail(PP_ECUDA, "k_combine_s launch: %s", cudaGetErrorString(cudaGetLastError()));
-        PP_CHECK_LAUNCH("k_combine_s");
+        if ((rc = launch_combine(b, db, S(stream), pdl, j, 1, maxV - j, combine_parts(total_inst * (maxV - j)))))
+            return rc;
     }
     dim3 gb(b->n_inst, maxV);
     k_backtrack_p<<<gb, 32, 0, S(stream)>>>(db);

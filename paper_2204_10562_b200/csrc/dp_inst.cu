@@ -35,7 +35,7 @@ __device__ __forceinline__ void dp_inst_combine(const pp_batch& b, const pp_inst
         const double* Stri = smem + (int64_t)q * per_item;
         const double* Xs = Stri + tri;
         const int slot = reinterpret_cast<const int*>(ws + lay.sidx)[(r - 1) * V + (i - 1)];
-        const bool mono = g_combine_early_exit && reinterpret_cast<const int*>(ws + lay.smono)[slot];
+        const bool mono = g_combine_early_exit && (reinterpret_cast<const int*>(ws + lay.smono)[slot] & 1);
         double acc[TL][TX];
         if (mono) combine_tile_s_desc<TX, TL>(Stri, trio, Xs, L, j, l0, xi0, 1, L - 1, acc);
         else combine_tile_s<TX, TL>(Stri, trio, Xs, L, j, l0, xi0, 1, L - 1, acc);

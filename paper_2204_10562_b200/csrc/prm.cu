@@ -333,26 +333,33 @@ __device__ __forceinline__ void stab_fill(const pp_batch& b, const pp_instance& 
             st_evict_last(out + off + (l - lp - 1), sv, pol);
         }
     }
-    // Is the triangle non-increasing in l' (S(l', l) >= S(l'+1, l) for every l)?
-    // In exact arithmetic it is (span and parameter sums shrink as the stage
-    // loses layers); the flag certifies it for these rounded values, and only a
-    // certified triangle lets the combine stop scanning l' early.
+    // Is the triangle non-increasing in l' (S(l', l) >= S(l'+1, l) for every l;
+    // bit 0) and non-decreasing in l (S(l', l) <= S(l', l+1); bit 1)?  In exact
+    // arithmetic it is both (the stage loses layers as l' grows and gains them
+    // as l grows); the flags certify it for these rounded values.  Bit 0 lets
+    // the combine stop scanning l' early and bisect for the crossing; bit 1
+    // lets the bisection of cell l start from cell l-1's crossing.
     if (nw == 1) __syncwarp();
     else __syncthreads();
-    bool bad = false;
-    for (int lp = 1 + warp; lp + 1 < L; lp += nw) {
+    bool bad = false, bad_l = false;
+    for (int lp = 1 + warp; lp < L; lp += nw) {
         const int o0 = (lp - 1) * L - (lp - 1) * lp / 2, o1 = lp * L - lp * (lp + 1) / 2;
-        for (int l = lp + 2 + lane; l <= L; l += 32)
-            bad |= !(out[o0 + (l - lp - 1)] >= out[o1 + (l - lp - 2)]);
+        for (int l = lp + 1 + lane; l <= L; l += 32) {
+            if (lp + 1 < L && l >= lp + 2) bad |= !(out[o0 + (l - lp - 1)] >= out[o1 + (l - lp - 2)]);
+            if (l < L) bad_l |= !(out[o0 + (l - lp - 1)] <= out[o0 + (l - lp)]);
+        }
     }
     bad = __any_sync(0xffffffffu, bad);
+    bad_l = __any_sync(0xffffffffu, bad_l);
+    const int flags = (bad ? 0 : 1) | (bad_l ? 0 : 2);
     if (nw == 1) {
-        if (lane == 0) reinterpret_cast<int*>(ws + lay.smono)[slot] = !bad;
+        if (lane == 0) reinterpret_cast<int*>(ws + lay.smono)[slot] = flags;
         return;
     }
     if (lane == 0 && bad) atomicOr(s_bad, 1);
+    if (lane == 0 && bad_l) atomicOr(s_bad, 2);
     __syncthreads();
-    if (threadIdx.x == 0) { reinterpret_cast<int*>(ws + lay.smono)[slot] = !*s_bad; *s_bad = 0; }
+    if (threadIdx.x == 0) { reinterpret_cast<int*>(ws + lay.smono)[slot] = 3 & ~*s_bad; *s_bad = 0; }
     __syncthreads();
 }
 
@@ -1364,7 +1371,7 @@ __device__ __forceinline__ void combine_item_s(const pp_batch& b, const pp_insta
     __syncthreads();
     pdl_trigger_at<1>();
     const double* S = j > S_DIRECT_J ? Stri : Sg;
-    const bool mono = g_combine_early_exit && reinterpret_cast<const int*>(ws + lay.smono)[slot];
+    const bool mono = g_combine_early_exit && (reinterpret_cast<const int*>(ws + lay.smono)[slot] & 1);
     if (j >= 4) combine_tiles_s<4, COMBINE_TL4>(Wi, i, r, L, j, S, trio, Xs, s_hist, s_order, part, nparts, lA, lB, atomic, mono);
     else if (j >= 2) combine_tiles_s<2, 4 * COMBINE_TL4 / 2>(Wi, i, r, L, j, S, trio, Xs, s_hist, s_order, part, nparts, lA, lB, atomic, mono);
     else combine_tiles_s<1, 8 * COMBINE_TL4 / 2>(Wi, i, r, L, j, S, trio, Xs, s_hist, s_order, part, nparts, lA, lB, atomic, mono);

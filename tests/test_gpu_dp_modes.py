@@ -183,3 +183,27 @@ def test_graph_replay_across_batches(persistent):
             got = [planner._decode(db, h, k, items[k][1], packs[k]) for k in range(len(items))]
             assert got == want
         del db
+
+
+@pytest.mark.parametrize("early", [True, False])
+def test_crossing_search_combine_identical(early_exit, early):
+    """Per-step combine: crossing search (default) vs the exhaustive register
+    tiles, with and without the monotonicity certificates in use: identical
+    results on random, C2, C3 (full 96 x 64, uniform and jittered) and C4."""
+    rng = random.Random(1234)
+    specs = (_rand_specs(rng, 40, 60, 24) + [W.c2_bert24(), W.c3_gpt96(M=8), W.c3_gpt96(M=256, jitter_seed=7)]
+             + W.c4_batch(6))
+    models = [s.to_model() for s in specs]
+    prev = _lib.dp_combine(0)
+    try:
+        early_exit(True)
+        ref = P.spp_many(models)
+        _lib.dp_combine(1)
+        early_exit(early)
+        got = P.spp_many(models)
+        one = [P.spp(*m) for m in models[-8:]]   # single-instance path (split critical chain)
+    finally:
+        _lib.dp_combine(prev)
+    for s, x, y in zip(specs, ref, got):
+        assert x == y, s.name
+    assert one == ref[-8:]
