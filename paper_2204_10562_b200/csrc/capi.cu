@@ -20,7 +20,7 @@ __global__ void k_stab_big(pp_batch b);
 __global__ void k_expand_s_p(const pp_batch* bp, int j, int rfirst, int rlast);
 __global__ void k_expand_m_p(const pp_batch* bp, int j, int rb);
 __global__ void k_combine_s_p(const pp_batch* bp, int j, int r0);
-__global__ void k_combine_bis_p(const pp_batch* bp, int j, int r0);
+__global__ void k_combine_bis_p(const pp_batch* bp, int j, int r0, int rg);
 __global__ void k_backtrack_p(const pp_batch* bp);
 __global__ void k_phi(pp_batch b);
 __global__ void k_base(pp_batch b, int full_rows);
@@ -584,7 +584,7 @@ static int prm_tables_p(const pp_batch* b, const pp_batch* db, void* stream) {
                          (int)std::max(ex_smem, sizeof(double) * (size_t)(EX_SMEM_DOUBLES + 2)));
     cudaFuncSetAttribute(k_combine_s_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs_smem);
     cudaFuncSetAttribute(k_combine_bis_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(double) * ((size_t)(maxL - 1) * maxL / 2 + (size_t)(maxL > 1 ? maxL - 1 : 0) * maxV + 4)));
+                         (int)(sizeof(double) * combine_bis_smem_doubles(maxL, maxV, maxL)));
     return PP_OK;
 }
 
@@ -599,9 +599,15 @@ static int launch_combine(const pp_batch* b, const pp_batch* db, cudaStream_t st
     cfg.numAttrs = 1;
     cudaError_t e;
     if (g_combine_kind == 1) {
-        cfg.gridDim = dim3(b->n_inst, nitems, 1);
-        cfg.dynamicSmemBytes = sizeof(double) * ((size_t)(maxL - 1) * maxL / 2 + (size_t)(maxL > 1 ? maxL - 1 : 0) * j + 4);
-        e = cudaLaunchKernelEx(&cfg, k_combine_bis_p, db, j, r0);
+        // row groups: split items until the launch has ~2 waves of CTAs (at most L/8 groups)
+        const int64_t items = (int64_t)b->n_inst * nitems;
+        int groups = (int)std::min<int64_t>((2 * num_sms() + items - 1) / items, (maxL + 7) / 8);
+        if (groups < 1) groups = 1;
+        const int rg = (maxL + groups - 1) / groups;
+        groups = (maxL + rg - 1) / rg;
+        cfg.gridDim = dim3(b->n_inst, nitems, groups);
+        cfg.dynamicSmemBytes = sizeof(double) * combine_bis_smem_doubles(maxL, j, rg);
+        e = cudaLaunchKernelEx(&cfg, k_combine_bis_p, db, j, r0, rg);
     } else {
         cfg.gridDim = dim3(b->n_inst, nitems, parts);
         cfg.dynamicSmemBytes = sizeof(double) * ((maxL + 1) / 2 + 3 + (size_t)(maxL - 1) * maxL / 2 +

@@ -14,134 +14,143 @@
 //     l' <  p*:  f = S(l', l) >= S(p*-1, l)  (S falls, and dominates X)
 // so the minimum over the whole range is EXACTLY min(X(p*), S(p*-1, l)) — the
 // same value, bit for bit, as the exhaustive min (min/max only select).  p* is
-// found by bisection; when the triangle is also non-decreasing in l (bit 1),
-// p*(l) >= p*(l-1) and each cell gallops forward from its predecessor's p*.
+// found by a branch-free bisection (ceil(log2(l - xi + 1)) + 1 probes).
 // Columns or triangles without the certificate fold every l' (descending with
 // the early exit of DESIGN.md §4.3 when bit 0 holds).  The stored value is all
 // the backtrack needs (it re-derives the reference's first-found arg-min).
 //
-// Work per cell drops from (l - xi + 1) candidates to ~2-7 probes; a thread
-// owns one column and CB_RB consecutive rows, so the W stores of a warp are
-// consecutive xi of one row (coalesced).
+// A CTA owns one item and a group of rows l in [l0, l1]: it stages only what
+// those cells read — X rows 1..l1-1 (one TMA bulk copy) and the triangle
+// columns S(., l) for its rows, gathered transposed (cp.async) so a cell's
+// probes index one contiguous column — and checks the column certificates
+// over the staged rows only (all its cells' candidate ranges lie there).
+// One thread per cell; a warp's W stores are consecutive xi of one row.
+// Small batches split an item over many row groups (the critical item of the
+// split chain runs as L/8 CTAs), large ones use one group per item.
 #include "common.cuh"
 
 namespace pp {
 
-constexpr int CB_RB = 8;     // rows per thread (one column)
 constexpr int CB_T = 256;    // threads per CTA
 
-// S(l', l) in the packed triangle: row l' holds l = l'+1..L
+// S(l', l) in the packed row-major triangle: row l' holds l = l'+1..L
 __device__ __forceinline__ int tri_off(int L, int lp, int l) { return (lp - 1) * L - (lp - 1) * lp / 2 + (l - lp - 1); }
 
-__device__ __forceinline__ void combine_item_bis(const pp_batch& b, const pp_instance& I, int j, int r,
-                                                 double* cs_smem) {
+// dynamic shared memory of one CTA: X rows (L-1) x j, the group's triangle
+// columns (sum of l - 1 over its rows <= min(rg (L-1), L (L-1)/2)), spare
+__host__ __device__ __forceinline__ size_t combine_bis_smem_doubles(int L, int j, int rg) {
+    const size_t lm = L > 1 ? L - 1 : 0;
+    return lm * j + std::min<size_t>((size_t)rg * lm, (size_t)L * lm / 2) + 4;
+}
+
+__device__ __forceinline__ void combine_item_bis(const pp_batch& b, const pp_instance& I, int j, int r, int l0,
+                                                 int rg, double* cs_smem) {
     const int L = I.L, V = I.V;
-    if (j >= V || r > V - j) return;
+    if (j >= V || r > V - j || l0 > L) return;
     const int i = j + r;
     const bool allow = I.flags & PP_ALLOW_REPLICATION;
     if (!(allow || r == 1)) return;   // partition.py:103-104 (structural +inf, W_at)
+    const int l1 = min(L, l0 + rg - 1), nrow = l1 - l0 + 1;
     const WsLayout lay = ws_layout(L, V);
     double* ws = b.ws + I.ws_off;
     double* Wi = ws + lay.W + W_base(L, i);
     const int t = threadIdx.x;
     const int ncol = min(j, L - 1);   // xi = 2..ncol+1 (xi <= L: cells l >= xi exist)
-    __shared__ uint64_t s_bar[2];
-    __shared__ unsigned char s_xmono[SR_MAX];
+    __shared__ uint64_t s_bar[1];
+    __shared__ unsigned s_bad[SR_MAX / 32];   // columns without the certificate
     const int ns = (L - 1) * L / 2;
     const int slot = reinterpret_cast<const int*>(ws + lay.sidx)[(r - 1) * V + (i - 1)];
     const double* Sg = ws + lay.Stab + (int64_t)slot * ns;
     const double* Xg = ws + lay.X + X_base(L, i, r);
-    double* Stri = cs_smem;
-    Stri += dphase(Stri) ^ dphase(Sg);
-    double* Xs = cs_smem + 2 + ns;
+    // the group's triangle columns, packed: S(p, l) = Sc[co(l) + p - 1], p = 1..l-1,
+    // co(l) = sum_{l0 <= l' < l} (l' - 1) = ((l-1)(l-2) - (l0-1)(l0-2)) / 2
+    double* Sc = cs_smem;
+    const int cob = (l0 - 1) * (l0 - 2) / 2 + 1;   // column base: Sc + (l-1)(l-2)/2 - cob, indexed by p
+    double* Xs = cs_smem + (l1 * (l1 - 1) / 2 - (l0 - 1) * (l0 - 2) / 2) + 1;
     Xs += dphase(Xs) ^ dphase(Xg);
-    if (t == 0) { mbar_init(&s_bar[0]); mbar_init(&s_bar[1]); }
+    const int nx = (min(l1, L) - 1) * j;   // X rows 1..l1-1
+    if (t == 0) mbar_init(&s_bar[0]);
+    if (t < SR_MAX / 32) s_bad[t] = 0;
     __syncthreads();
     // the triangle was built before the wavefront: it streams in under PDL while
     // the expand drains; X (this step's expand) after the dependency wait
-    stage_span(Stri, Sg, 0, ns, &s_bar[0], l2_evict_last_policy());
-    pdl_wait();
-    stage_span(Xs, Xg, 0, (L - 1) * j, &s_bar[1], l2_evict_normal_policy());
+    {
+        const uint64_t pol = l2_evict_last_policy();
+        const int lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+        for (int l = l0 + warp; l <= l1; l += nw) {
+            double* col = Sc + ((l - 1) * (l - 2) / 2 - cob);
+            for (int p = 1 + lane; p < l; p += 32) cp_async8_hint(col + p, Sg + tri_off(L, p, l), pol);
+        }
+        cp_async_commit();
+    }
     const int sflags = reinterpret_cast<const int*>(ws + lay.smono)[slot];
     // g_combine_early_exit = 0 (pp_dp_set_early_exit): fold every l' (test knob)
-    const bool s_dec = (sflags & 1) && g_combine_early_exit, s_inc = (sflags & 2) != 0;
+    const bool s_dec = (sflags & 1) && g_combine_early_exit;
+    pdl_wait();
+    stage_span(Xs, Xg, 0, nx, &s_bar[0], l2_evict_normal_policy());
+    cp_async_wait<0>();
     mbar_wait0(&s_bar[0]);
-    mbar_wait0(&s_bar[1]);
     __syncthreads();
     pdl_trigger_at<1>();
-    // column certificates: X(., xi) non-decreasing over l' in [xi-1, L-1]
+    // column certificates: X(., xi) non-decreasing over the staged rows l' in [xi-1, l1-1]
     {
         const int lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
         for (int c = warp; c < ncol; c += nw) {
             const int xi = c + 2;
-            bool bad = false;
-            for (int lp = xi - 1 + lane; lp + 1 <= L - 1; lp += 32)
-                bad |= !(Xs[lp * j + c] >= Xs[(lp - 1) * j + c]);   // rows l' = 1..L-1 at (l'-1)*j
+            if (xi > l1) continue;   // no cell of this group in the column: plain +inf stores
+            bool bad = !s_dec;
+            for (int lp = xi - 1 + lane; lp + 1 <= l1 - 1; lp += 32)
+                bad |= !(Xs[lp * j + c] >= Xs[(lp - 1) * j + c]);   // rows l' = 1.. at (l'-1)*j
             bad = __any_sync(0xffffffffu, bad);
-            if (lane == 0) s_xmono[c] = !bad;
+            if (lane == 0 && bad) atomicOr(&s_bad[c >> 5], 1u << (c & 31));
         }
     }
     __syncthreads();
-    const int nrb = (L + CB_RB - 1) / CB_RB;
-    for (int u = t; u < ncol * nrb; u += blockDim.x) {
-        const int c = u % ncol, rb = u / ncol;
+    const int64_t ostride = (int64_t)i * i;
+    for (int u = t; u < nrow * ncol; u += blockDim.x) {
+        const int c = u % ncol, l = l0 + u / ncol;
         const int xi = c + 2;
-        const int l0 = 1 + rb * CB_RB, l1 = min(L, l0 + CB_RB - 1);
-        const double* Xc = Xs + c;   // X(l', xi) = Xc[(l'-1) * j]
-        double* out = Wi + (int64_t)(r - 1) * i + (xi - 1);   // W(l, xi, r, i) = out[(l-1) * i * i]
-        const int64_t ostride = (int64_t)i * i;
-        const bool bis = s_dec && s_xmono[c];
-        int pstar = -1;   // p* of the previous cell (gallop start), -1 = none
-        for (int l = l0; l <= l1; ++l) {
-            double w = PP_INF;
-            if (l >= xi) {
-                const int lo = xi - 1, hi = l - 1;
-                if (bis) {
-                    // first p in [lo, hi] with X(p) >= S(p, l); hi + 1 if none
-                    int a = lo, z = hi + 1;   // invariant: answer in [a, z]
-                    if (s_inc && pstar >= 0) {
-                        // p*(l) >= p*(l-1): gallop forward from it (1 probe when it stays)
-                        a = pstar;
-                        for (int step = 1;; step <<= 1) {
-                            const int p = a + step - 1;
-                            if (p > hi) break;
-                            if (Xc[(p - 1) * j] >= Stri[tri_off(L, p, l)]) { z = p; break; }
-                            a = p + 1;
-                        }
-                    }
-                    while (a < z) {
-                        const int m = (a + z) >> 1;
-                        if (Xc[(m - 1) * j] >= Stri[tri_off(L, m, l)]) z = m;
-                        else a = m + 1;
-                    }
-                    pstar = a;
-                    if (a <= hi) w = Xc[(a - 1) * j];
-                    if (a > lo) w = dmin(w, Stri[tri_off(L, a - 1, l)]);
-                } else if (s_dec) {
-                    // descending l': S only grows, stop once it reaches the running min
-                    for (int p = hi; p >= lo; --p) {
-                        const double s = Stri[tri_off(L, p, l)];
-                        if (s >= w) break;
-                        w = dmin(w, dmax(Xc[(p - 1) * j], s));
-                    }
-                } else {
-                    for (int p = lo; p <= hi; ++p) w = dmin(w, dmax(Xc[(p - 1) * j], Stri[tri_off(L, p, l)]));
+        double w = PP_INF;
+        if (l >= xi) {
+            const bool cert = !((s_bad[c >> 5] >> (c & 31)) & 1u);
+            const int lo = xi - 1, hi = l - 1;
+            const double* Xc = Xs + c;                          // X(l', xi) = Xc[(l'-1) * j]
+            const double* Sl = Sc + ((l - 1) * (l - 2) / 2 - cob);   // S(l', l) = Sl[l']
+            if (cert) {
+                // first p in [lo, hi] with X(p) >= S(p, l) (hi + 1 if none): branch-free lower bound
+                int base = lo, n = hi - lo + 1;
+                while (n > 0) {
+                    const int half = n >> 1, m = base + half;
+                    const bool ge = Xc[(m - 1) * j] >= Sl[m];
+                    base = ge ? base : m + 1;
+                    n = ge ? half : n - half - 1;
                 }
+                if (base <= hi) w = Xc[(base - 1) * j];
+                if (base > lo) w = dmin(w, Sl[base - 1]);
+            } else if (s_dec) {
+                // descending l': S only grows, stop once it reaches the running min
+                for (int p = hi; p >= lo; --p) {
+                    const double sv = Sl[p];
+                    if (sv >= w) break;
+                    w = dmin(w, dmax(Xc[(p - 1) * j], sv));
+                }
+            } else {
+                for (int p = lo; p <= hi; ++p) w = dmin(w, dmax(Xc[(p - 1) * j], Sl[p]));
             }
-            out[(int64_t)(l - 1) * ostride] = w;
         }
+        Wi[(int64_t)(l - 1) * ostride + (int64_t)(r - 1) * i + (xi - 1)] = w;
     }
 }
 
-// one CTA per (instance, item r = r0 + blockIdx.y), target i = j + r
-__global__ void __launch_bounds__(CB_T, 2) k_combine_bis_p(const pp_batch* __restrict__ bp, int j, int r0) {
+// one CTA per (instance, item r = r0 + blockIdx.y, rows 1 + rg * blockIdx.z ..), target i = j + r
+__global__ void __launch_bounds__(CB_T, 2) k_combine_bis_p(const pp_batch* __restrict__ bp, int j, int r0, int rg) {
     pdl_trigger_at<0>();
     StepTrace tr;
     tr.begin();
     const pp_batch b = *bp;
     const pp_instance I = b.inst[blockIdx.x];
     extern __shared__ __align__(16) double cs_smem[];
-    combine_item_bis(b, I, j, blockIdx.y + r0, cs_smem);
+    combine_item_bis(b, I, j, blockIdx.y + r0, 1 + rg * (int)blockIdx.z, rg, cs_smem);
     pdl_trigger_at<2>();
     tr.end(2, j);
 }
