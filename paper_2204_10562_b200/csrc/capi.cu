@@ -20,7 +20,7 @@ __global__ void k_stab_big(pp_batch b);
 __global__ void k_expand_s_p(const pp_batch* bp, int j, int rfirst, int rlast);
 __global__ void k_expand_m_p(const pp_batch* bp, int j, int rb);
 __global__ void k_combine_s_p(const pp_batch* bp, int j, int r0);
-__global__ void k_combine_bis_p(const pp_batch* bp, int j, int r0, int rg);
+__global__ void k_combine_bis_p(const pp_batch* bp, int j, int r0, int rg, int rb);
 __global__ void k_backtrack_p(const pp_batch* bp);
 __global__ void k_phi(pp_batch b);
 __global__ void k_base(pp_batch b, int full_rows);
@@ -110,6 +110,8 @@ static const int g_c1_parts = getenv("PP_C1_PARTS") ? std::max(1, std::min(64, a
 static const int g_pdl = getenv("PP_PDL") ? atoi(getenv("PP_PDL")) : 1;
 // combine kernel of the per-step schedule: 1 = crossing search (combine_bis.cu),
 // 0 = exhaustive register tiles (k_combine_s_p); same bits either way
+static const int g_bis_rb = getenv("PP_BIS_RB") ? atoi(getenv("PP_BIS_RB")) : 0;   // rows per thread (0 = auto)
+static const int g_bis_waves = getenv("PP_BIS_WAVES") ? atoi(getenv("PP_BIS_WAVES")) : 2;
 static std::atomic<int> g_combine_kind{getenv("PP_COMBINE_BIS") ? atoi(getenv("PP_COMBINE_BIS")) : 1};
 
 static int num_sms() {
@@ -601,13 +603,14 @@ static int launch_combine(const pp_batch* b, const pp_batch* db, cudaStream_t st
     if (g_combine_kind == 1) {
         // row groups: split items until the launch has ~2 waves of CTAs (at most L/8 groups)
         const int64_t items = (int64_t)b->n_inst * nitems;
-        int groups = (int)std::min<int64_t>((2 * num_sms() + items - 1) / items, (maxL + 7) / 8);
+        int groups = (int)std::min<int64_t>((g_bis_waves * num_sms() + items - 1) / items, (maxL + 7) / 8);
         if (groups < 1) groups = 1;
         const int rg = (maxL + groups - 1) / groups;
         groups = (maxL + rg - 1) / rg;
         cfg.gridDim = dim3(b->n_inst, nitems, groups);
         cfg.dynamicSmemBytes = sizeof(double) * combine_bis_smem_doubles(maxL, j, rg);
-        e = cudaLaunchKernelEx(&cfg, k_combine_bis_p, db, j, r0, rg);
+        const int rb = g_bis_rb > 0 ? g_bis_rb : (groups > 1 ? 1 : 8);
+        e = cudaLaunchKernelEx(&cfg, k_combine_bis_p, db, j, r0, rg, rb);
     } else {
         cfg.gridDim = dim3(b->n_inst, nitems, parts);
         cfg.dynamicSmemBytes = sizeof(double) * ((maxL + 1) / 2 + 3 + (size_t)(maxL - 1) * maxL / 2 +

@@ -40,11 +40,12 @@ __device__ __forceinline__ int tri_off(int L, int lp, int l) { return (lp - 1) *
 // columns (sum of l - 1 over its rows <= min(rg (L-1), L (L-1)/2)), spare
 __host__ __device__ __forceinline__ size_t combine_bis_smem_doubles(int L, int j, int rg) {
     const size_t lm = L > 1 ? L - 1 : 0;
-    return lm * j + std::min<size_t>((size_t)rg * lm, (size_t)L * lm / 2) + 4;
+    const size_t a = (size_t)rg * lm, b = (size_t)L * lm / 2;
+    return lm * j + (a < b ? a : b) + 4;
 }
 
 __device__ __forceinline__ void combine_item_bis(const pp_batch& b, const pp_instance& I, int j, int r, int l0,
-                                                 int rg, double* cs_smem) {
+                                                 int rg, int rb, double* cs_smem) {
     const int L = I.L, V = I.V;
     if (j >= V || r > V - j || l0 > L) return;
     const int i = j + r;
@@ -85,7 +86,7 @@ __device__ __forceinline__ void combine_item_bis(const pp_batch& b, const pp_ins
     }
     const int sflags = reinterpret_cast<const int*>(ws + lay.smono)[slot];
     // g_combine_early_exit = 0 (pp_dp_set_early_exit): fold every l' (test knob)
-    const bool s_dec = (sflags & 1) && g_combine_early_exit;
+    const bool s_dec = (sflags & 1) && g_combine_early_exit, s_inc = (sflags & 2) != 0;
     pdl_wait();
     stage_span(Xs, Xg, 0, nx, &s_bar[0], l2_evict_normal_policy());
     cp_async_wait<0>();
@@ -107,50 +108,72 @@ __device__ __forceinline__ void combine_item_bis(const pp_batch& b, const pp_ins
     }
     __syncthreads();
     const int64_t ostride = (int64_t)i * i;
-    for (int u = t; u < nrow * ncol; u += blockDim.x) {
-        const int c = u % ncol, l = l0 + u / ncol;
+    // thread = (column, rb consecutive rows): the first row bisects, later rows of
+    // a certified column gallop forward from the previous crossing when the
+    // triangle is also non-decreasing in l (p*(l) >= p*(l-1)); rb = 1 for small
+    // batches (latency: one cell per thread), 8 for large ones (work)
+    const int nrb = (nrow + rb - 1) / rb;
+    for (int u = t; u < nrb * ncol; u += blockDim.x) {
+        const int c = u % ncol, la = l0 + (u / ncol) * rb, lz = min(l1, la + rb - 1);
         const int xi = c + 2;
-        double w = PP_INF;
-        if (l >= xi) {
-            const bool cert = !((s_bad[c >> 5] >> (c & 31)) & 1u);
-            const int lo = xi - 1, hi = l - 1;
-            const double* Xc = Xs + c;                          // X(l', xi) = Xc[(l'-1) * j]
-            const double* Sl = Sc + ((l - 1) * (l - 2) / 2 - cob);   // S(l', l) = Sl[l']
-            if (cert) {
-                // first p in [lo, hi] with X(p) >= S(p, l) (hi + 1 if none): branch-free lower bound
-                int base = lo, n = hi - lo + 1;
-                while (n > 0) {
-                    const int half = n >> 1, m = base + half;
-                    const bool ge = Xc[(m - 1) * j] >= Sl[m];
-                    base = ge ? base : m + 1;
-                    n = ge ? half : n - half - 1;
+        const bool cert = !((s_bad[c >> 5] >> (c & 31)) & 1u);
+        const double* Xc = Xs + c;   // X(l', xi) = Xc[(l'-1) * j]
+        int pstar = -1;              // crossing of the previous row (gallop start)
+        for (int l = la; l <= lz; ++l) {
+            double w = PP_INF;
+            if (l >= xi) {
+                const int lo = xi - 1, hi = l - 1;
+                const double* Sl = Sc + ((l - 1) * (l - 2) / 2 - cob);   // S(l', l) = Sl[l']
+                if (cert) {
+                    // first p in [lo, hi] with X(p) >= S(p, l) (hi + 1 if none)
+                    int base = lo, n = hi - lo + 1;
+                    if (s_inc && pstar >= 0) {
+                        base = pstar;
+                        n = hi - pstar + 1;
+                        // gallop: probe pstar, pstar + 1, pstar + 3, ... (1 probe when it stays)
+                        for (int step = 1; n > 0; step <<= 1) {
+                            const int p = base + step - 1;
+                            if (p > hi) break;
+                            if (Xc[(p - 1) * j] >= Sl[p]) { n = step - 1; break; }
+                            base = p + 1;
+                            n = hi - base + 1;
+                        }
+                    }
+                    while (n > 0) {   // branch-free lower bound over [base, base + n)
+                        const int half = n >> 1, m = base + half;
+                        const bool ge = Xc[(m - 1) * j] >= Sl[m];
+                        base = ge ? base : m + 1;
+                        n = ge ? half : n - half - 1;
+                    }
+                    pstar = base;
+                    if (base <= hi) w = Xc[(base - 1) * j];
+                    if (base > lo) w = dmin(w, Sl[base - 1]);
+                } else if (s_dec) {
+                    // descending l': S only grows, stop once it reaches the running min
+                    for (int p = hi; p >= lo; --p) {
+                        const double sv = Sl[p];
+                        if (sv >= w) break;
+                        w = dmin(w, dmax(Xc[(p - 1) * j], sv));
+                    }
+                } else {
+                    for (int p = lo; p <= hi; ++p) w = dmin(w, dmax(Xc[(p - 1) * j], Sl[p]));
                 }
-                if (base <= hi) w = Xc[(base - 1) * j];
-                if (base > lo) w = dmin(w, Sl[base - 1]);
-            } else if (s_dec) {
-                // descending l': S only grows, stop once it reaches the running min
-                for (int p = hi; p >= lo; --p) {
-                    const double sv = Sl[p];
-                    if (sv >= w) break;
-                    w = dmin(w, dmax(Xc[(p - 1) * j], sv));
-                }
-            } else {
-                for (int p = lo; p <= hi; ++p) w = dmin(w, dmax(Xc[(p - 1) * j], Sl[p]));
             }
+            Wi[(int64_t)(l - 1) * ostride + (int64_t)(r - 1) * i + (xi - 1)] = w;
         }
-        Wi[(int64_t)(l - 1) * ostride + (int64_t)(r - 1) * i + (xi - 1)] = w;
     }
 }
 
 // one CTA per (instance, item r = r0 + blockIdx.y, rows 1 + rg * blockIdx.z ..), target i = j + r
-__global__ void __launch_bounds__(CB_T, 2) k_combine_bis_p(const pp_batch* __restrict__ bp, int j, int r0, int rg) {
+__global__ void __launch_bounds__(CB_T, 2) k_combine_bis_p(const pp_batch* __restrict__ bp, int j, int r0, int rg,
+                                                           int rb) {
     pdl_trigger_at<0>();
     StepTrace tr;
     tr.begin();
     const pp_batch b = *bp;
     const pp_instance I = b.inst[blockIdx.x];
     extern __shared__ __align__(16) double cs_smem[];
-    combine_item_bis(b, I, j, blockIdx.y + r0, 1 + rg * (int)blockIdx.z, rg, cs_smem);
+    combine_item_bis(b, I, j, blockIdx.y + r0, 1 + rg * (int)blockIdx.z, rg, rb, cs_smem);
     pdl_trigger_at<2>();
     tr.end(2, j);
 }
