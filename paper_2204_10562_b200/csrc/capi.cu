@@ -1,5 +1,6 @@
 // capi.cu — extern "C" entry points of libpipeplan_b200.so (include/pipeplan_b200.h).
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -111,7 +112,7 @@ static const int g_pdl = getenv("PP_PDL") ? atoi(getenv("PP_PDL")) : 1;
 // combine kernel of the per-step schedule: 1 = crossing search (combine_bis.cu),
 // 0 = exhaustive register tiles (k_combine_s_p); same bits either way
 static const int g_bis_rb = getenv("PP_BIS_RB") ? atoi(getenv("PP_BIS_RB")) : 0;   // rows per thread (0 = auto)
-static const int g_bis_waves = getenv("PP_BIS_WAVES") ? atoi(getenv("PP_BIS_WAVES")) : 2;
+static const double g_bis_waves = getenv("PP_BIS_WAVES") ? atof(getenv("PP_BIS_WAVES")) : 2.0;
 static std::atomic<int> g_combine_kind{getenv("PP_COMBINE_BIS") ? atoi(getenv("PP_COMBINE_BIS")) : 1};
 
 static int num_sms() {
@@ -603,7 +604,7 @@ static int launch_combine(const pp_batch* b, const pp_batch* db, cudaStream_t st
     if (g_combine_kind == 1) {
         // row groups: split items until the launch has ~2 waves of CTAs (at most L/8 groups)
         const int64_t items = (int64_t)b->n_inst * nitems;
-        int groups = (int)std::min<int64_t>((g_bis_waves * num_sms() + items - 1) / items, (maxL + 7) / 8);
+        int groups = (int)std::min<int64_t>((int64_t)std::ceil(g_bis_waves * num_sms() / (double)items), (maxL + 7) / 8);
         if (groups < 1) groups = 1;
         const int rg = (maxL + groups - 1) / groups;
         groups = (maxL + rg - 1) / rg;

@@ -15,9 +15,16 @@
 // so the minimum over the whole range is EXACTLY min(X(p*), S(p*-1, l)) — the
 // same value, bit for bit, as the exhaustive min (min/max only select).  p* is
 // found by a branch-free bisection (ceil(log2(l - xi + 1)) + 1 probes).
-// Columns or triangles without the certificate fold every l' (descending with
-// the early exit of DESIGN.md §4.3 when bit 0 holds).  The stored value is all
-// the backtrack needs (it re-derives the reference's first-found arg-min).
+// A column that is NOT monotone is handled through its suffix minima
+//     g_l(p) = min X(p..l-1),
+// non-decreasing in p: a candidate l' is dominated by any later l'' <= l-1 with
+// X(l'') <= X(l') (both terms of its max are >= those of l''), so
+//     min_{l'} max(X(l'), S(l', l)) = min_p max(g_l(p), S(p, l)),
+// again a valley, bisected the same way; g_l(p) is the last element < l of the
+// next-strictly-smaller chain from p (built once per column with the
+// pointer-jumping stack, amortised O(L)), a value of X bit for bit.  Only
+// triangles without bit 0 fold every l'.  The stored value is all the
+// backtrack needs (it re-derives the reference's first-found arg-min).
 //
 // A CTA owns one item and a group of rows l in [l0, l1]: it stages only what
 // those cells read — X rows 1..l1-1 (one TMA bulk copy) and the triangle
@@ -37,11 +44,12 @@ constexpr int CB_T = 256;    // threads per CTA
 __device__ __forceinline__ int tri_off(int L, int lp, int l) { return (lp - 1) * L - (lp - 1) * lp / 2 + (l - lp - 1); }
 
 // dynamic shared memory of one CTA: X rows (L-1) x j, the group's triangle
-// columns (sum of l - 1 over its rows <= min(rg (L-1), L (L-1)/2)), spare
+// columns (sum of l - 1 over its rows <= min(rg (L-1), L (L-1)/2)), spare, then
+// the next-smaller chains (j x (L+1) bytes)
 __host__ __device__ __forceinline__ size_t combine_bis_smem_doubles(int L, int j, int rg) {
     const size_t lm = L > 1 ? L - 1 : 0;
     const size_t a = (size_t)rg * lm, b = (size_t)L * lm / 2;
-    return lm * j + (a < b ? a : b) + 4;
+    return lm * j + (a < b ? a : b) + 4 + ((size_t)j * (L + 1) + 7) / 8;
 }
 
 __device__ __forceinline__ void combine_item_bis(const pp_batch& b, const pp_instance& I, int j, int r, int l0,
@@ -107,6 +115,23 @@ __device__ __forceinline__ void combine_item_bis(const pp_batch& b, const pp_ins
         }
     }
     __syncthreads();
+    // next-strictly-smaller chains of the uncertified columns over the staged rows
+    // (rows >= l1 are never read: every cell of the group has l - 1 <= l1 - 1)
+    unsigned char* nse = reinterpret_cast<unsigned char*>(Xs + nx + 1);
+    if (s_dec)
+        for (int c = t; c < ncol; c += blockDim.x) {
+            if (!((s_bad[c >> 5] >> (c & 31)) & 1u)) continue;
+            const int xi = c + 2;
+            unsigned char* ns = nse + c * (L + 1);
+            const double* Xc = Xs + c;
+            for (int p = l1 - 1; p >= xi - 1; --p) {
+                const double xp = Xc[(p - 1) * j];
+                int q = p + 1;
+                while (q <= l1 - 1 && Xc[(q - 1) * j] >= xp) q = ns[q];
+                ns[p] = (unsigned char)(q <= l1 - 1 ? q : 255);
+            }
+        }
+    __syncthreads();
     const int64_t ostride = (int64_t)i * i;
     // thread = (column, rb consecutive rows): the first row bisects, later rows of
     // a certified column gallop forward from the previous crossing when the
@@ -149,12 +174,24 @@ __device__ __forceinline__ void combine_item_bis(const pp_batch& b, const pp_ins
                     if (base <= hi) w = Xc[(base - 1) * j];
                     if (base > lo) w = dmin(w, Sl[base - 1]);
                 } else if (s_dec) {
-                    // descending l': S only grows, stop once it reaches the running min
-                    for (int p = hi; p >= lo; --p) {
-                        const double sv = Sl[p];
-                        if (sv >= w) break;
-                        w = dmin(w, dmax(Xc[(p - 1) * j], sv));
+                    // the same lower bound on the suffix minima g_l(p) = X(last of p's
+                    // next-smaller chain below l)
+                    const unsigned char* ns = nse + c * (L + 1);
+                    int base = lo, n = hi - lo + 1;
+                    while (n > 0) {
+                        const int half = n >> 1, m = base + half;
+                        int q = m;
+                        while (ns[q] < l) q = ns[q];
+                        const bool ge = Xc[(q - 1) * j] >= Sl[m];
+                        base = ge ? base : m + 1;
+                        n = ge ? half : n - half - 1;
                     }
+                    if (base <= hi) {
+                        int q = base;
+                        while (ns[q] < l) q = ns[q];
+                        w = Xc[(q - 1) * j];
+                    }
+                    if (base > lo) w = dmin(w, Sl[base - 1]);
                 } else {
                     for (int p = lo; p <= hi; ++p) w = dmin(w, dmax(Xc[(p - 1) * j], Sl[p]));
                 }
