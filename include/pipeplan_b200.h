@@ -139,10 +139,12 @@ int pp_dp_set_persistent(int32_t mode);
  * Returns the previous value (needs a device: the flag is device state). */
 int pp_dp_set_early_exit(int32_t on);
 
-/* Combine kernel of the per-step DP schedule: 1 (default) = crossing search
- * (combine_bis.cu: bisection for the valley of max(X, S) under certified
- * monotonicity, exhaustive fold otherwise), 0 = exhaustive register tiles.
- * Identical results; a performance / test knob.  Returns the previous kind. */
+/* Combine kernel of the per-step DP schedule: 1 = crossing search
+ * (combine_bis.cu: bisection for the valley of max(X, S) under a certified
+ * monotone stage-term triangle), 0 = exhaustive register tiles, 2 (default) =
+ * auto (crossing search for batches of <= 2 instances, where the wavefront is
+ * latency-bound; tiles above).  Identical results; a performance / test knob.
+ * Returns the previous kind. */
 int pp_dp_set_combine(int32_t kind);
 
 /* Debug: record the persistent DP's per-task timeline (4 x u64 per task:

@@ -164,8 +164,8 @@ def dp_early_exit(on: bool) -> bool:
 
 
 def dp_combine(kind: int) -> int:
-    """Per-step combine kernel: 1 crossing search (default), 0 exhaustive
-    register tiles.  Returns the previous kind; results are identical."""
+    """Per-step combine kernel: 1 crossing search, 0 exhaustive register
+    tiles, 2 auto (default).  Returns the previous kind; results are identical."""
     return int(load(require_device=False).pp_dp_set_combine(int(kind)))
 
 

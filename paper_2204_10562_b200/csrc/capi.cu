@@ -110,10 +110,13 @@ static const int g_c1_parts = getenv("PP_C1_PARTS") ? std::max(1, std::min(64, a
 // programmatic dependent launch in the per-step chain (PP_PDL=0 disables)
 static const int g_pdl = getenv("PP_PDL") ? atoi(getenv("PP_PDL")) : 1;
 // combine kernel of the per-step schedule: 1 = crossing search (combine_bis.cu),
-// 0 = exhaustive register tiles (k_combine_s_p); same bits either way
+// 0 = exhaustive register tiles (k_combine_s_p), 2 = auto; same bits either way
 static const int g_bis_rb = getenv("PP_BIS_RB") ? atoi(getenv("PP_BIS_RB")) : 0;   // rows per thread (0 = auto)
 static const double g_bis_waves = getenv("PP_BIS_WAVES") ? atof(getenv("PP_BIS_WAVES")) : 2.0;
-static std::atomic<int> g_combine_kind{getenv("PP_COMBINE_BIS") ? atoi(getenv("PP_COMBINE_BIS")) : 1};
+static std::atomic<int> g_combine_kind{getenv("PP_COMBINE_BIS") ? atoi(getenv("PP_COMBINE_BIS")) : 2};
+// auto (kind 2): the crossing search for batches of at most this many instances
+// (latency-bound chains), the register tiles above it (throughput)
+static const int g_bis_max_inst = getenv("PP_BIS_MAX_INST") ? atoi(getenv("PP_BIS_MAX_INST")) : 2;
 
 static int num_sms() {
     static thread_local int dev = -1, sms = 148;
@@ -323,7 +326,7 @@ static int prm_inst(const pp_batch* b, void* stream) {
     return PP_OK;
 }
 
-int pp_dp_set_combine(int32_t kind) { return g_combine_kind.exchange(kind ? 1 : 0); }
+int pp_dp_set_combine(int32_t kind) { return g_combine_kind.exchange(kind < 0 || kind > 2 ? 2 : kind); }
 
 int pp_dp_set_early_exit(int32_t on) {
     int prev = 1, v = on ? 1 : 0;
@@ -593,7 +596,7 @@ static int prm_tables_p(const pp_batch* b, const pp_batch* db, void* stream) {
 
 // one combine launch of the per-step schedule: items r0 .. r0 + nitems - 1 of step j
 static int launch_combine(const pp_batch* b, const pp_batch* db, cudaStream_t st, cudaLaunchAttribute* attrs, int j,
-                          int r0, int nitems, int parts) {
+                          int r0, int nitems, int parts, int total_inst) {
     const int maxL = b->max_L;
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(256);
@@ -601,7 +604,8 @@ static int launch_combine(const pp_batch* b, const pp_batch* db, cudaStream_t st
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
     cudaError_t e;
-    if (g_combine_kind == 1) {
+    const int kind = g_combine_kind.load();
+    if (kind == 1 || (kind == 2 && total_inst <= g_bis_max_inst)) {
         // row groups: split items until the launch has ~2 waves of CTAs (at most L/8 groups)
         const int64_t items = (int64_t)b->n_inst * nitems;
         int groups = (int)std::min<int64_t>((int64_t)std::ceil(g_bis_waves * num_sms() / (double)items), (maxL + 7) / 8);
@@ -676,7 +680,7 @@ static int prm_chain_split_p(const pp_batch* b, const pp_batch* db, void* stream
         return PP_OK;
     };
     auto combine = [&](cudaStream_t st, int j, int r0, int nitems, int parts) -> int {
-        return launch_combine(b, db, st, pdl, j, r0, nitems, parts);
+        return launch_combine(b, db, st, pdl, j, r0, nitems, parts, total_inst);
     };
     for (int j = 1; j < maxV; ++j) {
         if (j >= 3) cudaStreamWaitEvent(s0, cb[(j - 2) % 3], 0);
@@ -733,7 +737,8 @@ static int prm_chain_p(const pp_batch* b, const pp_batch* db, void* stream, int 
                 return fail(PP_ECUDA, "k_expand_s launch: %s", cudaGetErrorString(cudaGetLastError()));
             PP_CHECK_LAUNCH("k_expand_s");
         }
-        if ((rc = launch_combine(b, db, S(stream), pdl, j, 1, maxV - j, combine_parts(total_inst * (maxV - j)))))
+        if ((rc = launch_combine(b, db, S(stream), pdl, j, 1, maxV - j, combine_parts(total_inst * (maxV - j)),
+                                 total_inst)))
             return rc;
     }
     dim3 gb(b->n_inst, maxV);

@@ -20,10 +20,12 @@
 // non-decreasing in p: a candidate l' is dominated by any later l'' <= l-1 with
 // X(l'') <= X(l') (both terms of its max are >= those of l''), so
 //     min_{l'} max(X(l'), S(l', l)) = min_p max(g_l(p), S(p, l)),
-// again a valley, bisected the same way; g_l(p) is the last element < l of the
-// next-strictly-smaller chain from p (built once per column with the
-// pointer-jumping stack, amortised O(L)), a value of X bit for bit.  Only
-// triangles without bit 0 fold every l'.  The stored value is all the
+// again a valley, bisected the same way.  X is non-decreasing between its
+// descents d (X(d+1) < X(d)), so g_l(p) = min(X(p), X(d+1) : p <= d <= l-2),
+// a value of X bit for bit; the certificate pass records up to CB_DESC
+// descents per column (columns with more, or triangles without bit 0, fold
+// the candidates: descending with the early exit when bit 0 holds, every l'
+// otherwise).  The stored value is all the
 // backtrack needs (it re-derives the reference's first-found arg-min).
 //
 // A CTA owns one item and a group of rows l in [l0, l1]: it stages only what
@@ -39,17 +41,17 @@
 namespace pp {
 
 constexpr int CB_T = 256;    // threads per CTA
+constexpr int CB_DESC = 8;   // descents of an X column handled by the suffix-minimum bisection
 
 // S(l', l) in the packed row-major triangle: row l' holds l = l'+1..L
 __device__ __forceinline__ int tri_off(int L, int lp, int l) { return (lp - 1) * L - (lp - 1) * lp / 2 + (l - lp - 1); }
 
 // dynamic shared memory of one CTA: X rows (L-1) x j, the group's triangle
-// columns (sum of l - 1 over its rows <= min(rg (L-1), L (L-1)/2)), spare, then
-// the next-smaller chains (j x (L+1) bytes)
+// columns (sum of l - 1 over its rows <= min(rg (L-1), L (L-1)/2)), spare
 __host__ __device__ __forceinline__ size_t combine_bis_smem_doubles(int L, int j, int rg) {
     const size_t lm = L > 1 ? L - 1 : 0;
     const size_t a = (size_t)rg * lm, b = (size_t)L * lm / 2;
-    return lm * j + (a < b ? a : b) + 4 + ((size_t)j * (L + 1) + 7) / 8;
+    return lm * j + (a < b ? a : b) + 4;
 }
 
 __device__ __forceinline__ void combine_item_bis(const pp_batch& b, const pp_instance& I, int j, int r, int l0,
@@ -66,7 +68,6 @@ __device__ __forceinline__ void combine_item_bis(const pp_batch& b, const pp_ins
     const int t = threadIdx.x;
     const int ncol = min(j, L - 1);   // xi = 2..ncol+1 (xi <= L: cells l >= xi exist)
     __shared__ uint64_t s_bar[1];
-    __shared__ unsigned s_bad[SR_MAX / 32];   // columns without the certificate
     const int ns = (L - 1) * L / 2;
     const int slot = reinterpret_cast<const int*>(ws + lay.sidx)[(r - 1) * V + (i - 1)];
     const double* Sg = ws + lay.Stab + (int64_t)slot * ns;
@@ -79,7 +80,6 @@ __device__ __forceinline__ void combine_item_bis(const pp_batch& b, const pp_ins
     Xs += dphase(Xs) ^ dphase(Xg);
     const int nx = (min(l1, L) - 1) * j;   // X rows 1..l1-1
     if (t == 0) mbar_init(&s_bar[0]);
-    if (t < SR_MAX / 32) s_bad[t] = 0;
     __syncthreads();
     // the triangle was built before the wavefront: it streams in under PDL while
     // the expand drains; X (this step's expand) after the dependency wait
@@ -101,36 +101,27 @@ __device__ __forceinline__ void combine_item_bis(const pp_batch& b, const pp_ins
     mbar_wait0(&s_bar[0]);
     __syncthreads();
     pdl_trigger_at<1>();
-    // column certificates: X(., xi) non-decreasing over the staged rows l' in [xi-1, l1-1]
+    // column certificates: the descents d of X(., xi) over the staged rows
+    // l' in [xi-1, l1-1] (X(d+1) < X(d)); none = monotone
+    __shared__ unsigned char s_desc[SR_MAX][CB_DESC];
+    __shared__ unsigned char s_ndesc[SR_MAX];   // 0..CB_DESC, or 255 = more
     {
         const int lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
         for (int c = warp; c < ncol; c += nw) {
             const int xi = c + 2;
-            if (xi > l1) continue;   // no cell of this group in the column: plain +inf stores
-            bool bad = !s_dec;
-            for (int lp = xi - 1 + lane; lp + 1 <= l1 - 1; lp += 32)
-                bad |= !(Xs[lp * j + c] >= Xs[(lp - 1) * j + c]);   // rows l' = 1.. at (l'-1)*j
-            bad = __any_sync(0xffffffffu, bad);
-            if (lane == 0 && bad) atomicOr(&s_bad[c >> 5], 1u << (c & 31));
+            int nd = s_dec ? 0 : 255;
+            for (int lp0 = xi - 1; lp0 + 1 <= l1 - 1 && nd != 255; lp0 += 32) {
+                const int lp = lp0 + lane;
+                const bool dsc = lp + 1 <= l1 - 1 && !(Xs[lp * j + c] >= Xs[(lp - 1) * j + c]);
+                const unsigned m = __ballot_sync(0xffffffffu, dsc);
+                const int k = nd + __popc(m & ((1u << lane) - 1u));
+                if (dsc && k < CB_DESC) s_desc[c][k] = (unsigned char)lp;
+                nd += __popc(m);
+                if (nd > CB_DESC) nd = 255;
+            }
+            if (lane == 0) s_ndesc[c] = (unsigned char)nd;
         }
     }
-    __syncthreads();
-    // next-strictly-smaller chains of the uncertified columns over the staged rows
-    // (rows >= l1 are never read: every cell of the group has l - 1 <= l1 - 1)
-    unsigned char* nse = reinterpret_cast<unsigned char*>(Xs + nx + 1);
-    if (s_dec)
-        for (int c = t; c < ncol; c += blockDim.x) {
-            if (!((s_bad[c >> 5] >> (c & 31)) & 1u)) continue;
-            const int xi = c + 2;
-            unsigned char* ns = nse + c * (L + 1);
-            const double* Xc = Xs + c;
-            for (int p = l1 - 1; p >= xi - 1; --p) {
-                const double xp = Xc[(p - 1) * j];
-                int q = p + 1;
-                while (q <= l1 - 1 && Xc[(q - 1) * j] >= xp) q = ns[q];
-                ns[p] = (unsigned char)(q <= l1 - 1 ? q : 255);
-            }
-        }
     __syncthreads();
     const int64_t ostride = (int64_t)i * i;
     // thread = (column, rb consecutive rows): the first row bisects, later rows of
@@ -141,7 +132,8 @@ __device__ __forceinline__ void combine_item_bis(const pp_batch& b, const pp_ins
     for (int u = t; u < nrb * ncol; u += blockDim.x) {
         const int c = u % ncol, la = l0 + (u / ncol) * rb, lz = min(l1, la + rb - 1);
         const int xi = c + 2;
-        const bool cert = !((s_bad[c >> 5] >> (c & 31)) & 1u);
+        const int nd = s_ndesc[c];
+        const bool cert = nd == 0;
         const double* Xc = Xs + c;   // X(l', xi) = Xc[(l'-1) * j]
         int pstar = -1;              // crossing of the previous row (gallop start)
         for (int l = la; l <= lz; ++l) {
@@ -173,25 +165,33 @@ __device__ __forceinline__ void combine_item_bis(const pp_batch& b, const pp_ins
                     pstar = base;
                     if (base <= hi) w = Xc[(base - 1) * j];
                     if (base > lo) w = dmin(w, Sl[base - 1]);
-                } else if (s_dec) {
-                    // the same lower bound on the suffix minima g_l(p) = X(last of p's
-                    // next-smaller chain below l)
-                    const unsigned char* ns = nse + c * (L + 1);
+                } else if (nd != 255) {
+                    // the same lower bound on the suffix minima g_l(p) = min(X(p), X(d+1) : p <= d <= l-2)
+                    const unsigned char* dl = s_desc[c];
+                    auto g = [&](int p) {
+                        double v = Xc[(p - 1) * j];
+                        for (int k = 0; k < nd; ++k) {
+                            const int d = dl[k];
+                            if (d >= p && d <= l - 2) v = dmin(v, Xc[d * j]);
+                        }
+                        return v;
+                    };
                     int base = lo, n = hi - lo + 1;
                     while (n > 0) {
                         const int half = n >> 1, m = base + half;
-                        int q = m;
-                        while (ns[q] < l) q = ns[q];
-                        const bool ge = Xc[(q - 1) * j] >= Sl[m];
+                        const bool ge = g(m) >= Sl[m];
                         base = ge ? base : m + 1;
                         n = ge ? half : n - half - 1;
                     }
-                    if (base <= hi) {
-                        int q = base;
-                        while (ns[q] < l) q = ns[q];
-                        w = Xc[(q - 1) * j];
-                    }
+                    if (base <= hi) w = g(base);
                     if (base > lo) w = dmin(w, Sl[base - 1]);
+                } else if (s_dec) {
+                    // descending l': S only grows, stop once it reaches the running min
+                    for (int p = hi; p >= lo; --p) {
+                        const double sv = Sl[p];
+                        if (sv >= w) break;
+                        w = dmin(w, dmax(Xc[(p - 1) * j], sv));
+                    }
                 } else {
                     for (int p = lo; p <= hi; ++p) w = dmin(w, dmax(Xc[(p - 1) * j], Sl[p]));
                 }

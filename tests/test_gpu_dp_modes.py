@@ -195,6 +195,7 @@ def test_crossing_search_combine_identical(early_exit, early):
              + W.c4_batch(6))
     models = [s.to_model() for s in specs]
     prev = _lib.dp_combine(0)
+    assert prev == 2
     try:
         early_exit(True)
         ref = P.spp_many(models)
