@@ -142,7 +142,7 @@ int pp_dp_set_early_exit(int32_t on);
 /* Combine kernel of the per-step DP schedule: 1 = crossing search
  * (combine_bis.cu: bisection for the valley of max(X, S) under a certified
  * monotone stage-term triangle), 0 = exhaustive register tiles, 2 (default) =
- * auto (crossing search for batches of <= 2 instances, where the wavefront is
+ * auto (crossing search for single-instance batches, where the wavefront is
  * latency-bound; tiles above).  Identical results; a performance / test knob.
  * Returns the previous kind. */
 int pp_dp_set_combine(int32_t kind);

@@ -40,6 +40,9 @@ __global__ void k_query(pp_batch b, int n, const int* qi, const int* ql, const i
                         const int* qd, int max_xi, double* w, int* frag, int* feas);
 template <bool SMEM> __global__ void k_rdo(pp_batch b, int resume);
 __global__ void k_rdo_plan(pp_batch b, int round, int predict);
+__global__ void k_rdo_hash(pp_batch b, int dedup);
+__global__ void k_rdo_rep(pp_batch b);
+__global__ void k_rdo_copy(pp_batch b);
 template <bool SMEM> __global__ void k_rdo_cut(pp_batch b);
 template <bool SMEM>
 __global__ void k_min_cut(pp_batch b, int k, const int* verts, int n, unsigned char* in_a, double* weight);
@@ -116,7 +119,7 @@ static const double g_bis_waves = getenv("PP_BIS_WAVES") ? atof(getenv("PP_BIS_W
 static std::atomic<int> g_combine_kind{getenv("PP_COMBINE_BIS") ? atoi(getenv("PP_COMBINE_BIS")) : 2};
 // auto (kind 2): the crossing search for batches of at most this many instances
 // (latency-bound chains), the register tiles above it (throughput)
-static const int g_bis_max_inst = getenv("PP_BIS_MAX_INST") ? atoi(getenv("PP_BIS_MAX_INST")) : 2;
+static const int g_bis_max_inst = getenv("PP_BIS_MAX_INST") ? atoi(getenv("PP_BIS_MAX_INST")) : 1;
 
 static int num_sms() {
     static thread_local int dev = -1, sms = 148;
@@ -173,9 +176,19 @@ int pp_rdo_set_rounds(int32_t rounds) {
     return g_rdo_rounds.exchange(rounds);
 }
 
+// RDO deduplication across a batch (rdo.cu): PP_RDO_DEDUP=0 disables (A/B knob)
+static const int g_rdo_dedup = getenv("PP_RDO_DEDUP") ? atoi(getenv("PP_RDO_DEDUP")) : 1;
+
 int pp_rdo(const pp_batch* b, void* stream) {
     if (b->n_inst <= 0) return PP_OK;
     const int V = b->max_V;
+    const int dedup = g_rdo_dedup && b->n_inst > 1;
+    k_rdo_hash<<<b->n_inst, 32, 0, S(stream)>>>(*b, dedup);
+    PP_CHECK_LAUNCH("k_rdo_hash");
+    if (dedup) {
+        k_rdo_rep<<<b->n_inst, 32, 0, S(stream)>>>(*b);
+        PP_CHECK_LAUNCH("k_rdo_rep");
+    }
     const int in_smem = V <= RDO_SMEM_MAX;
     const int rounds = V >= 2 ? g_rdo_rounds.load() : 0;
     if (rounds > 0) {
@@ -202,6 +215,10 @@ int pp_rdo(const pp_batch* b, void* stream) {
         k_rdo<false><<<b->n_inst, 32 * RDO_WARPS, smem, S(stream)>>>(*b, rounds > 0);
     }
     PP_CHECK_LAUNCH("k_rdo");
+    if (dedup) {
+        k_rdo_copy<<<b->n_inst, 64, 0, S(stream)>>>(*b);
+        PP_CHECK_LAUNCH("k_rdo_copy");
+    }
     return PP_OK;
 }
 

@@ -112,3 +112,37 @@ def test_spp_batch_orders_with_speculation(rounds):
         res = spp_many(W.models_of(specs))
         for s, r in zip(specs, res):
             assert r.device_order == oracle_order(s.gpu_ids, s.links), (s.name, n_rounds)
+
+
+def test_batch_dedup_of_identical_clusters():
+    """A batch that plans one cluster many times (the C3 shape) runs RDO once
+    per distinct bandwidth matrix (k_rdo_hash / k_rdo_rep / k_rdo_copy).
+    Duplicates with different GPU ids, a near-duplicate differing in one
+    bandwidth by one ulp, and a different V of the same data must all get
+    their own correct order."""
+    import math
+    rng = random.Random(7)
+    ids, links = W.two_tier_cluster(4, 4)
+    base = W.c3_gpt96(M=8, L=6, nodes=4, per_node=4)
+    specs = []
+    for k in range(5):
+        s = base.with_m(8 + k)
+        specs.append(s)
+    # same matrix, other (sorted-equivalent) ids: positions, not ids, decide the order
+    shifted = [g + 100 for g in ids]
+    specs.append(W.InstanceSpec("shift", base.fwd, base.bwd, base.param, base.efwd, base.ebwd, shifted,
+                                [(a + 100, b + 100, w) for a, b, w in links], 8))
+    # one ulp off on one pair
+    near = list(links)
+    a, b, w = near[3]
+    near[3] = (a, b, math.nextafter(w, math.inf))
+    specs.append(W.InstanceSpec("near", base.fwd, base.bwd, base.param, base.efwd, base.ebwd, ids, near, 8))
+    # random clusters interleaved
+    for k in range(4):
+        rids = rng.sample(range(1, 500), 16)
+        specs.append(W.InstanceSpec(f"rand{k}", base.fwd, base.bwd, base.param, base.efwd, base.ebwd, rids,
+                                    clique(rids, lambda x, y: math.exp(rng.uniform(20, 25))), 8))
+    specs.append(base.with_m(99))
+    res = spp_many([s.to_model() for s in specs])
+    for s, r in zip(specs, res):
+        assert r.device_order == oracle_order(s.gpu_ids, s.links), s.name
