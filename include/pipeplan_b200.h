@@ -147,6 +147,12 @@ int pp_dp_set_early_exit(int32_t on);
  * Returns the previous kind. */
 int pp_dp_set_combine(int32_t kind);
 
+/* RDO deduplication across a batch (instances with bitwise-equal bandwidth
+ * matrices share one RDO run): 0 off, 1 (default) auto = only for batches of
+ * more than 2 x SMs instances (RDO is latency-bound below that), 2 always.
+ * Identical results; a performance / test knob.  Returns the previous mode. */
+int pp_rdo_set_dedup(int32_t mode);
+
 /* Debug: record the persistent DP's per-task timeline (4 x u64 per task:
  * smid << 32 | kind, fetch, inputs-ready, end; globaltimer ns) into the device
  * buffer d_buf of 4 * cap entries; NULL disables.  Not on the planning path. */

@@ -88,7 +88,8 @@ EXPORTS = ("pp_version", "pp_last_error", "pp_device_count", "pp_layout", "pp_rd
            "pp_pe_sweep", "pp_select", "pp_spp", "pp_prm_query", "pp_simulate", "pp_min_cut",
            "pp_launch_count", "pp_phi", "pp_peak_minmax", "pp_format_trace", "pp_validate_schedule",
            "pp_rdo_set_rounds", "pp_dp_set_persistent", "pp_dp_trace",
-           "pp_dp_set_early_exit", "pp_step_trace", "pp_dp_set_combine")
+           "pp_dp_set_early_exit", "pp_step_trace", "pp_dp_set_combine",
+           "pp_rdo_set_dedup")
 
 _lib = None
 
@@ -140,6 +141,8 @@ def _declare(L):
     L.pp_dp_set_persistent.restype = C.c_int
     L.pp_dp_set_early_exit.argtypes = [i32]
     L.pp_dp_set_early_exit.restype = C.c_int
+    L.pp_rdo_set_dedup.argtypes = [i32]
+    L.pp_rdo_set_dedup.restype = C.c_int
     L.pp_dp_set_combine.argtypes = [i32]
     L.pp_dp_set_combine.restype = C.c_int
     L.pp_step_trace.argtypes = [vp, i32]
@@ -167,6 +170,12 @@ def dp_combine(kind: int) -> int:
     """Per-step combine kernel: 1 crossing search, 0 exhaustive register
     tiles, 2 auto (default).  Returns the previous kind; results are identical."""
     return int(load(require_device=False).pp_dp_set_combine(int(kind)))
+
+
+def rdo_dedup(mode: int) -> int:
+    """RDO deduplication across a batch: 0 off, 1 auto (default), 2 always.
+    Returns the previous mode; orders are identical either way."""
+    return int(load(require_device=False).pp_rdo_set_dedup(int(mode)))
 
 
 def rdo_rounds(rounds: int) -> int:

@@ -176,13 +176,19 @@ int pp_rdo_set_rounds(int32_t rounds) {
     return g_rdo_rounds.exchange(rounds);
 }
 
-// RDO deduplication across a batch (rdo.cu): PP_RDO_DEDUP=0 disables (A/B knob)
-static const int g_rdo_dedup = getenv("PP_RDO_DEDUP") ? atoi(getenv("PP_RDO_DEDUP")) : 1;
+// RDO deduplication across a batch (rdo.cu).  RDO is latency-bound (one CTA per
+// instance), so deduplicating only saves SM time once a batch has more
+// instances than ~2 waves of SMs; below that it is skipped (C3, 12 instances of
+// one cluster: RDO 0.37 ms either way).  PP_RDO_DEDUP: 0 off, 1 auto, 2 always.
+static std::atomic<int> g_rdo_dedup{getenv("PP_RDO_DEDUP") ? atoi(getenv("PP_RDO_DEDUP")) : 1};
+
+int pp_rdo_set_dedup(int32_t mode) { return g_rdo_dedup.exchange(mode < 0 || mode > 2 ? 1 : mode); }
 
 int pp_rdo(const pp_batch* b, void* stream) {
     if (b->n_inst <= 0) return PP_OK;
     const int V = b->max_V;
-    const int dedup = g_rdo_dedup && b->n_inst > 1;
+    const int dm = g_rdo_dedup.load();
+    const int dedup = b->n_inst > 1 && (dm == 2 || (dm == 1 && b->n_inst > 2 * num_sms()));
     k_rdo_hash<<<b->n_inst, 32, 0, S(stream)>>>(*b, dedup);
     PP_CHECK_LAUNCH("k_rdo_hash");
     if (dedup) {

@@ -252,23 +252,33 @@ __global__ void __launch_bounds__(32) k_rdo_hash(pp_batch b, int dedup) {
         k->rep = blockIdx.x;
     }
 }
-// one warp per instance k: the first k' < k with the same V, hash and matrix bits
+// one warp per instance k: the first k' < k with the same V, hash and matrix
+// bits (32 candidate hashes per iteration, then a bitwise check of each hit)
 __global__ void __launch_bounds__(32) k_rdo_rep(pp_batch b) {
-    const int k = blockIdx.x;
+    const int k = blockIdx.x, lane = threadIdx.x;
     const pp_instance I = b.inst[k];
     if (I.flags & PP_GIVEN_ORDER) return;
     const int V = I.V;
     const unsigned long long hk = rdo_key(b, I)->hash;
     const unsigned long long* wk = reinterpret_cast<const unsigned long long*>(b.bw + I.bw_off);
-    for (int q = 0; q < k; ++q) {
-        const pp_instance J = b.inst[q];
-        if (J.V != V || (J.flags & PP_GIVEN_ORDER) || rdo_key(b, J)->hash != hk) continue;
-        const unsigned long long* wq = reinterpret_cast<const unsigned long long*>(b.bw + J.bw_off);
-        bool diff = false;
-        for (int e = threadIdx.x; e < V * V; e += 32) diff |= wq[e] != wk[e];
-        if (!__any_sync(0xffffffffu, diff)) {
-            if (threadIdx.x == 0) rdo_key(b, I)->rep = q;
-            return;
+    for (int q0 = 0; q0 < k; q0 += 32) {
+        const int q = q0 + lane;
+        bool hit = false;
+        if (q < k) {
+            const pp_instance J = b.inst[q];
+            hit = J.V == V && !(J.flags & PP_GIVEN_ORDER) && rdo_key(b, J)->hash == hk;
+        }
+        unsigned m = __ballot_sync(0xffffffffu, hit);
+        while (m) {
+            const int qq = q0 + __ffs(m) - 1;
+            m &= m - 1;
+            const unsigned long long* wq = reinterpret_cast<const unsigned long long*>(b.bw + b.inst[qq].bw_off);
+            bool diff = false;
+            for (int e = lane; e < V * V; e += 32) diff |= wq[e] != wk[e];
+            if (!__any_sync(0xffffffffu, diff)) {
+                if (lane == 0) rdo_key(b, I)->rep = qq;
+                return;
+            }
         }
     }
 }

@@ -143,6 +143,10 @@ def test_batch_dedup_of_identical_clusters():
         specs.append(W.InstanceSpec(f"rand{k}", base.fwd, base.bwd, base.param, base.efwd, base.ebwd, rids,
                                     clique(rids, lambda x, y: math.exp(rng.uniform(20, 25))), 8))
     specs.append(base.with_m(99))
-    res = spp_many([s.to_model() for s in specs])
+    prev = _lib.rdo_dedup(2)
+    try:
+        res = spp_many([s.to_model() for s in specs])
+    finally:
+        _lib.rdo_dedup(prev)
     for s, r in zip(specs, res):
         assert r.device_order == oracle_order(s.gpu_ids, s.links), s.name
