@@ -200,15 +200,19 @@ int pp_rdo(const pp_batch* b, void* stream) {
     if (rounds > 0) {
         const size_t plan_smem = sizeof(int) * (size_t)V * (3 + RDO_WARPS);
         const size_t cut_smem = (in_smem ? sizeof(double) * V * V : 0) + sizeof(int) * V + V + 16;
+        // a batch above RDO_SMEM_MAX may still hold instances below it: their cuts run
+        // in the shared-memory variant (k_rdo_cut<false> has no scratch for them)
+        const int vs = V < RDO_SMEM_MAX ? V : RDO_SMEM_MAX;
+        const size_t cut_smem_s = sizeof(double) * vs * vs + sizeof(int) * vs + vs + 16;
         cudaFuncSetAttribute(k_rdo_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan_smem);
-        if (in_smem) cudaFuncSetAttribute(k_rdo_cut<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cut_smem);
+        cudaFuncSetAttribute(k_rdo_cut<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cut_smem_s);
         const dim3 gc(b->n_inst, V - 1);
         for (int r = 0; r <= rounds; ++r) {
             k_rdo_plan<<<b->n_inst, 32 * RDO_WARPS, plan_smem, S(stream)>>>(*b, r, r < rounds);
             PP_CHECK_LAUNCH("k_rdo_plan");
             if (r == rounds) break;
-            if (in_smem) k_rdo_cut<true><<<gc, 32, cut_smem, S(stream)>>>(*b);
-            else k_rdo_cut<false><<<gc, 32, cut_smem, S(stream)>>>(*b);
+            k_rdo_cut<true><<<gc, 32, cut_smem_s, S(stream)>>>(*b);
+            if (!in_smem) k_rdo_cut<false><<<gc, 32, cut_smem, S(stream)>>>(*b);
             PP_CHECK_LAUNCH("k_rdo_cut");
         }
     }

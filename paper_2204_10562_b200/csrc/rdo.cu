@@ -399,6 +399,9 @@ __global__ void __launch_bounds__(32) k_rdo_cut(pp_batch b) {
     const pp_instance I = b.inst[blockIdx.x];
     if (rdo_skip(b, I, blockIdx.x)) return;
     const int V = I.V;
+    // the global-memory variant's per-item scratch (rdo_iw) exists only for
+    // V > RDO_SMEM_MAX: a mixed batch runs both variants, each on its instances
+    if ((V <= RDO_SMEM_MAX) != SMEM) return;
     const RdoState st = rdo_spec_state(b, I);
     const int item = blockIdx.y;
     if (item >= st.cnt[0]) return;
