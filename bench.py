@@ -288,16 +288,19 @@ def run_ours(args):
     best_peak = live_minmax_peak(dev, stream)
     dp_ops = 2 * sum(t_fact(s.L, s.V) for s in specs)   # one max + one min per factored candidate
     dp_achieved = dp_ops / (phase["dp"] / 1e3)
-    traffic = None
-    tpath = os.path.join(REPO, "profiles", "ncu_dp_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_step")
-        except (OSError, ValueError):
-            traffic = None
+    traffic, traffic_src = None, None
+    for name in ("r02_dp_traffic_warm.json", "ncu_dp_traffic.json"):   # newest measurement first
+        tpath = os.path.join(REPO, "profiles", name)
+        if os.path.exists(tpath):
+            try:
+                tj = json.load(open(tpath))
+                traffic, traffic_src = tj.get("dram_bytes_per_step"), f"profiles/{name}: {tj.get('what', '')}"
+                break
+            except (OSError, ValueError):
+                pass
     roofline = {"bound": "fp64_minmax", "kernel": "pp_prm (k_combine + k_expand wavefront)",
                 "achieved": dp_achieved / 1e12, "peak": best_peak / 1e12, "unit": "Tminmax/s",
-                "frac": dp_achieved / best_peak, "traffic": traffic,
+                "frac": dp_achieved / best_peak, "traffic": traffic, "traffic_source": traffic_src,
                 "peak_source": "k_peak_minmax measured live (no fp64 min/max figure in MEASURED_PEAKS.json)",
                 "algorithmic_ops_per_step": dp_ops,
                 "phase_ms": phase}
@@ -346,6 +349,8 @@ def run_ours(args):
     cpu = None
     if not args.no_cpu_baseline:
         cpu = cpu_baseline(specs, args.cpu_threads)
+        cpu["python_reference"] = python_reference_timing()
+        cpu["host"] = host_info()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": max_ms / args.steps, "higher_is_better": True,
@@ -408,6 +413,38 @@ def cpu_baseline(specs, threads=0):
                       "(SURVEY.md §6 extrapolation), not runnable on the GPU box"}
 
 
+def python_reference_timing():
+    """The untouched Python reference (pipeplan.spp from baseline/_ref, staged by
+    tools/stage_reference.py), timed in-process on one core for C1 and C2
+    (single-threaded like the reference).  None when the staged
+    copy is absent.  Measured in a subprocess so its `pipeplan` never meets ours."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isfile(os.path.join(ref, "pipeplan", "planner.py")):
+        return None
+    code = r"""
+import json, statistics, sys, time
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[2])
+import pipeplan as P
+from paper_2204_10562_b200 import workloads as W
+out = {"python": sys.version.split()[0], "module": P.__file__}
+for name, spec, reps in (("C1", W.c1_vgg19(), 7), ("C2", W.c2_bert24(), 3)):
+    layers = tuple(P.LayerProfile(k + 1, f, b, p) for k, (f, b, p) in enumerate(zip(spec.fwd, spec.bwd, spec.param)))
+    edges = tuple(P.InterLayerEdge(k + 1, k + 2, a, b) for k, (a, b) in enumerate(zip(spec.efwd, spec.ebwd)))
+    prof = P.ModelProfile(spec.name, 1, layers, edges)
+    clu = P.make_cluster(spec.gpu_ids, spec.links)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter(); P.spp(prof, clu, spec.M); ts.append(time.perf_counter() - t0)
+    out[name] = {"p50_s": statistics.median(ts), "reps": reps}
+print(json.dumps(out))
+"""
+    try:
+        r = subprocess.run([sys.executable, "-c", code, ref, REPO], capture_output=True, text=True, timeout=300)
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except (subprocess.SubprocessError, ValueError, IndexError):
+        return None
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -435,7 +472,8 @@ def run_reference(args):
         "config": {"workload": WORKLOAD, "layers": 96, "gpus_in_topology": 64,
                    "step": f"{nt} C3 instances, one per host thread"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nt, "kind": "port",
-                         "sample": f"{nt} C3 instances per step x {args.steps} steps"},
+                         "sample": f"{nt} C3 instances per step x {args.steps} steps",
+                         "python_reference": python_reference_timing(), "host": host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

@@ -5,6 +5,7 @@ from collections import defaultdict
 
 src, dst = sys.argv[1], sys.argv[2]
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+warm = len(sys.argv) > 4 and sys.argv[4] == "warm"   # captured with --cache-control none
 rows = [r for r in csv.reader(open(src)) if r and not r[0].startswith("==")]
 hdr = rows[0]
 ki, mi, vi = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
@@ -25,7 +26,8 @@ rd = sum(p["read"] for k, p in per.items() if dp.match(k)) / steps
 wr = sum(p["write"] for k, p in per.items() if dp.match(k)) / steps
 out = {"what": "DRAM bytes (read+write) of the DP phase (pp_prm graph: prep, base, sdedup, stab, expand, combine, "
                "backtrack kernels) per C3 12-instance step; ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum "
-               "(ncu flushes caches per kernel: cold-cache upper bound)",
+               + ("--cache-control none (caches NOT flushed between kernels: the warm traffic of a steady-state step, "
+                  "kernels serialised)" if warm else "(ncu flushes caches per kernel: cold-cache upper bound)"),
        "dram_bytes_per_step": rd + wr, "read": rd, "write": wr,
        "per_kernel": {k: {kk: (vv / steps if kk != "launches" else vv // steps) for kk, vv in p.items()}
                       for k, p in sorted(per.items(), key=lambda kv: -kv[1]["time_ns"])}}
