@@ -34,6 +34,7 @@ __global__ void k_combine_s(pp_batch b, int j);
 __global__ void k_dp_reset(pp_batch b);
 __global__ void k_dp_persist(pp_batch b);
 __global__ void k_dp_inst(pp_batch b, int smem_doubles);
+__global__ void k_dp_inst2(pp_batch b);
 __global__ void k_dp_cluster(pp_batch b);
 __global__ void k_backtrack(pp_batch b);
 __global__ void k_query(pp_batch b, int n, const int* qi, const int* ql, const int* qx, const int* qr,
@@ -276,7 +277,10 @@ static std::atomic<int> g_dp_persist{2};
 
 int pp_dp_set_persistent(int32_t mode) { return g_dp_persist.exchange(mode < 0 || mode > 4 ? 2 : mode); }
 
-static int prm_prep(const pp_batch* b, void* stream);
+static int prm_prep(const pp_batch* b, void* stream, bool tables = true);
+// instance-per-CTA DP kernel: 2 = k_dp_inst2 (operands built in shared memory)
+// when its footprint fits, 1 = k_dp_inst (table-staged); PP_DP_INST env
+static const int g_dp_inst_kind = getenv("PP_DP_INST") ? atoi(getenv("PP_DP_INST")) : 2;
 
 // cluster size of the cluster-per-instance schedule (PP_DP_CLUSTER env: 2..16)
 static int read_cluster_size() {
@@ -330,6 +334,19 @@ static int prm_cluster(const pp_batch* b, void* stream) {
 static int prm_inst(const pp_batch* b, void* stream) {
     const int maxL = b->max_L, maxV = b->max_V;
     int rc;
+    // k_dp_inst2: one CTA per instance with every operand built in shared memory
+    // (<= 113 KB: two CTAs per SM); the triangle tables are then never built
+    const size_t smem2 = sizeof(double) * (size_t)dp_inst2_smem_doubles(maxL, maxV);
+    if (g_dp_inst_kind == 2 && maxV > 1 && smem2 <= 113 * 1024) {
+        if ((rc = prm_prep(b, stream, false))) return rc;
+        cudaFuncSetAttribute(k_dp_inst2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+        k_dp_inst2<<<b->n_inst, DI2_T, smem2, S(stream)>>>(*b);
+        PP_CHECK_LAUNCH("k_dp_inst2");
+        dim3 gb(b->n_inst, maxV);
+        k_backtrack<<<gb, 32, 0, S(stream)>>>(*b);
+        PP_CHECK_LAUNCH("k_backtrack");
+        return PP_OK;
+    }
     if ((rc = prm_prep(b, stream))) return rc;
     if (maxV > 1) {
         // smallest chunk: one expand row at j = V-1 or one combine item at j = V-1
@@ -571,7 +588,7 @@ static int prm_steps_graph(const pp_batch* b, void* stream) {
 
 // Tables every DP schedule needs: prep, base rows, and (shared-memory path)
 // the deduplicated stage-term triangles.
-static int prm_prep(const pp_batch* b, void* stream) {
+static int prm_prep(const pp_batch* b, void* stream, bool tables) {
     const int maxL = b->max_L, maxV = b->max_V;
     dim3 gp(b->n_inst, maxL > maxV ? maxL : maxV);
     k_prep<<<gp, 128, maxV <= PREP_CM_MAX ? sizeof(double) * maxV * maxV : 0, S(stream)>>>(*b);
@@ -579,7 +596,7 @@ static int prm_prep(const pp_batch* b, void* stream) {
     dim3 gbase(b->n_inst, maxL > maxV ? maxL : maxV);
     k_base<<<gbase, 128, 0, S(stream)>>>(*b, !(maxL <= SR_MAX && maxV <= SR_MAX));
     PP_CHECK_LAUNCH("k_base");
-    if (maxL <= SR_MAX && maxV <= SR_MAX) {
+    if (tables && maxL <= SR_MAX && maxV <= SR_MAX) {
         k_sdedup<<<dim3(b->n_inst, (maxV - 1 + 7) / 8 > 0 ? (maxV - 1 + 7) / 8 : 1), 256, 0, S(stream)>>>(*b);
         PP_CHECK_LAUNCH("k_sdedup");
         if (maxV > 1 && maxL > 1) {

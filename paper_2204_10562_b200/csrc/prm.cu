@@ -1435,7 +1435,10 @@ __device__ void dp_walk(const pp_batch& b, const pp_instance& I, int l, int x, i
     while (x >= 2) {
         const int j = i - r;
         const double* X = ws + lay.X + X_base(L, i, r);
-        const double* St = tables ? ws + lay.Stab + (int64_t)sidx[(r - 1) * V + (i - 1)] * tri : nullptr;
+        // slot -1: the batch built no triangle for this item (k_dp_inst2 computes
+        // its triangles in shared memory): the scalar stage_term, same expression
+        const int slot = tables ? sidx[(r - 1) * V + (i - 1)] : -1;
+        const double* St = slot >= 0 ? ws + lay.Stab + (int64_t)slot * tri : nullptr;
         int lp = -1;
         for (int base = x - 1; base <= l - 1 && lp < 0; base += 32) {
             const int c = base + lane;

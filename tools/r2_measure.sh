@@ -12,8 +12,12 @@ ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum 
 python tools/dp_traffic.py gpurun_out/r2m_traffic_cold.csv profiles/r02_dp_traffic_cold.json 1
 for k in k_combine_s_p:120 k_expand_m_p:60 k_rdo_cut:0 k_rdo:0 k_pe_sweep_w:0 k_event_merge:0 k_select:0 k_backtrack_p:0 k_stab_big_p:0; do
   name=${k%%:*}; skip=${k##*:}
-  ncu --set full --import-source on --clock-control none -k regex:"${name}" -s $skip -c 1 -o gpurun_out/r2m_ncu_${name} python bench.py --profile-steps 1 > /dev/null 2>&1
+  ncu --set full --import-source on --clock-control none -k regex:"${name}" -s $skip -c 1 -o /tmp/r2m_ncu_${name} python bench.py --profile-steps 1 > /dev/null 2>&1
+  (python tools/summarize_ncu.py /tmp/r2m_ncu_${name}.ncu-rep; python tools/ncu_lines.py /tmp/r2m_ncu_${name}.ncu-rep 25) > gpurun_out/r2m_ncu_${name}.txt 2>&1
 done
+bash tools/prof_c4.sh > /dev/null 2>&1
+(python tools/summarize_ncu.py gpurun_out/dpinst_c4.ncu-rep; python tools/ncu_lines.py gpurun_out/dpinst_c4.ncu-rep 25) > gpurun_out/r2m_ncu_dp_inst_c4.txt 2>&1
+rm -f gpurun_out/*.ncu-rep
 python tools/step_trace.py 12 > gpurun_out/r2m_trace12.txt 2>&1
 python tools/step_trace.py 1 > gpurun_out/r2m_trace1.txt 2>&1
 (python tools/phases.py c3 1; python tools/phases.py c3 12; python tools/phases.py c4) > gpurun_out/r2m_phases.txt 2>&1
