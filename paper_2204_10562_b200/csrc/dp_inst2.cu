@@ -42,11 +42,13 @@ __host__ __device__ __forceinline__ void dp_inst2_regions(int L, int V, int64_t&
         xs = lm * j * nr > xs ? lm * j * nr : xs;
     }
 }
-// prefix (L+1), psum (L x L), minpair (V x V), Mp (L), R1, XS
+// prefix (L+1), psum (L x L), minpair (V x V), Mp (L), R1, XS, then the packed
+// triangle's (l', l) of every offset (2 bytes each)
 __host__ __device__ __forceinline__ int64_t dp_inst2_smem_doubles(int L, int V) {
     int64_t r1, xs;
     dp_inst2_regions(L, V, r1, xs);
-    return (L + 1) + (int64_t)L * L + (int64_t)V * V + L + r1 + xs;
+    const int64_t tri = (int64_t)(L > 1 ? L - 1 : 0) * L / 2;
+    return (L + 1) + (int64_t)L * L + (int64_t)V * V + L + r1 + xs + (2 * tri + 7) / 8;
 }
 
 __global__ void __launch_bounds__(DI2_T, 2) k_dp_inst2(pp_batch b) {
@@ -72,13 +74,16 @@ __global__ void __launch_bounds__(DI2_T, 2) k_dp_inst2(pp_batch b) {
     int64_t r1n, xsn;
     dp_inst2_regions(L, V, r1n, xsn);
     double* XS = R1 + r1n;
-    const int lane = t & 31, warp = t >> 5, nw = nt >> 5;
+    unsigned char* tlp = reinterpret_cast<unsigned char*>(XS + xsn);   // offset o -> l' (then l)
+    unsigned char* tl = tlp + tri;
     for (int e = t; e <= L; e += nt) prefix[e] = ws[lay.prefix + e];
     for (int e = t; e < L * L; e += nt) psum[e] = ws[lay.psum + e];
     for (int e = t; e < V * V; e += nt) minpair[e] = ws[lay.minpair + e];
     for (int lp = 1 + t; lp < L; lp += nt) {
-        trio[lp] = (lp - 1) * L - (lp - 1) * lp / 2;
+        const int o0 = (lp - 1) * L - (lp - 1) * lp / 2;
+        trio[lp] = o0;
         Mp[lp] = (double)M * (b.efwd[I.layer_off + lp - 1] + b.ebwd[I.layer_off + lp - 1]);   // partition.py:131,137
+        for (int l = lp + 1; l <= L; ++l) { tlp[o0 + l - lp - 1] = (unsigned char)lp; tl[o0 + l - lp - 1] = (unsigned char)l; }
     }
     // no per-instance triangle table exists: the backtrack computes its stage terms
     int* sidx = reinterpret_cast<int*>(ws + lay.sidx);
@@ -155,30 +160,26 @@ __global__ void __launch_bounds__(DI2_T, 2) k_dp_inst2(pp_batch b) {
         const int r_hi = allow ? nr : 1;   // without replication only r = 1 holds values (partition.py:103-104)
         // stage-term triangles S(l', l) of the items (k_stab's expression, cost.py:99)
         for (int q = t; q < r_hi; q += nt) s_mono[q] = 1;
-        // one warp per (item, row l'), lanes over l = l'+1..L:
+        // every (item, l', l) of the step's triangles, one element per thread:
         //   S(l', l) = (M * span(l'+1, l)) / r + ((2 (r-1)) * P(l'+1..l)) / (r * minpair)
-        for (int u = warp; u < r_hi * lm; u += nw) {
-            const int q = u / lm, lp = u - q * lm + 1;
+        // (k_stab / stage_term's expression, cost.py:99, partition.py:127-129)
+        const float rtri = 1.0f / (float)tri;
+        for (int e = t; e < r_hi * tri; e += nt) {
+            int q, o;
+            divmod_small(e, tri, rtri, q, o);
+            const int lp = tlp[o], l = tl[o];
             const int r = q + 1, i = j + r;
-            double* Srow = R1 + (int64_t)q * tri + trio[lp] - lp - 1;   // Srow[l] = S(l', l)
-            const double pl = prefix[lp], den = (double)r * minpair[(i - r) * V + (i - 1)];
-            const double num = 2.0 * (double)(r - 1);
-            for (int l = lp + 1 + lane; l <= L; l += 32) {
-                double sv = (double)M * (prefix[l] - pl) / (double)r;
-                if (r > 1) sv += num * psum[lp * L + (l - 1)] / den;
-                Srow[l] = sv;
-            }
+            double sv = (double)M * (prefix[l] - prefix[lp]) / (double)r;
+            if (r > 1) sv += 2.0 * (double)(r - 1) * psum[lp * L + (l - 1)] / ((double)r * minpair[(i - r) * V + (i - 1)]);
+            R1[e] = sv;
         }
         __syncthreads();
         if (g_combine_early_exit)   // certificate: non-increasing in l' (S(l', l) >= S(l'+1, l))
-            for (int u = warp; u < r_hi * lm; u += nw) {
-                const int q = u / lm, lp = u - q * lm + 1;
-                if (lp + 1 >= L) continue;
-                const double* S0 = R1 + (int64_t)q * tri + trio[lp] - lp - 1;
-                const double* S1 = R1 + (int64_t)q * tri + trio[lp + 1] - lp - 2;
-                bool bad = false;
-                for (int l = lp + 2 + lane; l <= L; l += 32) bad |= !(S0[l] >= S1[l]);
-                if (__any_sync(0xffffffffu, bad) && lane == 0) s_mono[q] = 0;
+            for (int e = t; e < r_hi * tri; e += nt) {
+                int q, o;
+                divmod_small(e, tri, rtri, q, o);
+                const int lp = tlp[o], l = tl[o];
+                if (l >= lp + 2 && !(R1[e] >= R1[(int64_t)q * tri + trio[lp + 1] + (l - lp - 2)])) s_mono[q] = 0;
             }
         __syncthreads();
         {
