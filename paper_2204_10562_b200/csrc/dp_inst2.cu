@@ -51,6 +51,89 @@ __host__ __device__ __forceinline__ int64_t dp_inst2_smem_doubles(int L, int V) 
     return (L + 1) + (int64_t)L * L + (int64_t)V * V + L + r1 + xs + (2 * tri + 7) / 8;
 }
 
+// E(j) tiles: TXI columns xi x TRR targets r per thread and row l'; K = r'
+template <int TXI, int TRR>
+__device__ __forceinline__ void dp_inst2_expand(const double* A, const double* B, double* XS, double* Xg, int L,
+                                                int j, int nr) {
+    const int lm = L - 1, jj = j * j, jn = j * nr;
+    const int ntx = (j + TXI - 1) / TXI, ntr = (nr + TRR - 1) / TRR, per_row = ntx * ntr;
+    for (int id = threadIdx.x; id < lm * per_row; id += blockDim.x) {
+        const int k = id / per_row, rem = id - k * per_row;   // row l' = k + 1
+        const int tr = rem / ntx, tx = rem - tr * ntx;
+        const int xi0 = 2 + TXI * tx, r0 = 1 + TRR * tr, lp = k + 1;
+        double acc[TXI][TRR];
+#pragma unroll
+        for (int a = 0; a < TXI; ++a)
+#pragma unroll
+            for (int c = 0; c < TRR; ++c) acc[a][c] = PP_INF;
+        if (xi0 - 1 <= lp) {   // else W_j(l', xi', .) = inf for every xi' >= xi0 - 1 > l'
+            const int kend = j - xi0 + 2;   // W_j(l', xi-1, r') = inf for r' > j - xi + 2
+            int xa[TXI], rc[TRR];
+#pragma unroll
+            for (int a = 0; a < TXI; ++a) xa[a] = min(xi0 - 1 + a, j) - 1;
+#pragma unroll
+            for (int c = 0; c < TRR; ++c) rc[c] = min(r0 + c, nr) - 1;
+            const double* Ar = A + (int64_t)k * jj;
+            const double* Br = B + (int64_t)k * jn;
+            for (int rp = 1; rp <= kend; ++rp) {
+                double p[TXI], q[TRR];
+#pragma unroll
+                for (int a = 0; a < TXI; ++a) p[a] = Ar[xa[a]];
+#pragma unroll
+                for (int c = 0; c < TRR; ++c) q[c] = Br[rc[c]];
+#pragma unroll
+                for (int a = 0; a < TXI; ++a)
+#pragma unroll
+                    for (int c = 0; c < TRR; ++c) acc[a][c] = dmin(acc[a][c], dmax(p[a], q[c]));
+                Ar += j;
+                Br += nr;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < TRR; ++c) {
+            const int r = r0 + c;
+            if (r > nr) continue;
+            double* xs = XS + ((int64_t)(r - 1) * lm + k) * j;
+            double* xg = Xg + X_base(L, j + r, r) + (int64_t)k * j;
+#pragma unroll
+            for (int a = 0; a < TXI; ++a) {
+                const int xi = xi0 + a;
+                if (xi <= j + 1) { xs[xi - 2] = acc[a][c]; xg[xi - 2] = acc[a][c]; }
+            }
+        }
+    }
+}
+
+// C(j) tiles: TL rows x TX columns per thread over every item of the step
+// (TX shrinks with j so few-column steps do not fold padded columns)
+template <int TX, int TL>
+__device__ __forceinline__ void dp_inst2_combine(double* Wg, const double* R1, const double* XS, const int* trio,
+                                                 const int* s_mono, int L, int j, int r_hi, int tri) {
+    const int lm = L - 1;
+    const int ntl = (L + TL - 1) / TL, ntx = (j + TX - 1) / TX, nti = ntl * ntx;
+    for (int id = threadIdx.x; id < r_hi * nti; id += blockDim.x) {
+        const int q = id / nti, rem = id - q * nti;
+        const int r = q + 1, i = j + r;
+        const int tl = rem / ntx, tx = rem - tl * ntx;
+        const int l0 = 1 + TL * tl, xi0 = 2 + TX * tx;
+        const double* Stri = R1 + (int64_t)q * tri;
+        const double* Xs = XS + (int64_t)q * lm * j;
+        double acc[TL][TX];
+        if (g_combine_early_exit && s_mono[q]) combine_tile_s_desc<TX, TL>(Stri, trio, Xs, L, j, l0, xi0, 1, L - 1, acc);
+        else combine_tile_s<TX, TL>(Stri, trio, Xs, L, j, l0, xi0, 1, L - 1, acc);
+        double* Wi = Wg + W_base(L, i);
+#pragma unroll
+        for (int a = 0; a < TL; ++a) {
+            const int l = l0 + a;
+            if (l > L) continue;
+            double* row = Wi + ((int64_t)(l - 1) * i + (r - 1)) * i;
+#pragma unroll
+            for (int c = 0; c < TX; ++c)
+                if (xi0 + c <= j + 1) row[xi0 + c - 1] = acc[a][c];
+        }
+    }
+}
+
 __global__ void __launch_bounds__(DI2_T, 2) k_dp_inst2(pp_batch b) {
     const pp_instance I = b.inst[blockIdx.x];
     const int L = I.L, V = I.V, M = I.M;
@@ -89,6 +172,17 @@ __global__ void __launch_bounds__(DI2_T, 2) k_dp_inst2(pp_batch b) {
     int* sidx = reinterpret_cast<int*>(ws + lay.sidx);
     for (int e = t; e < V * V; e += nt) sidx[e] = -1;
     __syncthreads();
+    // T1(r, l', l) = (M * span(l'+1, l)) / r, the i-independent half of every stage
+    // term (k_base's expression), once per instance for r = 1..V-1 (packed
+    // triangles, the instance's T1 region; L2-resident while this CTA runs)
+    double* T1 = ws + lay.T1;
+    for (int e = t; e < (V - 1) * tri; e += nt) {
+        int q, o;
+        divmod_small(e, tri, 1.0f / (float)tri, q, o);
+        const int lp = tlp[o], l = tl[o];
+        T1[e] = (double)M * (prefix[l] - prefix[lp]) / (double)(q + 1);
+    }
+    __syncthreads();
     for (int j = 1; j < V; ++j) {
         const int nr = V - j, jj = j * j;
         // ------------------------------------------------------------ E(j)
@@ -113,47 +207,13 @@ __global__ void __launch_bounds__(DI2_T, 2) k_dp_inst2(pp_batch b) {
                 B[e] = Mp[row + 1] / ((double)((rp + 1) * r) * cross[cross_idx(V, j + r, r, rp + 1)]);
             }
             __syncthreads();
-            const int ntx = (j + 3) >> 2, ntr = (nr + 3) >> 2, per_row = ntx * ntr;
-            for (int id = t; id < lm * per_row; id += nt) {
-                const int k = id / per_row, rem = id - k * per_row;   // row l' = k + 1
-                const int tr = rem / ntx, tx = rem - tr * ntx;
-                const int xi0 = 2 + 4 * tx, r0 = 1 + 4 * tr, lp = k + 1;
-                double acc[4][4];
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) acc[a][c] = PP_INF;
-                if (xi0 - 1 <= lp) {   // else W_j(l', xi', .) = inf for every xi' >= xi0 - 1 > l'
-                    const int kend = j - xi0 + 2;   // W_j(l', xi-1, r') = inf for r' > j - xi + 2
-                    const int xa[4] = {min(xi0 - 1, j) - 1, min(xi0, j) - 1, min(xi0 + 1, j) - 1, min(xi0 + 2, j) - 1};
-                    const int rc[4] = {min(r0, nr) - 1, min(r0 + 1, nr) - 1, min(r0 + 2, nr) - 1, min(r0 + 3, nr) - 1};
-                    const double* Ar = A + (int64_t)k * jj;
-                    const double* Br = B + (int64_t)k * jn;
-                    for (int rp = 1; rp <= kend; ++rp) {
-                        double p[4], q[4];
-#pragma unroll
-                        for (int a = 0; a < 4; ++a) { p[a] = Ar[xa[a]]; q[a] = Br[rc[a]]; }
-#pragma unroll
-                        for (int a = 0; a < 4; ++a)
-#pragma unroll
-                            for (int c = 0; c < 4; ++c) acc[a][c] = dmin(acc[a][c], dmax(p[a], q[c]));
-                        Ar += j;
-                        Br += nr;
-                    }
-                }
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const int r = r0 + c;
-                    if (r > nr) continue;
-                    double* xs = XS + ((int64_t)(r - 1) * lm + k) * j;
-                    double* xg = Xg + X_base(L, j + r, r) + (int64_t)k * j;
-#pragma unroll
-                    for (int a = 0; a < 4; ++a) {
-                        const int xi = xi0 + a;
-                        if (xi <= j + 1) { xs[xi - 2] = acc[a][c]; xg[xi - 2] = acc[a][c]; }
-                    }
-                }
-            }
+            // tile shape by the step's column / target counts (no folds of padding)
+            if (j == 1) dp_inst2_expand<1, 8>(A, B, XS, Xg, L, j, nr);
+            else if (nr <= 2) {
+                if (j >= 8) dp_inst2_expand<8, 2>(A, B, XS, Xg, L, j, nr);
+                else dp_inst2_expand<4, 2>(A, B, XS, Xg, L, j, nr);
+            } else if (j <= 3) dp_inst2_expand<2, 4>(A, B, XS, Xg, L, j, nr);
+            else dp_inst2_expand<4, 4>(A, B, XS, Xg, L, j, nr);
             __syncthreads();
         }
         // ------------------------------------------------------------ C(j)
@@ -169,7 +229,7 @@ __global__ void __launch_bounds__(DI2_T, 2) k_dp_inst2(pp_batch b) {
             divmod_small(e, tri, rtri, q, o);
             const int lp = tlp[o], l = tl[o];
             const int r = q + 1, i = j + r;
-            double sv = (double)M * (prefix[l] - prefix[lp]) / (double)r;
+            double sv = T1[(int64_t)q * tri + o];
             if (r > 1) sv += 2.0 * (double)(r - 1) * psum[lp * L + (l - 1)] / ((double)r * minpair[(i - r) * V + (i - 1)]);
             R1[e] = sv;
         }
@@ -182,31 +242,9 @@ __global__ void __launch_bounds__(DI2_T, 2) k_dp_inst2(pp_batch b) {
                 if (l >= lp + 2 && !(R1[e] >= R1[(int64_t)q * tri + trio[lp + 1] + (l - lp - 2)])) s_mono[q] = 0;
             }
         __syncthreads();
-        {
-            constexpr int TX = 4, TL = 2;
-            const int ntl = (L + TL - 1) / TL, ntx = (j + TX - 1) / TX, nti = ntl * ntx;
-            for (int id = t; id < r_hi * nti; id += nt) {
-                const int q = id / nti, rem = id - q * nti;
-                const int r = q + 1, i = j + r;
-                const int tl = rem / ntx, tx = rem - tl * ntx;
-                const int l0 = 1 + TL * tl, xi0 = 2 + TX * tx;
-                const double* Stri = R1 + (int64_t)q * tri;
-                const double* Xs = XS + (int64_t)q * lm * j;
-                double acc[TL][TX];
-                if (g_combine_early_exit && s_mono[q]) combine_tile_s_desc<TX, TL>(Stri, trio, Xs, L, j, l0, xi0, 1, L - 1, acc);
-                else combine_tile_s<TX, TL>(Stri, trio, Xs, L, j, l0, xi0, 1, L - 1, acc);
-                double* Wi = Wg + W_base(L, i);
-#pragma unroll
-                for (int a = 0; a < TL; ++a) {
-                    const int l = l0 + a;
-                    if (l > L) continue;
-                    double* row = Wi + ((int64_t)(l - 1) * i + (r - 1)) * i;
-#pragma unroll
-                    for (int c = 0; c < TX; ++c)
-                        if (xi0 + c <= j + 1) row[xi0 + c - 1] = acc[a][c];
-                }
-            }
-        }
+        if (j >= 4) dp_inst2_combine<4, 2>(Wg, R1, XS, trio, s_mono, L, j, r_hi, tri);
+        else if (j >= 2) dp_inst2_combine<2, 4>(Wg, R1, XS, trio, s_mono, L, j, r_hi, tri);
+        else dp_inst2_combine<1, 8>(Wg, R1, XS, trio, s_mono, L, j, r_hi, tri);
         __syncthreads();   // W_{j+1} complete (its last item, r = 1, was just written) before E(j+1)
     }
 }
