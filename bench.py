@@ -576,7 +576,7 @@ def run_secondary(args):
                 "e2e": {"value": n_total * len(e2e) / e2e_s, "unit": "instances/s",
                         "h2d_bytes_per_step": db.h2d_bytes(), "d2h_bytes_per_step": db.d2h_bytes(),
                         "api": "paper_2204_10562_b200.spp_many"},
-                "roofline": {"bound": "fp64_minmax", "kernel": "k_dp_inst (instance-per-CTA DP)",
+                "roofline": {"bound": "fp64_minmax", "kernel": "k_dp_inst2 (instance-per-CTA DP, operands in shared memory)",
                              "achieved": dp_rate / 1e12, "peak": peak / 1e12, "unit": "Tminmax/s",
                              "frac": dp_rate / peak, "traffic": None, "algorithmic_ops_per_step": dp_ops,
                              "phase_ms": phase, "peak_source": "k_peak_minmax measured live"},
