@@ -784,6 +784,55 @@ __global__ void __launch_bounds__(CD_T, 2) k_combine_diag(pp_batch b, int j, int
 // inter-thread imbalance inside a chunk).
 // ----------------------------------------------------------------------------
 
+// The (min, max) fold of one 4 xi x TRW r expand tile over r' (lanes sub, sub + ks,
+// ...): only the valid cells of A = W_j(l', xi', r') are read, so A's structural
+// cells may hold anything (no +inf pass).  Column a (xi = xi0 + a, xi' = xi - 1)
+// holds values for r' <= j - xi' + 1 = kend - a (kend = j - xi0 + 2): the bulk
+// of the r' range folds every column, the last 3 r' mask the columns whose
+// triangle ended.  xi0 = 2: column 0 is xi' = 1, whose only cell is the base
+// W_j(l', 1, j) (partition.py:117-121), folded once (min is idempotent, so
+// every split-K lane may add it).  With replication (callers check).
+template <int TRW>
+__device__ __forceinline__ void expand_fold_tri(double (&acc)[4][TRW], const double* A, const double* B, int j,
+                                                int nrs, int xi0, const int (&xa)[4], const int (&ra)[TRW], int sub,
+                                                int ks) {
+    const int kend = j - xi0 + 2;
+    const bool base_col = xi0 == 2;
+    int rp = 1 + sub;
+    for (; rp <= kend - 3; rp += ks) {
+        const double* Ar = A + (rp - 1) * j;
+        const double* Br = B + (rp - 1) * nrs;
+        double p[4], q[TRW];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) p[a] = Ar[xa[a]];
+        if (base_col) p[0] = PP_INF;
+#pragma unroll
+        for (int c = 0; c < TRW; ++c) q[c] = Br[ra[c]];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < TRW; ++c) acc[a][c] = dmin(acc[a][c], dmax(p[a], q[c]));
+    }
+    for (; rp <= kend; rp += ks) {
+        const double* Ar = A + (rp - 1) * j;
+        const double* Br = B + (rp - 1) * nrs;
+        double p[4], q[TRW];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) p[a] = (rp <= kend - a && !(a == 0 && base_col)) ? Ar[xa[a]] : PP_INF;
+#pragma unroll
+        for (int c = 0; c < TRW; ++c) q[c] = Br[ra[c]];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < TRW; ++c) acc[a][c] = dmin(acc[a][c], dmax(p[a], q[c]));
+    }
+    if (base_col) {
+        const double pb = A[(j - 1) * j];
+#pragma unroll
+        for (int c = 0; c < TRW; ++c) acc[0][c] = dmin(acc[0][c], dmax(pb, B[(j - 1) * nrs + ra[c]]));
+    }
+}
+
 // expand, step j: one CTA per (instance, l').  smem: A = W_j(l', ., .) block
 // [r'][xi'] (j x j, one contiguous copy), B = chan(l', r', r) [r'][r]
 // (j x (V-j) exact divisions).  Tiles 4 xi x 4 r; tile K range r' <= j - xi0 + 2.
@@ -926,14 +975,16 @@ __device__ __forceinline__ void expand_rows_cls(const pp_batch& b, const pp_inst
     for (int q = t; q < nr; q += blockDim.x) s_xb[q] = X_base(L, j + 1 + q, 1 + q);
     mbar_wait0(&s_mbar[0]);
     mbar_wait0(&s_mbar[1]);
-    __syncthreads();   // head / tail copies land before the +inf pass
-    for (int rp = 1 + warp; rp <= j; rp += nw)
-        for (int xip = 1 + lane; xip <= j; xip += 32)
-            if (!W_structural(j, rp, xip, allow)) {
-                const int e = (rp - 1) * j + (xip - 1);
-                for (int k = 0; k < nrows; ++k) A0[k * j * j + e] = PP_INF;
-            }
-    __syncthreads();
+    __syncthreads();   // head / tail copies land (before the +inf pass without replication)
+    if (!allow) {      // without replication the valid cells are not a triangle: mask them explicitly
+        for (int rp = 1 + warp; rp <= j; rp += nw)
+            for (int xip = 1 + lane; xip <= j; xip += 32)
+                if (!W_structural(j, rp, xip, allow)) {
+                    const int e = (rp - 1) * j + (xip - 1);
+                    for (int k = 0; k < nrows; ++k) A0[k * j * j + e] = PP_INF;
+                }
+        __syncthreads();
+    }
     pdl_trigger_at<1>();
     constexpr int TRW = EXPAND_TRW;
     const int ntx = (j + 3) >> 2, ntr = (nr + TRW - 1) / TRW, per_row = ntx * ntr, ntiles = nrows * per_row;
@@ -957,18 +1008,22 @@ __device__ __forceinline__ void expand_rows_cls(const pp_batch& b, const pp_inst
 #pragma unroll
         for (int c = 0; c < TRW; ++c) ra[c] = min(r0 + c, nr) - 1;
         const double* A = A0 + k * j * j;
-        for (int rp = 1 + sub; rp <= kend; rp += ks) {
-            const double* Ar = A + (rp - 1) * j;
-            const double* Br = B + (rp - 1) * nr;
-            double p[4], q[TRW];
+        if (allow) {
+            expand_fold_tri<TRW>(acc, A, B, j, nr, xi0, xa, ra, sub, ks);
+        } else {
+            for (int rp = 1 + sub; rp <= kend; rp += ks) {
+                const double* Ar = A + (rp - 1) * j;
+                const double* Br = B + (rp - 1) * nr;
+                double p[4], q[TRW];
 #pragma unroll
-            for (int a = 0; a < 4; ++a) p[a] = Ar[xa[a]];
+                for (int a = 0; a < 4; ++a) p[a] = Ar[xa[a]];
 #pragma unroll
-            for (int c = 0; c < TRW; ++c) q[c] = Br[ra[c]];
+                for (int c = 0; c < TRW; ++c) q[c] = Br[ra[c]];
 #pragma unroll
-            for (int a = 0; a < 4; ++a)
+                for (int a = 0; a < 4; ++a)
 #pragma unroll
-                for (int c = 0; c < TRW; ++c) acc[a][c] = dmin(acc[a][c], dmax(p[a], q[c]));
+                    for (int c = 0; c < TRW; ++c) acc[a][c] = dmin(acc[a][c], dmax(p[a], q[c]));
+            }
         }
         for (int off = 1; off < ks; off <<= 1)
 #pragma unroll
