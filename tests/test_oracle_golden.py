@@ -163,3 +163,18 @@ def test_spp_batch_matches_single():
     for k, c in enumerate(cases):
         assert mk[k].hex() == c["makespan"]
         assert bx[k] == len(c["plan"]["stages"])
+
+
+def test_c3_full_size_python_reference_goldens():
+    """The headline shape (96 layers x 64 GPUs, 8x8 two-tier) pinned by the
+    Python reference itself (tests/golden/make_c3_full.py: ~2.3 h of
+    pipeplan.spp per case): uniform M = 8, jittered M = 8 and M = 256."""
+    import glob
+    import os
+    from helpers import GOLDEN
+    paths = sorted(glob.glob(os.path.join(GOLDEN, "c3_full_*.json")))
+    assert paths, "no c3_full golden"
+    cases = [load(os.path.basename(p)[:-5]) for p in paths]
+    from concurrent.futures import ThreadPoolExecutor   # the oracle call releases the GIL
+    with ThreadPoolExecutor(len(cases)) as ex:
+        list(ex.map(lambda c: check_spp_cases([c]), cases))
