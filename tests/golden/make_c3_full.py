@@ -30,6 +30,8 @@ CASES = {
     "j96_8": dict(M=8, jitter_seed=96),
     "j96_256": dict(M=256, jitter_seed=96),
     "u32": dict(M=32, jitter_seed=None),
+    "j96_64": dict(M=64, jitter_seed=96),
+    "u128": dict(M=128, jitter_seed=None),
 }
 
 
