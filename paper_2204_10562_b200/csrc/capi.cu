@@ -102,7 +102,7 @@ static const int g_combine_waves = read_combine_waves();
 static const int g_expand_wide = getenv("PP_EXPAND_WIDE") ? atoi(getenv("PP_EXPAND_WIDE")) : 2;
 // rows per expand CTA when a step has more than PP_EXPAND_RB_MIN rows per SM
 // (PP_EXPAND_RB env, default 4; the chan block is shared by the CTA's rows)
-static const int g_expand_rb = getenv("PP_EXPAND_RB") ? std::max(1, atoi(getenv("PP_EXPAND_RB"))) : 4;
+static const int g_expand_rb = getenv("PP_EXPAND_RB") ? std::max(1, atoi(getenv("PP_EXPAND_RB"))) : 2;   // r02: 2 rows x 80 registers (3 CTAs/SM) beat 4 rows x 126 (C3 n = 12 DP 2.56 -> 2.50 ms)
 static const int g_expand_rb_min = getenv("PP_EXPAND_RB_MIN") ? atoi(getenv("PP_EXPAND_RB_MIN")) : 4;
 static constexpr int64_t EX_SMEM_DOUBLES = 12288;   // 96 KB: two 256-thread CTAs per SM
 // per-step chain with the critical path (items r = 1) split from the bulk, for

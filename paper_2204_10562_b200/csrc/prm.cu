@@ -1054,7 +1054,13 @@ __global__ void __launch_bounds__(128) k_expand_s(pp_batch b, int j) {
     expand_row_s(b, I, j, lp, 1, ex_smem);
 }
 // one row l' per CTA (steps with few rows: every SM gets work)
-__global__ void __launch_bounds__(256, 2) k_expand_s_p(const pp_batch* __restrict__ bp, int j, int rfirst, int rlast) {
+#ifndef EXPAND_MINB
+#define EXPAND_MINB 3   // resident 256-thread expand CTAs per SM the register budget targets (80 registers, no spills)
+#endif
+#ifndef COMBINE_MINB
+#define COMBINE_MINB (COMBINE_TL4 == 2 ? 3 : 2)
+#endif
+__global__ void __launch_bounds__(256, EXPAND_MINB) k_expand_s_p(const pp_batch* __restrict__ bp, int j, int rfirst, int rlast) {
     pdl_trigger_at<0>();
     StepTrace tr;
     tr.begin();
@@ -1069,7 +1075,7 @@ __global__ void __launch_bounds__(256, 2) k_expand_s_p(const pp_batch* __restric
 }
 // rb rows per CTA (host: rb * j^2 + j (V-j) doubles of shared memory): rows of one
 // payload class share their chan block (expand_rows_cls), others go row by row.
-__global__ void __launch_bounds__(256, 2) k_expand_m_p(const pp_batch* __restrict__ bp, int j, int rb) {
+__global__ void __launch_bounds__(256, EXPAND_MINB) k_expand_m_p(const pp_batch* __restrict__ bp, int j, int rb) {
     pdl_trigger_at<0>();
     StepTrace tr;
     tr.begin();
@@ -1439,7 +1445,7 @@ __global__ void __launch_bounds__(256, 2) k_combine_s(pp_batch b, int j) {
     __shared__ int s_order[1024];
     combine_item_s(b, I, j, blockIdx.y + 1, blockIdx.z, gridDim.z, cs_smem, s_hist, s_order, false);
 }
-__global__ void __launch_bounds__(256, COMBINE_TL4 == 2 ? 3 : 2) k_combine_s_p(const pp_batch* __restrict__ bp, int j, int r0) {
+__global__ void __launch_bounds__(256, COMBINE_MINB) k_combine_s_p(const pp_batch* __restrict__ bp, int j, int r0) {
     pdl_trigger_at<0>();
     StepTrace tr;
     tr.begin();
