@@ -73,3 +73,22 @@ def test_c5_candidate_simulation_vs_oracle():
     assert best + 1 == min(range(256), key=lambda k: (want[k], k)) + 1
     for k in (0, 59, 255):
         assert got[k][1] == O.lemma1_bound(inst, oplans[k])
+
+
+def test_c5_scaled_chunked_dp_vs_oracle_golden():
+    """The C5 generator at 256 layers x 64 GPUs (L > 128: the chunked DP kernels
+    that also run the full 1024 x 256 C5 DP) against the oracle's result
+    (tests/golden/make_c5_scaled.py; 237 s of the C oracle)."""
+    import glob
+    import os
+    from helpers import GOLDEN, load, model_of
+    paths = sorted(glob.glob(os.path.join(GOLDEN, "c5_scaled_*.json")))
+    assert paths
+    h = lambda x: None if x is None else float(x).hex()
+    for path in paths:
+        c = load(os.path.basename(path)[:-5])
+        r = P.spp(*model_of(c["input"]))
+        assert list(r.device_order) == c["device_order"]
+        assert [[e.stage_count, e.feasible, h(e.workload), h(e.makespan), h(e.bound)] for e in r.sweep] == c["sweep"]
+        assert [[s.layer_start, s.layer_end, list(s.devices)] for s in r.plan.stages] == c["plan"]["stages"]
+        assert (h(r.makespan), h(r.phi), h(r.theorem_factor)) == (c["makespan"], c["phi"], c["theorem_factor"])
