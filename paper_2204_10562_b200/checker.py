@@ -73,11 +73,12 @@ class _Events:
     def __init__(self, events):
         if isinstance(events, LazyEvents):
             self.lazy = events
-            self.m = np.ascontiguousarray(events._m, np.int32)
-            self.start = np.ascontiguousarray(events._s, np.float64)
-            self.end = np.ascontiguousarray(events._e, np.float64)
+            em, ep, es, ee = events._arrays()
+            self.m = np.ascontiguousarray(em, np.int32)
+            self.start = np.ascontiguousarray(es, np.float64)
+            self.end = np.ascontiguousarray(ee, np.float64)
             self.res_names, self.lab_names = events._res, events._lab
-            self.q = np.asarray(events._p, np.int64)
+            self.q = np.asarray(ep, np.int64)
         else:
             self.lazy = None
             self.objs = tuple(events)

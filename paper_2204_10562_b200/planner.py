@@ -49,17 +49,48 @@ def bound_factor(num_gpus: int, microbatch_count: int) -> float:
     return 2.0 + (4.0 * num_gpus - 4.0) / microbatch_count
 
 
+# Validated + packed profiles across calls.  A ModelProfile is deeply immutable
+# (frozen dataclasses in tuples), so the same OBJECT always packs to the same
+# arrays; entries are keyed by id and held through a weak reference, so a
+# recycled id can never hit a stale entry.  Clusters are NOT cached: their
+# bandwidth dict is mutable.
+_profile_cache = {}
+
+
+def _cached_profile(profile):
+    ent = _profile_cache.get(id(profile))
+    if ent is not None and ent[0]() is profile:
+        return ent[1]
+    return None
+
+
+def _cache_profile(profile, packed):
+    import weakref
+    key = id(profile)
+    try:
+        ref = weakref.ref(profile, lambda _r, k=key: _profile_cache.pop(k, None))
+    except TypeError:   # not weak-referenceable: no caching
+        return
+    if len(_profile_cache) > 4096:
+        _profile_cache.clear()
+    _profile_cache[key] = (ref, packed)
+
+
 def _items(instances):
     """Validate and pack every instance.  Within one call the same profile /
     cluster OBJECT (e.g. one cluster planned for several models or M values)
-    is validated and packed once; objects are not cached across calls (their
-    bandwidth dict is mutable)."""
+    is validated and packed once; profiles (immutable) are also remembered
+    across calls, clusters (mutable bandwidth dict) are not."""
     items, packs = [], []
     seen_p, seen_c, seen_pc = {}, {}, {}
     flags = _lib.PP_ALLOW_REPLICATION | sum_flags()
     for profile, cluster, M in instances:
         # same check order as validate_profile, validate_cluster, check_numeric_range
         pp, cc = seen_p.get(id(profile)), seen_c.get(id(cluster))
+        if pp is None:
+            hit = _cached_profile(profile)
+            if hit is not None:
+                pp = seen_p[id(profile)] = (profile, hit)
         if pp is None:
             validate_profile(profile)
         arrays = None
@@ -69,6 +100,7 @@ def _items(instances):
         if pp is None:
             check_profile_range(profile)
             pp = seen_p[id(profile)] = (profile, _device.pack_profile(profile))
+            _cache_profile(profile, pp[1])
         if cc is None:
             check_cluster_range(cluster, arrays)
             cc = seen_c[id(cluster)] = (cluster, _device.pack_cluster(cluster, arrays))

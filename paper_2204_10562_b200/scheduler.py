@@ -187,9 +187,7 @@ def _build_schedule(plan: Plan, rec, tiebreak=None) -> Schedule:
     # stable order of the reference: (start, resource key, microbatch), ties in queue order
     if tiebreak is None and rec.get("ev_order") is not None:
         # ordered on the device (k_event_order): rank k holds event (m-1)*J + pos-1
-        o = rec["ev_order"]
-        mo, po = np.divmod(o, J)
-        events = LazyEvents(res, lab, mo + 1, po + 1, start[o], end[o])
+        events = LazyEvents.from_order(res, lab, J, rec["ev_order"], start, end)
     elif tiebreak is None:
         # PE queues: same-resource, same-microbatch ties are in position order
         order, mo, po = _pe_tiebreak_order(N, M)
