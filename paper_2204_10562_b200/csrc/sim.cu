@@ -308,6 +308,127 @@ __device__ void pe_simulate_warp(const P& p, const InstView& I, int N, int M, do
     if (lane == 0) *o_mk = dmax(rf[0], arend);
 }
 
+// ---- PE sweep, nw WARPS per plan (R = 2N-1 <= 32 nw S): the warp version's
+// register blocks, with the two resources at each warp boundary exchanged
+// through shared memory (double-buffered by pass parity) and one named barrier
+// of the nw warps per pass.  Replaces the one-resource-per-thread CTA sweep
+// (pe_simulate) for large N: S independent resources per lane give the pass
+// ILP and the barrier spans nw = R / 128 warps instead of R / 32 (C5's
+// xi = 256 plan: 1532 passes at ~1.4 k cycles each before).  Same recurrence,
+// same fp64 operations in the same order per resource (bit-identical).
+// smem: xch[2][2][nw] (fe, be boundary values per pass parity) + red[2 nw]
+template <int S, class P>
+__device__ void pe_simulate_mw(const P& p, const InstView& I, int N, int M, int nw, double* sm, double* o_mk,
+                               double* o_bound, double* ev_s, double* ev_e, double* ar_s, double* ar_e) {
+    const unsigned FULL = 0xffffffffu;
+    const int R = 2 * N - 1, J = 4 * N - 3;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nthr = 32 * nw;
+    double* xfe = sm;            // [2][nw]: fe of the warp's last resource
+    double* xbe = sm + 2 * nw;   // [2][nw]: be of the warp's first resource
+    double* red = sm + 4 * nw;   // [2][nw]
+    double dA[S], dB[S], ar[S], fe[S], be[S], rf[S];
+    bool has_ar[S], act[S], from_left[S];
+    int p1[S], p2[S];
+    double cy = -PP_INF, am = -PP_INF;
+    const int q0 = (warp * 32 + lane) * S;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int q = q0 + s;
+        act[s] = q < R;
+        LaneCost c{0.0, 0.0, 0.0, 0.0, false, 0.0, 0.0, PP_INF};
+        if (act[s]) c = lane_cost(p, I, N, q);
+        dA[s] = c.dA; dB[s] = c.dB; ar[s] = c.ar; has_ar[s] = act[s] && c.has_ar;
+        if (act[s]) cy = dmax(cy, c.cyc);
+        if (has_ar[s]) am = dmax(am, c.ar);
+        const bool st = (q & 1) == 0;
+        const int n = q / 2 + 1;
+        if (st) {
+            if (n < N) { p1[s] = 4 * N - 1 - 2 * n; p2[s] = 2 * n - 1; }   // B_n, F_n
+            else { p1[s] = 2 * N - 1; p2[s] = 0; }                       // FB_N
+        } else { p1[s] = 4 * N - 2 - 2 * n; p2[s] = 2 * n; }              // Y_n, X_n
+        from_left[s] = st && n == N;
+        fe[s] = 0.0; be[s] = 0.0; rf[s] = 0.0;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        cy = dmax(cy, __shfl_xor_sync(FULL, cy, off));
+        am = dmax(am, __shfl_xor_sync(FULL, am, off));
+    }
+    if (lane == 0) { red[warp] = cy; red[nw + warp] = am; xfe[warp] = 0.0; xbe[warp] = 0.0; }
+    if (nw > 1) bar_sync(nthr);
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < nw; ++w) { cy = dmax(cy, red[w]); am = dmax(am, red[nw + w]); }
+        *o_bound = (double)(M + 4 * N - 4) * cy + (am == -PP_INF ? 0.0 : am);   // scheduler.py:238
+    }
+    const int P_total = M + J - 1;
+    for (int pass = 1; pass <= P_total; ++pass) {
+        const int cur = pass & 1, prv = cur ^ 1;
+        // neighbours' pass-1 ends: left fe of q-1, right be of q+1 (other warps' via xch)
+        double fe_in = __shfl_up_sync(FULL, fe[S - 1], 1);
+        double be_in = __shfl_down_sync(FULL, be[0], 1);
+        if (lane == 0) fe_in = warp > 0 ? xfe[prv * nw + warp - 1] : 0.0;
+        if (lane == 31) be_in = warp + 1 < nw ? xbe[prv * nw + warp + 1] : 0.0;
+        double fn[S], bn[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            fn[s] = fe[s]; bn[s] = be[s];
+            if (!act[s]) continue;
+            const int q = q0 + s;
+            const double left = q == 0 ? 0.0 : (s > 0 ? fe[s - 1] : fe_in);
+            const double right = q + 1 >= R ? 0.0 : (s + 1 < S ? be[s + 1] : be_in);
+            int m = pass - p1[s] + 1;
+            if ((unsigned)(m - 1) < (unsigned)M) {   // 1 <= m <= M
+                const double st = dmax(rf[s], from_left[s] ? left : right);
+                const double en = st + dB[s];   // B / FB / Y
+                rf[s] = en;
+                bn[s] = en;
+                if (ev_s) { const int64_t x = (int64_t)(m - 1) * J + p1[s] - 1; ev_s[x] = st; ev_e[x] = en; }
+            }
+            if (p2[s]) {
+                m = pass - p2[s] + 1;
+                if ((unsigned)(m - 1) < (unsigned)M) {
+                    const double st = dmax(rf[s], left);
+                    const double en = st + dA[s];   // F / X
+                    rf[s] = en;
+                    fn[s] = en;
+                    if (ev_s) { const int64_t x = (int64_t)(m - 1) * J + p2[s] - 1; ev_s[x] = st; ev_e[x] = en; }
+                }
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) { fe[s] = fn[s]; be[s] = bn[s]; }
+        if (nw > 1) {
+            if (lane == 31) xfe[cur * nw + warp] = fe[S - 1];
+            if (lane == 0) xbe[cur * nw + warp] = be[0];
+            bar_sync(nthr);
+        }
+    }
+    // AllReduce windows start at the stage's last compute end (scheduler.py:195-198);
+    // makespan = max(last B_1 / FB_1 end, AllReduce ends)   (scheduler.py:216-220)
+    double arend = -PP_INF;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int q = q0 + s;
+        if (act[s] && (q & 1) == 0 && has_ar[s]) {
+            const double e = rf[s] + ar[s];
+            arend = dmax(arend, e);
+            if (ar_s) { ar_s[q / 2] = rf[s]; ar_e[q / 2] = e; }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) arend = dmax(arend, __shfl_xor_sync(FULL, arend, off));
+    if (nw > 1) {
+        if (lane == 0) red[warp] = arend;
+        bar_sync(nthr);
+        if (threadIdx.x == 0)
+            for (int w = 1; w < nw; ++w) arend = dmax(arend, red[w]);
+    }
+    if (threadIdx.x == 0) *o_mk = dmax(rf[0], arend);
+}
+constexpr int PE_MW_S = 4;   // resources per lane of the multi-warp sweep
+__host__ __device__ inline int pe_mw_warps(int N) { return (2 * N - 1 + 32 * PE_MW_S - 1) / (32 * PE_MW_S); }
+
 template <class P>
 __device__ void pe_simulate_warp_any(const P& p, const InstView& I, int N, int M, double* o_mk, double* o_bound,
                                      double* ev_s, double* ev_e, double* ar_s, double* ar_e) {
@@ -479,14 +600,14 @@ __global__ void __launch_bounds__(1024) k_pe_sweep(pp_batch b) {
         if (threadIdx.x == 0) { b.sweep_mk[so] = PP_INF; b.sweep_bound[so] = PP_INF; }
         return;
     }
-    const int nthr = sim_threads(xi);
-    if ((int)threadIdx.x >= nthr) return;
+    const int nw = pe_mw_warps(xi);
+    if ((int)threadIdx.x >= 32 * nw) return;
     extern __shared__ double smem_d[];
     const int64_t st = I.stage_off + (int64_t)xi * (xi - 1) / 2;
     SppPlanView p{b.stage_ls + st, b.stage_le + st, b.stage_dlo + st, b.stage_dhi + st, b.order + I.order_off};
     InstView iv(b, I);
-    pe_simulate(p, iv, xi, I.M, nthr, smem_d, b.sweep_mk + so, b.sweep_bound + so, nullptr, nullptr, nullptr,
-                nullptr);
+    pe_simulate_mw<PE_MW_S>(p, iv, xi, I.M, nw, smem_d, b.sweep_mk + so, b.sweep_bound + so, nullptr, nullptr,
+                            nullptr, nullptr);
 }
 
 // spp selection (planner.py:66-77): first xi with strictly smallest makespan.
@@ -515,15 +636,15 @@ __global__ void __launch_bounds__(1024) k_replay(pp_batch b) {
     const pp_instance I = b.inst[blockIdx.x];
     const int xi = b.best_xi[blockIdx.x];
     if (xi <= 0) return;
-    const int nthr = sim_threads(xi);
-    if ((int)threadIdx.x >= nthr) return;
+    const int nw = pe_mw_warps(xi);
+    if ((int)threadIdx.x >= 32 * nw) return;
     extern __shared__ double smem_d[];
     __shared__ double s_mk, s_bd;
     const int64_t st = I.stage_off + (int64_t)xi * (xi - 1) / 2;
     SppPlanView p{b.stage_ls + st, b.stage_le + st, b.stage_dlo + st, b.stage_dhi + st, b.order + I.order_off};
     InstView iv(b, I);
-    pe_simulate(p, iv, xi, I.M, nthr, smem_d, &s_mk, &s_bd, b.ev_start + I.ev_off, b.ev_end + I.ev_off,
-                b.ar_start + I.ar_off, b.ar_end + I.ar_off);
+    pe_simulate_mw<PE_MW_S>(p, iv, xi, I.M, nw, smem_d, &s_mk, &s_bd, b.ev_start + I.ev_off, b.ev_end + I.ev_off,
+                            b.ar_start + I.ar_off, b.ar_end + I.ar_off);
 }
 
 // ---- plan costs (cost_summary, cost.py:172-202; channel_times :162-169;
@@ -660,8 +781,10 @@ __global__ void __launch_bounds__(1024) k_sim_plans(pp_batch b, pp_sim_batch s) 
         bar_sync(nthr);
     }
     if (P.flags & PP_SIM_PE_ORDER) {
-        pe_simulate(pv, iv, N, M, nthr, smem_d, s.makespan + blockIdx.x, s.bound + blockIdx.x, ev_s, ev_e,
-                    s.ar_start + P.ar_off, s.ar_end + P.ar_off);
+        const int nw = pe_mw_warps(N);
+        if ((int)threadIdx.x < 32 * nw)
+            pe_simulate_mw<PE_MW_S>(pv, iv, N, M, nw, smem_d, s.makespan + blockIdx.x, s.bound + blockIdx.x, ev_s,
+                                    ev_e, s.ar_start + P.ar_off, s.ar_end + P.ar_off);
         if (threadIdx.x == 0) { s.status[blockIdx.x] = 0; s.n_done[blockIdx.x] = (int64_t)M * J; }
         for (int r = threadIdx.x; r < R; r += nthr) s.head[P.lane_off + r] = -1;
         return;
