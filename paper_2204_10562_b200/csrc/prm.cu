@@ -736,8 +736,11 @@ __device__ void combine_compute(double* Wi, int i, int r, int L, int l0, int nl,
             double* row = Wi + ((int64_t)(l - 1) * i + (r - 1)) * i;
 #pragma unroll
             for (int c = 0; c < TX; ++c) {
+                // only this CTA's DP columns: a padded column past cB is either a
+                // structural cell of this plane (the +inf loop writes it) or the
+                // next xi plane's first column (its CTA writes it) — never both
                 const int xi = cA + TX * tj[u] + c;
-                if (xi - cA < wx && xi <= i) row[xi - 1] = acc[u][a][c];
+                if (xi - cA < ncol) row[xi - 1] = acc[u][a][c];
             }
         }
     }
@@ -763,7 +766,7 @@ __global__ void __launch_bounds__(CD_T, 2) k_combine_diag(pp_batch b, int j, int
     const int wx = dp_cells ? (ncol + TX - 1) / TX * TX : 0;
     for (int e = threadIdx.x; e < nl * nx; e += CD_T) {   // xi = 1, xi > j + 1, disabled widths
         const int l = l0 + e / nx, xi = x0 + e % nx;
-        if (dp_cells && xi >= cA && xi < cA + wx) continue;
+        if (dp_cells && xi >= cA && xi <= cB) continue;
         Wi[((int64_t)(l - 1) * i + (r - 1)) * i + (xi - 1)] = PP_INF;
     }
     if (!dp_cells) return;
