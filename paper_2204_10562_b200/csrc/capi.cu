@@ -55,6 +55,7 @@ __global__ void k_event_rank(pp_batch b);
 __global__ void k_select(pp_batch b);
 __global__ void k_replay(pp_batch b);
 __global__ void k_sim_plans(pp_batch b, pp_sim_batch s);
+__global__ void k_sim_plans_pe(pp_batch b, pp_sim_batch s);
 __global__ void k_peak_minmax(double* out, int iters, double seed);
 }  // namespace pp
 
@@ -863,9 +864,7 @@ int pp_pe_sweep(const pp_batch* b, void* stream) {
         PP_CHECK_LAUNCH("k_pe_sweep");
         return PP_OK;
     }
-    const size_t smem = sim_smem(b->max_V);
-    cudaFuncSetAttribute(k_pe_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_pe_sweep<<<g, sim_block(b->max_V), smem, S(stream)>>>(*b);
+    k_pe_sweep<<<g, 32 * pe_mw_warps(b->max_V), sizeof(double) * 6 * 8, S(stream)>>>(*b);
     PP_CHECK_LAUNCH("k_pe_sweep");
     return PP_OK;
 }
@@ -878,9 +877,7 @@ int pp_select(const pp_batch* b, void* stream) {
         if (b->max_V <= PE_WARP_MAXN) {
             k_replay_w<<<b->n_inst, 32, 0, S(stream)>>>(*b);
         } else {
-            const size_t smem = sim_smem(b->max_V);
-            cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_replay<<<b->n_inst, sim_block(b->max_V), smem, S(stream)>>>(*b);
+            k_replay<<<b->n_inst, 32 * pe_mw_warps(b->max_V), sizeof(double) * 6 * 8, S(stream)>>>(*b);
         }
         PP_CHECK_LAUNCH("k_replay");
         if (b->ev_order) {
@@ -934,6 +931,9 @@ int pp_simulate(const pp_batch* ib, const pp_sim_batch* s, void* stream) {
     cudaFuncSetAttribute(k_sim_plans, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_sim_plans<<<s->n_plan, sim_block(s->max_N), smem, S(stream)>>>(*ib, *s);
     PP_CHECK_LAUNCH("k_sim_plans");
+    // PE-order plans without cost outputs (the others returned above): multi-warp sweep
+    k_sim_plans_pe<<<s->n_plan, 32 * pe_mw_warps(s->max_N), sizeof(double) * 6 * 8, S(stream)>>>(*ib, *s);
+    PP_CHECK_LAUNCH("k_sim_plans_pe");
     return PP_OK;
 }
 

@@ -590,8 +590,8 @@ __host__ __device__ inline int sim_threads(int N) {
     return t < 32 ? 32 : t;
 }
 
-// Every feasible xi plan of every instance: grid (n_inst, maxV).
-__global__ void __launch_bounds__(1024) k_pe_sweep(pp_batch b) {
+// Every feasible xi plan of every instance: grid (n_inst, maxV), block 32 pe_mw_warps(maxV).
+__global__ void __launch_bounds__(256) k_pe_sweep(pp_batch b) {
     const pp_instance I = b.inst[blockIdx.x];
     const int xi = blockIdx.y + 1;
     if (xi > I.V) return;
@@ -631,8 +631,8 @@ __global__ void __launch_bounds__(32) k_select(pp_batch b) {
     if (lane == 0) { b.best_xi[blockIdx.x] = bx; b.best_mk[blockIdx.x] = best; }
 }
 
-// Replay the selected plan with event capture: grid n_inst.
-__global__ void __launch_bounds__(1024) k_replay(pp_batch b) {
+// Replay the selected plan with event capture: grid n_inst, block 32 pe_mw_warps(maxV).
+__global__ void __launch_bounds__(256) k_replay(pp_batch b) {
     const pp_instance I = b.inst[blockIdx.x];
     const int xi = b.best_xi[blockIdx.x];
     if (xi <= 0) return;
@@ -743,8 +743,33 @@ __device__ void cycle_simulate(const LaneCost& c, int N, int M, int nthr, double
 }
 
 // ---- caller plans -------------------------------------------------------------
+// PE-order plans without cost outputs: the multi-warp sweep, <= 8 warps per plan
+// (block 32 pe_mw_warps(max_N); the register budget of 256 threads, no spills)
+__device__ __forceinline__ bool sim_plan_is_pe_only(const pp_plan& P, const pp_sim_batch& s) {
+    return (P.flags & PP_SIM_PE_ORDER) && !(P.flags & (PP_SIM_CYCLE | PP_SIM_COSTS_ONLY)) && !s.lane_cost &&
+           !s.workload;
+}
+__global__ void __launch_bounds__(256) k_sim_plans_pe(pp_batch b, pp_sim_batch s) {
+    const pp_plan P = s.plan[blockIdx.x];
+    if (!sim_plan_is_pe_only(P, s)) return;
+    const pp_instance I = b.inst[P.inst];
+    const int N = P.N, M = P.M, R = 2 * N - 1, J = 4 * N - 3;
+    const int nw = pe_mw_warps(N);
+    if ((int)threadIdx.x >= 32 * nw) return;
+    extern __shared__ double smem_d[];
+    ExplicitPlanView pv{s.ls + P.stage_off, s.le + P.stage_off, s.dev_off + P.devoff_off, s.devs};
+    InstView iv(b, I);
+    double* ev_s = s.ev_start ? s.ev_start + P.ev_off : nullptr;
+    double* ev_e = s.ev_end ? s.ev_end + P.ev_off : nullptr;
+    pe_simulate_mw<PE_MW_S>(pv, iv, N, M, nw, smem_d, s.makespan + blockIdx.x, s.bound + blockIdx.x, ev_s, ev_e,
+                            s.ar_start + P.ar_off, s.ar_end + P.ar_off);
+    if (threadIdx.x == 0) { s.status[blockIdx.x] = 0; s.n_done[blockIdx.x] = (int64_t)M * J; }
+    for (int r = threadIdx.x; r < R; r += 32 * nw) s.head[P.lane_off + r] = -1;
+}
+
 __global__ void __launch_bounds__(1024) k_sim_plans(pp_batch b, pp_sim_batch s) {
     const pp_plan P = s.plan[blockIdx.x];
+    if (sim_plan_is_pe_only(P, s)) return;   // k_sim_plans_pe
     const pp_instance I = b.inst[P.inst];
     const int N = P.N, M = P.M, R = 2 * N - 1, J = 4 * N - 3;
     const int nthr = sim_threads(N);
