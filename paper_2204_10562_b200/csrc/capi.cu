@@ -864,7 +864,7 @@ int pp_pe_sweep(const pp_batch* b, void* stream) {
         PP_CHECK_LAUNCH("k_pe_sweep");
         return PP_OK;
     }
-    k_pe_sweep<<<g, 32 * pe_mw_warps(b->max_V), sizeof(double) * 6 * 8, S(stream)>>>(*b);
+    k_pe_sweep<<<g, 32 * pe_mw_warps(b->max_V), sizeof(double) * 6 * 32, S(stream)>>>(*b);
     PP_CHECK_LAUNCH("k_pe_sweep");
     return PP_OK;
 }
@@ -877,7 +877,7 @@ int pp_select(const pp_batch* b, void* stream) {
         if (b->max_V <= PE_WARP_MAXN) {
             k_replay_w<<<b->n_inst, 32, 0, S(stream)>>>(*b);
         } else {
-            k_replay<<<b->n_inst, 32 * pe_mw_warps(b->max_V), sizeof(double) * 6 * 8, S(stream)>>>(*b);
+            k_replay<<<b->n_inst, 32 * pe_mw_warps(b->max_V), sizeof(double) * 6 * 32, S(stream)>>>(*b);
         }
         PP_CHECK_LAUNCH("k_replay");
         if (b->ev_order) {
@@ -932,7 +932,7 @@ int pp_simulate(const pp_batch* ib, const pp_sim_batch* s, void* stream) {
     k_sim_plans<<<s->n_plan, sim_block(s->max_N), smem, S(stream)>>>(*ib, *s);
     PP_CHECK_LAUNCH("k_sim_plans");
     // PE-order plans without cost outputs (the others returned above): multi-warp sweep
-    k_sim_plans_pe<<<s->n_plan, 32 * pe_mw_warps(s->max_N), sizeof(double) * 6 * 8, S(stream)>>>(*ib, *s);
+    k_sim_plans_pe<<<s->n_plan, 32 * pe_mw_warps(s->max_N), sizeof(double) * 6 * 32, S(stream)>>>(*ib, *s);
     PP_CHECK_LAUNCH("k_sim_plans_pe");
     return PP_OK;
 }

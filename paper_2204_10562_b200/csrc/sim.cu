@@ -426,7 +426,7 @@ __device__ void pe_simulate_mw(const P& p, const InstView& I, int N, int M, int 
     }
     if (threadIdx.x == 0) *o_mk = dmax(rf[0], arend);
 }
-constexpr int PE_MW_S = 4;   // resources per lane of the multi-warp sweep
+constexpr int PE_MW_S = 1;   // resources per lane of the multi-warp sweep (measured: 1 beats 4, the pass is latency-bound)
 __host__ __device__ inline int pe_mw_warps(int N) { return (2 * N - 1 + 32 * PE_MW_S - 1) / (32 * PE_MW_S); }
 
 template <class P>
@@ -591,7 +591,7 @@ __host__ __device__ inline int sim_threads(int N) {
 }
 
 // Every feasible xi plan of every instance: grid (n_inst, maxV), block 32 pe_mw_warps(maxV).
-__global__ void __launch_bounds__(256) k_pe_sweep(pp_batch b) {
+__global__ void __launch_bounds__(1024) k_pe_sweep(pp_batch b) {
     const pp_instance I = b.inst[blockIdx.x];
     const int xi = blockIdx.y + 1;
     if (xi > I.V) return;
@@ -632,7 +632,7 @@ __global__ void __launch_bounds__(32) k_select(pp_batch b) {
 }
 
 // Replay the selected plan with event capture: grid n_inst, block 32 pe_mw_warps(maxV).
-__global__ void __launch_bounds__(256) k_replay(pp_batch b) {
+__global__ void __launch_bounds__(1024) k_replay(pp_batch b) {
     const pp_instance I = b.inst[blockIdx.x];
     const int xi = b.best_xi[blockIdx.x];
     if (xi <= 0) return;
@@ -749,7 +749,7 @@ __device__ __forceinline__ bool sim_plan_is_pe_only(const pp_plan& P, const pp_s
     return (P.flags & PP_SIM_PE_ORDER) && !(P.flags & (PP_SIM_CYCLE | PP_SIM_COSTS_ONLY)) && !s.lane_cost &&
            !s.workload;
 }
-__global__ void __launch_bounds__(256) k_sim_plans_pe(pp_batch b, pp_sim_batch s) {
+__global__ void __launch_bounds__(1024) k_sim_plans_pe(pp_batch b, pp_sim_batch s) {
     const pp_plan P = s.plan[blockIdx.x];
     if (!sim_plan_is_pe_only(P, s)) return;
     const pp_instance I = b.inst[P.inst];
