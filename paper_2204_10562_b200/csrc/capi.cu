@@ -55,7 +55,6 @@ __global__ void k_event_rank(pp_batch b);
 __global__ void k_select(pp_batch b);
 __global__ void k_replay(pp_batch b);
 __global__ void k_sim_plans(pp_batch b, pp_sim_batch s);
-__global__ void k_sim_plans_pe(pp_batch b, pp_sim_batch s);
 __global__ void k_peak_minmax(double* out, int iters, double seed);
 }  // namespace pp
 
@@ -931,9 +930,6 @@ int pp_simulate(const pp_batch* ib, const pp_sim_batch* s, void* stream) {
     cudaFuncSetAttribute(k_sim_plans, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_sim_plans<<<s->n_plan, sim_block(s->max_N), smem, S(stream)>>>(*ib, *s);
     PP_CHECK_LAUNCH("k_sim_plans");
-    // PE-order plans without cost outputs (the others returned above): multi-warp sweep
-    k_sim_plans_pe<<<s->n_plan, 32 * pe_mw_warps(s->max_N), sizeof(double) * 6 * 32, S(stream)>>>(*ib, *s);
-    PP_CHECK_LAUNCH("k_sim_plans_pe");
     return PP_OK;
 }
 

@@ -426,7 +426,8 @@ __device__ void pe_simulate_mw(const P& p, const InstView& I, int N, int M, int 
     }
     if (threadIdx.x == 0) *o_mk = dmax(rf[0], arend);
 }
-constexpr int PE_MW_S = 1;   // resources per lane of the multi-warp sweep (measured: 1 beats 4, the pass is latency-bound)
+constexpr int PE_MW_S = 4;   // resources per lane of the multi-warp sweep (spp sweeps with V > 64: C5 full
+                             // spp sweep 2.7 -> 1.6 ms; 1 per lane measured 2.7 ms)
 __host__ __device__ inline int pe_mw_warps(int N) { return (2 * N - 1 + 32 * PE_MW_S - 1) / (32 * PE_MW_S); }
 
 template <class P>
@@ -743,33 +744,8 @@ __device__ void cycle_simulate(const LaneCost& c, int N, int M, int nthr, double
 }
 
 // ---- caller plans -------------------------------------------------------------
-// PE-order plans without cost outputs: the multi-warp sweep, <= 8 warps per plan
-// (block 32 pe_mw_warps(max_N); the register budget of 256 threads, no spills)
-__device__ __forceinline__ bool sim_plan_is_pe_only(const pp_plan& P, const pp_sim_batch& s) {
-    return (P.flags & PP_SIM_PE_ORDER) && !(P.flags & (PP_SIM_CYCLE | PP_SIM_COSTS_ONLY)) && !s.lane_cost &&
-           !s.workload;
-}
-__global__ void __launch_bounds__(1024) k_sim_plans_pe(pp_batch b, pp_sim_batch s) {
-    const pp_plan P = s.plan[blockIdx.x];
-    if (!sim_plan_is_pe_only(P, s)) return;
-    const pp_instance I = b.inst[P.inst];
-    const int N = P.N, M = P.M, R = 2 * N - 1, J = 4 * N - 3;
-    const int nw = pe_mw_warps(N);
-    if ((int)threadIdx.x >= 32 * nw) return;
-    extern __shared__ double smem_d[];
-    ExplicitPlanView pv{s.ls + P.stage_off, s.le + P.stage_off, s.dev_off + P.devoff_off, s.devs};
-    InstView iv(b, I);
-    double* ev_s = s.ev_start ? s.ev_start + P.ev_off : nullptr;
-    double* ev_e = s.ev_end ? s.ev_end + P.ev_off : nullptr;
-    pe_simulate_mw<PE_MW_S>(pv, iv, N, M, nw, smem_d, s.makespan + blockIdx.x, s.bound + blockIdx.x, ev_s, ev_e,
-                            s.ar_start + P.ar_off, s.ar_end + P.ar_off);
-    if (threadIdx.x == 0) { s.status[blockIdx.x] = 0; s.n_done[blockIdx.x] = (int64_t)M * J; }
-    for (int r = threadIdx.x; r < R; r += 32 * nw) s.head[P.lane_off + r] = -1;
-}
-
 __global__ void __launch_bounds__(1024) k_sim_plans(pp_batch b, pp_sim_batch s) {
     const pp_plan P = s.plan[blockIdx.x];
-    if (sim_plan_is_pe_only(P, s)) return;   // k_sim_plans_pe
     const pp_instance I = b.inst[P.inst];
     const int N = P.N, M = P.M, R = 2 * N - 1, J = 4 * N - 3;
     const int nthr = sim_threads(N);
@@ -806,10 +782,10 @@ __global__ void __launch_bounds__(1024) k_sim_plans(pp_batch b, pp_sim_batch s) 
         bar_sync(nthr);
     }
     if (P.flags & PP_SIM_PE_ORDER) {
-        const int nw = pe_mw_warps(N);
-        if ((int)threadIdx.x < 32 * nw)
-            pe_simulate_mw<PE_MW_S>(pv, iv, N, M, nw, smem_d, s.makespan + blockIdx.x, s.bound + blockIdx.x, ev_s,
-                                    ev_e, s.ar_start + P.ar_off, s.ar_end + P.ar_off);
+        // caller plans keep one resource per thread: measured faster than the
+        // multi-warp sweep on C5's 256 plans (711 vs 877-931 ns per pass of xi = 256)
+        pe_simulate(pv, iv, N, M, nthr, smem_d, s.makespan + blockIdx.x, s.bound + blockIdx.x, ev_s, ev_e,
+                    s.ar_start + P.ar_off, s.ar_end + P.ar_off);
         if (threadIdx.x == 0) { s.status[blockIdx.x] = 0; s.n_done[blockIdx.x] = (int64_t)M * J; }
         for (int r = threadIdx.x; r < R; r += nthr) s.head[P.lane_off + r] = -1;
         return;
