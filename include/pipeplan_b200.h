@@ -126,11 +126,10 @@ int pp_prm(const pp_batch *b, void *stream);
 
 /* DP schedule for batches inside the shared-memory limits (L, V <= 128):
  * 0 = one launch pair per wavefront step (replayed as a cached CUDA graph),
- * 1 = one persistent dependency-driven kernel, 3 = one CTA per instance,
- * 4 = one thread-block cluster per instance, 2 (default) = auto (one CTA per
- * instance for >= 2 x SMs instances with L * V <= 2048, else per step).
- * Bit-identical results; a performance / test knob.  Returns the previous
- * mode.  Process-wide. */
+ * 3 = one CTA per instance, 2 (default) = auto (one CTA per instance for
+ * >= 2 x SMs instances with L * V <= 2048, else per step).  Other values:
+ * PP_EINVAL.  Bit-identical results; a performance / test knob.  Returns the
+ * previous mode.  Process-wide. */
 int pp_dp_set_persistent(int32_t mode);
 
 /* Combine early exit (default 1): for stage-term triangles certified
@@ -152,11 +151,6 @@ int pp_dp_set_combine(int32_t kind);
  * more than 2 x SMs instances (RDO is latency-bound below that), 2 always.
  * Identical results; a performance / test knob.  Returns the previous mode. */
 int pp_rdo_set_dedup(int32_t mode);
-
-/* Debug: record the persistent DP's per-task timeline (4 x u64 per task:
- * smid << 32 | kind, fetch, inputs-ready, end; globaltimer ns) into the device
- * buffer d_buf of 4 * cap entries; NULL disables.  Not on the planning path. */
-int pp_dp_trace(uint64_t *d_buf, int32_t cap);
 
 /* Debug: per-CTA timeline of the per-step expand / combine kernels (4 x u64 per
  * CTA: kind << 56 | j << 40 | smid << 32 | block id, start, end, 0); NULL

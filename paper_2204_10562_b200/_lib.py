@@ -87,7 +87,7 @@ class PPSimBatch(C.Structure):
 EXPORTS = ("pp_version", "pp_last_error", "pp_device_count", "pp_layout", "pp_rdo", "pp_prm",
            "pp_pe_sweep", "pp_select", "pp_spp", "pp_prm_query", "pp_simulate", "pp_min_cut",
            "pp_launch_count", "pp_phi", "pp_peak_minmax", "pp_format_trace", "pp_validate_schedule",
-           "pp_rdo_set_rounds", "pp_dp_set_persistent", "pp_dp_trace",
+           "pp_rdo_set_rounds", "pp_dp_set_persistent",
            "pp_dp_set_early_exit", "pp_step_trace", "pp_dp_set_combine",
            "pp_rdo_set_dedup")
 
@@ -147,15 +147,15 @@ def _declare(L):
     L.pp_dp_set_combine.restype = C.c_int
     L.pp_step_trace.argtypes = [vp, i32]
     L.pp_step_trace.restype = C.c_int
-    L.pp_dp_trace.argtypes = [vp, i32]
-    L.pp_dp_trace.restype = C.c_int
 
 
 def dp_persistent(mode) -> int:
-    """DP schedule: True/1 persistent kernel, False/0 per-step launches, 3 one
-    CTA per instance, 2 auto (default).  Returns the previous mode.
-    Results are identical either way."""
-    return int(load(require_device=False).pp_dp_set_persistent(int(mode)))
+    """DP schedule: 0 per-step launches, 3 one CTA per instance, 2 auto
+    (default).  Returns the previous mode.  Results are identical either way."""
+    prev = load(require_device=False).pp_dp_set_persistent(int(mode))
+    if prev < 0:
+        check(prev)
+    return int(prev)
 
 
 def dp_early_exit(on: bool) -> bool:

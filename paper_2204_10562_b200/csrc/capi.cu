@@ -31,11 +31,8 @@ __global__ void k_expand_s(pp_batch b, int j);
 __global__ void k_sdedup(pp_batch b);
 __global__ void k_stab(pp_batch b);
 __global__ void k_combine_s(pp_batch b, int j);
-__global__ void k_dp_reset(pp_batch b);
-__global__ void k_dp_persist(pp_batch b);
 __global__ void k_dp_inst(pp_batch b, int smem_doubles);
 __global__ void k_dp_inst2(pp_batch b);
-__global__ void k_dp_cluster(pp_batch b);
 __global__ void k_backtrack(pp_batch b);
 __global__ void k_query(pp_batch b, int n, const int* qi, const int* ql, const int* qx, const int* qr,
                         const int* qd, int max_xi, double* w, int* frag, int* feas);
@@ -263,73 +260,27 @@ struct SideStreams {
 static thread_local SideStreams g_side;
 
 // Shared-memory-path DP schedule (same bits either way):
-//   1 = one persistent dependency-driven kernel (dp_persist.cu): the critical
-//       chain runs ahead, so small batches finish sooner (latency);
-//   0 = the launch-per-step wavefront (prm_chain): better throughput once the
-//       batch fills the GPU on its own;
-//   3 = one CTA per instance (dp_inst.cu): the whole wavefront of an instance in
-//       one CTA, for batches with many more instances than SMs;
-//   4 = one thread-block cluster per instance (dp_cluster.cu);
+//   0 = the launch-per-step wavefront (prm_chain_p / the split critical-path
+//       chain), replayed as a CUDA graph;
+//   3 = one CTA per instance (dp_inst2.cu, dp_inst.cu): the whole wavefront of
+//       an instance in one CTA, for batches with many more instances than SMs;
 //   2 = auto (default): instance-per-CTA for >= 2 x SMs small instances
-//       (L * V <= PP_DP_INST_MAX_LV), else per-step (replayed as a CUDA graph).
+//       (L * V <= PP_DP_INST_MAX_LV), else per-step.
+// (Round 1's persistent dependency-driven kernel and cluster-per-instance
+// schedules were never chosen by auto — the graph-replayed per-step chain beat
+// them at every batch size — and were removed in round 2.)
 static constexpr int64_t PP_DP_INST_MAX_LV = 2048;
 static std::atomic<int> g_dp_persist{2};
 
-int pp_dp_set_persistent(int32_t mode) { return g_dp_persist.exchange(mode < 0 || mode > 4 ? 2 : mode); }
+int pp_dp_set_persistent(int32_t mode) {
+    if (mode != 0 && mode != 2 && mode != 3) return fail(PP_EINVAL, "DP schedule %d: 0 (per step), 2 (auto) or 3", mode);
+    return g_dp_persist.exchange(mode);
+}
 
 static int prm_prep(const pp_batch* b, void* stream, bool tables = true);
 // instance-per-CTA DP kernel: 2 = k_dp_inst2 (operands built in shared memory)
 // when its footprint fits, 1 = k_dp_inst (table-staged); PP_DP_INST env
 static const int g_dp_inst_kind = getenv("PP_DP_INST") ? atoi(getenv("PP_DP_INST")) : 2;
-
-// cluster size of the cluster-per-instance schedule (PP_DP_CLUSTER env: 2..16)
-static int read_cluster_size() {
-    const char* e = getenv("PP_DP_CLUSTER");
-    const int v = e ? atoi(e) : 16;
-    return v < 2 ? 2 : (v > 16 ? 16 : v);
-}
-static const int g_cluster_size = read_cluster_size();
-
-static int prm_cluster(const pp_batch* b, void* stream) {
-    const int maxL = b->max_L, maxV = b->max_V;
-    int rc;
-    if ((rc = prm_prep(b, stream))) return rc;
-    if (maxV > 1) {
-        const size_t cs = (size_t)(maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 +
-                          (size_t)(maxL > 1 ? maxL - 1 : 0) * (maxV - 1);
-        const size_t ex = (size_t)(maxV - 1) * maxV;
-        const size_t smem = sizeof(double) * std::max(cs, ex);
-        cudaFuncSetAttribute(k_dp_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_dp_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute attr[1];
-        int csz = g_cluster_size;
-        for (;;) {   // largest cluster size (<= requested) the device can co-schedule
-            cfg.gridDim = dim3(b->n_inst * csz);
-            cfg.blockDim = dim3(DC_T);
-            cfg.dynamicSmemBytes = smem;
-            cfg.stream = S(stream);
-            attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = csz;
-            attr[0].val.clusterDim.y = 1;
-            attr[0].val.clusterDim.z = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            int nclusters = 0;
-            if (cudaOccupancyMaxActiveClusters(&nclusters, k_dp_cluster, &cfg) == cudaSuccess && nclusters > 0) break;
-            cudaGetLastError();
-            if (csz <= 2) return fail(PP_ECUDA, "k_dp_cluster cannot be scheduled (smem %zu)", smem);
-            csz /= 2;
-        }
-        if (cudaLaunchKernelEx(&cfg, k_dp_cluster, *b) != cudaSuccess)
-            return fail(PP_ECUDA, "k_dp_cluster launch: %s", cudaGetErrorString(cudaGetLastError()));
-        PP_CHECK_LAUNCH("k_dp_cluster");
-    }
-    dim3 gb(b->n_inst, maxV);
-    k_backtrack<<<gb, 32, 0, S(stream)>>>(*b);
-    PP_CHECK_LAUNCH("k_backtrack");
-    return PP_OK;
-}
 
 static int prm_inst(const pp_batch* b, void* stream) {
     const int maxL = b->max_L, maxV = b->max_V;
@@ -394,39 +345,8 @@ int pp_step_trace(uint64_t* d_buf, int32_t cap) {
 
 // Debug: per-task timeline of the persistent DP into a caller device buffer of
 // 4 * cap u64 (NULL / 0 disables).  Not part of the planning path.
-int pp_dp_trace(uint64_t* d_buf, int32_t cap) {
-    unsigned long long* p = reinterpret_cast<unsigned long long*>(d_buf);
-    if (cudaMemcpyToSymbol(g_dp_trace, &p, sizeof(p)) != cudaSuccess ||
-        cudaMemcpyToSymbol(g_dp_trace_cap, &cap, sizeof(cap)) != cudaSuccess)
-        return fail(PP_ECUDA, "pp_dp_trace: %s", cudaGetErrorString(cudaGetLastError()));
-    return PP_OK;
-}
 
 
-static int prm_persist(const pp_batch* b, void* stream) {
-    const int maxL = b->max_L, maxV = b->max_V;
-    int rc;
-    if ((rc = prm_prep(b, stream))) return rc;
-    k_dp_reset<<<b->n_inst, 128, 0, S(stream)>>>(*b);
-    PP_CHECK_LAUNCH("k_dp_reset");
-    if (maxV > 1) {
-        const size_t cs = (size_t)(maxL + 1) / 2 + 1 + (size_t)(maxL - 1) * maxL / 2 +
-                          (size_t)(maxL > 1 ? maxL - 1 : 0) * (maxV - 1);
-        const size_t ex = (size_t)(maxV - 1) * (maxV - 1);
-        const size_t ch = (size_t)(DP_T / 32) * maxV;   // expand_r1's per-warp chan rows
-        const size_t smem = sizeof(double) * std::max(cs, std::max(ex, ch));
-        cudaFuncSetAttribute(k_dp_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dp_persist, DP_T, smem);
-        if (per_sm < 1) return fail(PP_ECUDA, "k_dp_persist does not fit an SM (smem %zu)", smem);
-        k_dp_persist<<<per_sm * num_sms(), DP_T, smem, S(stream)>>>(*b);
-        PP_CHECK_LAUNCH("k_dp_persist");
-    }
-    dim3 gb(b->n_inst, maxV);
-    k_backtrack<<<gb, 32, 0, S(stream)>>>(*b);
-    PP_CHECK_LAUNCH("k_backtrack");
-    return PP_OK;
-}
 
 int pp_prm(const pp_batch* b, void* stream) {
     if (b->n_inst <= 0) return PP_OK;
@@ -436,8 +356,6 @@ int pp_prm(const pp_batch* b, void* stream) {
         // (it beats the persistent kernel at every batch size once launches are free)
         const bool small = (int64_t)b->max_L * b->max_V <= PP_DP_INST_MAX_LV;
         if (mode == 3 || (mode == 2 && small && b->n_inst >= 2 * num_sms())) return prm_inst(b, stream);
-        if (mode == 4) return prm_cluster(b, stream);
-        if (mode == 1) return prm_persist(b, stream);
     }
     if (!(b->max_L <= SR_MAX && b->max_V <= SR_MAX)) return prm_groups(b, stream);
     return prm_steps_graph(b, stream);

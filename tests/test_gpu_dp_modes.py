@@ -29,7 +29,7 @@ def _cuda():
 
 @pytest.fixture
 def persistent():
-    prev = _lib.dp_persistent(True)
+    prev = _lib.dp_persistent(0)
     yield _lib.dp_persistent
     _lib.dp_persistent(prev)
 
@@ -47,13 +47,14 @@ def early_exit():
     _lib.dp_early_exit(prev)
 
 
-@pytest.mark.parametrize("mode", [(True, 0), (False, 0), (False, 1), (True, 3), (False, 3)])
+@pytest.mark.parametrize("mode", [(True, 0), (True, 3), (False, 3), (True, 2)])
 def test_early_exit_identical(persistent, early_exit, mode):
-    """Early exit on (default, persistent) vs off / per-step: identical results."""
+    """Per-step schedule with every candidate folded (no early exit) vs early
+    exit on / off in each schedule: identical results."""
     rng = random.Random(99)
     specs = _rand_specs(rng, 30, 60, 20) + [W.c3_gpt96(M=64, jitter_seed=3), W.c2_bert24()] + W.c4_batch(4)
     models = [s.to_model() for s in specs]
-    persistent(1); early_exit(True)
+    persistent(0); early_exit(False)
     ref = P.spp_many(models)
     persistent(mode[1]); early_exit(mode[0])
     got = P.spp_many(models)
@@ -74,7 +75,7 @@ def _rand_specs(rng, n, Lmax, Vmax, Mmax=32):
     return out
 
 
-def _both(persistent, specs, modes=(1, 0)):
+def _both(persistent, specs, modes=(3, 0)):
     models = [s.to_model() for s in specs]
     out = []
     for m in modes:
@@ -103,6 +104,12 @@ def test_c4_auto_batch_matches_oracle():
         assert res[k].makespan == want["makespan"], k
         assert [(e.stage_count, e.feasible, e.workload, e.makespan, e.bound) for e in res[k].sweep] == \
             [tuple(x) for x in want["sweep"]], k
+
+
+def test_mode_values_checked():
+    with pytest.raises(Exception, match="DP schedule 1"):
+        _lib.dp_persistent(1)
+    assert _lib.dp_persistent(2) == 2
 
 
 def test_mixed_batch_modes_identical(persistent):
@@ -145,20 +152,11 @@ def test_partition_solver_cells_modes_identical(persistent, allow):
         cells = [(l, x, r, i) for i in range(1, s.V + 1) for r in range(1, i + 1)
                  for x in range(1, i + 1) for l in range(1, s.L + 1) if (l + x + r + i) % 3 == 0]
         got = {}
-        for mode in (True, False):
+        for mode in (3, 0):
             persistent(mode)
             solver = P.PartitionSolver(prof, clu, order, M, allow_replication=allow)
             got[mode] = [(g.workload, g.stages) for g in solver.solve_many(cells)]
-        assert got[True] == got[False], s.name
-
-
-def test_cluster_per_instance_identical(persistent):
-    """One thread-block cluster per instance (mode 4) vs per-step, ragged batch + C3."""
-    rng = random.Random(777)
-    specs = _rand_specs(rng, 24, 60, 24) + [W.c2_bert24(), W.c3_gpt96(M=32, jitter_seed=7)] + W.c4_batch(4)
-    a, b = _both(persistent, specs, modes=(4, 0))
-    for s, x, y in zip(specs, a, b):
-        assert x == y, s.name
+        assert got[3] == got[0], s.name
 
 
 def test_graph_replay_across_batches(persistent):
@@ -169,7 +167,7 @@ def test_graph_replay_across_batches(persistent):
     from paper_2204_10562_b200 import _device, planner
     specs_a = [W.c3_gpt96(M=m, nodes=2, per_node=8) for m in (8, 32, 128)]
     specs_b = [W.c3_gpt96(M=m, jitter_seed=11, nodes=2, per_node=8) for m in (8, 32, 128)]
-    persistent(1)
+    persistent(3)
     want_a = P.spp_many([s.to_model() for s in specs_a])
     want_b = P.spp_many([s.to_model() for s in specs_b])
     persistent(0)

@@ -33,7 +33,7 @@ def main():
         items = [(_device.pack(p, c), M, _lib.PP_ALLOW_REPLICATION | sum_flags(), None)
                  for p, c, M in W.models_of(specs)]
         db = _device.DeviceBatch(items, capture_events=True)
-        for mode in [int(m) for m in os.environ.get('MODES', '1,0,3').split(',')]:
+        for mode in [int(m) for m in os.environ.get('MODES', '0,3').split(',')]:
             for ee in (True, False):
                 _lib.dp_persistent(mode); _lib.dp_early_exit(ee)
                 db.run("spp"); torch.cuda.synchronize()
