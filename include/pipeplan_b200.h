@@ -91,6 +91,11 @@ typedef struct {
     int32_t *ev_order;
     int32_t max_M;                    /* host copy: max microbatch count over the batch (0 = unknown;
                                          sizes the event-order launch)                        */
+    int64_t ws_doubles;               /* size of ws in doubles; > 0: pp_rdo / pp_prm / pp_spp check
+                                         every instance's workspace range (L, V limits and
+                                         ws_off + pp_layout's per-instance size <= ws_doubles)
+                                         against it first (one small D2H of the instance table +
+                                         a stream sync) and return PP_EINVAL; 0 = unchecked   */
 } pp_batch;
 
 /* ---- host helpers (no device work) ------------------------------------ */

@@ -64,7 +64,7 @@ class PPBatch(C.Structure):
                 ("ev_start", C.c_void_p), ("ev_end", C.c_void_p),
                 ("ar_start", C.c_void_p), ("ar_end", C.c_void_p),
                 ("ws", C.c_void_p), ("gamma", C.c_void_p), ("ev_order", C.c_void_p),
-                ("max_M", C.c_int32)]
+                ("max_M", C.c_int32), ("ws_doubles", C.c_int64)]
 
 
 class PPPlan(C.Structure):

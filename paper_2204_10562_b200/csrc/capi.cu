@@ -174,6 +174,28 @@ int pp_rdo_set_rounds(int32_t rounds) {
     return g_rdo_rounds.exchange(rounds);
 }
 
+// Workspace bounds check (pp_batch.ws_doubles > 0): the instance table lives in
+// device memory, so it is read back once (small, stream-ordered) and every
+// instance's shape and workspace range validated before any kernel touches ws.
+static int check_ws(const pp_batch* b, void* stream) {
+    if (b->ws_doubles <= 0 || b->n_inst <= 0) return PP_OK;
+    std::vector<pp_instance> h((size_t)b->n_inst);
+    if (cudaMemcpyAsync(h.data(), b->inst, sizeof(pp_instance) * h.size(), cudaMemcpyDeviceToHost, S(stream)) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(S(stream)) != cudaSuccess)
+        return fail(PP_ECUDA, "workspace check: %s", cudaGetErrorString(cudaGetLastError()));
+    for (int k = 0; k < b->n_inst; ++k) {
+        const pp_instance& I = h[(size_t)k];
+        if (I.L < 1 || I.L > PP_MAX_LAYERS || I.V < 1 || I.V > PP_MAX_GPUS || I.L > b->max_L || I.V > b->max_V)
+            return fail(PP_EINVAL, "instance %d: L=%d V=%d outside the batch limits", k, I.L, I.V);
+        const int64_t need = ws_layout(I.L, I.V).total;
+        if (I.ws_off < 0 || I.ws_off + need > b->ws_doubles)
+            return fail(PP_EINVAL, "instance %d: workspace [%lld, %lld) exceeds ws_doubles %lld", k,
+                        (long long)I.ws_off, (long long)(I.ws_off + need), (long long)b->ws_doubles);
+    }
+    return PP_OK;
+}
+
 // RDO deduplication across a batch (rdo.cu).  RDO is latency-bound (one CTA per
 // instance), so deduplicating only saves SM time once a batch has more
 // instances than ~2 waves of SMs; below that it is skipped (C3, 12 instances of
@@ -184,6 +206,7 @@ int pp_rdo_set_dedup(int32_t mode) { return g_rdo_dedup.exchange(mode < 0 || mod
 
 int pp_rdo(const pp_batch* b, void* stream) {
     if (b->n_inst <= 0) return PP_OK;
+    if (int rc = check_ws(b, stream)) return rc;
     const int V = b->max_V;
     const int dm = g_rdo_dedup.load();
     const int dedup = b->n_inst > 1 && (dm == 2 || (dm == 1 && b->n_inst > 2 * num_sms()));
@@ -350,6 +373,7 @@ int pp_step_trace(uint64_t* d_buf, int32_t cap) {
 
 int pp_prm(const pp_batch* b, void* stream) {
     if (b->n_inst <= 0) return PP_OK;
+    if (int rc = check_ws(b, stream)) return rc;
     const int mode = g_dp_persist.load();
     if (b->max_L <= SR_MAX && b->max_V <= SR_MAX) {
         // many SMALL instances: one CTA each; otherwise the graph-replayed per-step schedule

@@ -279,3 +279,21 @@ def test_edge_cases():
     bad = P.ModelProfile("bad", 1, (P.LayerProfile(1, math.inf, 2.0, 0.0),), ())
     with pytest.raises(P.ValidationError):
         P.spp(bad, P.make_cluster([1], []), 1)
+
+
+def test_workspace_bounds_check():
+    """pp_batch.ws_doubles > 0: pp_rdo / pp_prm / pp_spp validate every
+    instance's workspace range first (C callers); too small -> PP_EINVAL."""
+    from paper_2204_10562_b200 import _device, _lib, workloads as W
+    from paper_2204_10562_b200.partition import sum_flags
+    specs = [W.c2_bert24(), W.c4_instance(0)]
+    items = [(_device.pack(*s.to_model()[:2]), s.M, _lib.PP_ALLOW_REPLICATION | sum_flags(), None) for s in specs]
+    db = _device.DeviceBatch(items, capture_events=True)
+    db.batch.ws_doubles = db.sizes["ws"]
+    db.run("spp")   # exact size: accepted
+    h = db.fetch()
+    assert list(h["best_xi"]) == [len(r.plan.stages) for r in P.spp_many([s.to_model() for s in specs])]
+    db.batch.ws_doubles = db.sizes["ws"] - 1
+    with pytest.raises(RuntimeError, match="exceeds ws_doubles"):
+        db.run("spp")
+    db.batch.ws_doubles = 0
