@@ -279,6 +279,8 @@ struct SideStreams {
     // split chain (prm_chain_split_p): per group 3 bulk streams + its events
     cudaStream_t x[3 * PP_DP_STREAMS];
     cudaEvent_t xfork[PP_DP_STREAMS], c1[PP_DP_STREAMS][2], cb[PP_DP_STREAMS][3];
+    cudaStream_t aux;              // pp_spp: phi beside RDO + DP
+    cudaEvent_t aux_fork, aux_done;
 };
 static thread_local SideStreams g_side;
 
@@ -408,7 +410,10 @@ static int ensure_side_streams() {
         if (!ok) return fail(PP_ECUDA, "side stream creation: %s", cudaGetErrorString(cudaGetLastError()));
     }
     if (cudaEventCreateWithFlags(&g_side.fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&g_side.capture, cudaStreamNonBlocking) != cudaSuccess)
+        cudaStreamCreateWithFlags(&g_side.capture, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&g_side.aux, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_side.aux_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_side.aux_done, cudaEventDisableTiming) != cudaSuccess)
         return fail(PP_ECUDA, "event creation: %s", cudaGetErrorString(cudaGetLastError()));
     if (const char* e = getenv("PP_BULK")) {   // A/B knob: 0 stages the combine with per-element cp.async
         const int v = atoi(e);
@@ -849,9 +854,16 @@ int pp_phi(const pp_batch* b, void* stream) {
 
 int pp_spp(const pp_batch* b, void* stream) {
     int rc;
-    if ((rc = pp_phi(b, stream))) return rc;
+    if ((rc = ensure_side_streams())) return rc;
+    // phi (cost.py:131-142) depends on the inputs only: it runs on a side stream
+    // beside RDO and the DP (only the host reads it), joined before the sweep
+    cudaEventRecord(g_side.aux_fork, S(stream));
+    cudaStreamWaitEvent(g_side.aux, g_side.aux_fork, 0);
+    if ((rc = pp_phi(b, g_side.aux))) return rc;
+    cudaEventRecord(g_side.aux_done, g_side.aux);
     if ((rc = pp_rdo(b, stream))) return rc;
     if ((rc = pp_prm(b, stream))) return rc;
+    cudaStreamWaitEvent(S(stream), g_side.aux_done, 0);
     if ((rc = pp_pe_sweep(b, stream))) return rc;
     return pp_select(b, stream);
 }
