@@ -224,25 +224,62 @@ class DeviceBatch:
 
     # -- results --------------------------------------------------------------
     def fetch(self):
-        """Copy all outputs to host numpy (one D2H per dtype)."""
-        # pinned destinations (torch's caching host allocator), async copies, one sync
-        srcs = (self.d_fout, self.d_iout, self.d_iin[self.n_ib:])
+        """Copy the outputs to host numpy.  Everything but the schedule events in one
+        D2H per dtype; the events (capacity M (4V - 3) per instance, of which the
+        chosen plan uses M (4 xi - 3)) are then gathered on the device to just the
+        used prefixes and copied compactly (h["ev_coff"][k] = instance k's offset)."""
+        stream = torch.cuda.current_stream()
+        fe, ie = int(self.f_off[8]), int(self.i_off[6])   # starts of ev_start / ev_order
+        srcs = (self.d_fout[:fe], self.d_iout[:ie], self.d_iin[self.n_ib:])
         dst = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in srcs]
         for d, t in zip(dst, srcs):
             d.copy_(t, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        stream.synchronize()
         fo, io, order = (d.numpy() for d in dst)
         f = {k: fo[int(self.f_off[i]):int(self.f_off[i + 1])]
              for i, k in enumerate(("sweep_w", "sweep_mk", "sweep_bound", "best_mk", "phi", "gamma",
-                                    "ar_start", "ar_end", "ev_start", "ev_end"))}
+                                    "ar_start", "ar_end"))}
         g = {k: io[int(self.i_off[i]):int(self.i_off[i + 1])]
-             for i, k in enumerate(("sweep_r", "ls", "le", "dlo", "dhi", "best_xi", "ev_order"))}
+             for i, k in enumerate(("sweep_r", "ls", "le", "dlo", "dhi", "best_xi"))}
         f.update(g)
         f["order"] = order
+        if self.capture_events:
+            bx = g["best_xi"]
+            ev_s = self.d_fout[fe:int(self.f_off[9])]
+            ev_e = self.d_fout[int(self.f_off[9]):int(self.f_off[10])]
+            ev_o = self.d_iout[ie:int(self.i_off[7])]
+            parts_s, parts_e, parts_o, coff, c = [], [], [], np.zeros(self.n, np.int64), 0
+            for k in range(self.n):
+                x = int(bx[k])
+                cnt = self.items[k][1] * (4 * x - 3) if x > 0 else 0
+                coff[k] = c
+                if cnt:
+                    o = self.inst_host[k].ev_off
+                    parts_s.append(ev_s[o:o + cnt]); parts_e.append(ev_e[o:o + cnt]); parts_o.append(ev_o[o:o + cnt])
+                    c += cnt
+            self._d2h_events = c
+            if c:
+                dev_f = torch.cat(parts_s + parts_e)
+                dev_i = torch.cat(parts_o)
+                hf = torch.empty(dev_f.shape, dtype=dev_f.dtype, pin_memory=True)
+                hi = torch.empty(dev_i.shape, dtype=dev_i.dtype, pin_memory=True)
+                hf.copy_(dev_f, non_blocking=True)
+                hi.copy_(dev_i, non_blocking=True)
+                stream.synchronize()
+                hfn = hf.numpy()
+                f["ev_start"], f["ev_end"], f["ev_order"] = hfn[:c], hfn[c:], hi.numpy()
+            else:
+                f["ev_start"] = f["ev_end"] = np.zeros(0)
+                f["ev_order"] = np.zeros(0, np.int32)
+            f["ev_coff"] = coff
         return f
 
     def d2h_bytes(self):
-        return (self.d_fout.numel() * 8 + self.d_iout.numel() * 4 + (self.d_iin.numel() - self.n_ib) * 4)
+        """Bytes of the last fetch (events: only the chosen plans' prefixes)."""
+        ev = getattr(self, "_d2h_events", None)
+        if ev is None:   # before any fetch: the full capacity
+            return (self.d_fout.numel() * 8 + self.d_iout.numel() * 4 + (self.d_iin.numel() - self.n_ib) * 4)
+        return int(self.f_off[8]) * 8 + int(self.i_off[6]) * 4 + (self.d_iin.numel() - self.n_ib) * 4 + ev * 20
 
     def h2d_bytes(self):
         return self.d_fin.numel() * 8 + self.d_iin.numel() * 4

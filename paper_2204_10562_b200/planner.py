@@ -192,9 +192,10 @@ def _decode(db: _device.DeviceBatch, h, k: int, M: int, packed) -> SppResult:
     plan = Plan(stages=stages, microbatch_count=M)
     J = 4 * xi - 3
     mk = float(h["best_mk"][k])
+    eo = int(h["ev_coff"][k])   # compact events of the chosen plans (_device.DeviceBatch.fetch)
     rec = dict(makespan=mk,
-               ev_start=h["ev_start"][I.ev_off:I.ev_off + M * J], ev_end=h["ev_end"][I.ev_off:I.ev_off + M * J],
-               ev_order=h["ev_order"][I.ev_off:I.ev_off + M * J],
+               ev_start=h["ev_start"][eo:eo + M * J], ev_end=h["ev_end"][eo:eo + M * J],
+               ev_order=h["ev_order"][eo:eo + M * J],
                ar_start=h["ar_start"][I.ar_off:I.ar_off + xi], ar_end=h["ar_end"][I.ar_off:I.ar_off + xi])
     schedule = _build_schedule(plan, rec)
     p = float(h["phi"][k])
