@@ -763,7 +763,6 @@ __global__ void __launch_bounds__(CD_T, 2) k_combine_diag(pp_batch b, int j, int
     const bool dp_cells = (allow || r == 1) && cA <= cB;   // partition.py:103-104
     const int ncol = dp_cells ? cB - cA + 1 : 0;
     const int TX = ncol >= 4 ? 4 : (ncol >= 2 ? 2 : 1);
-    const int wx = dp_cells ? (ncol + TX - 1) / TX * TX : 0;
     for (int e = threadIdx.x; e < nl * nx; e += CD_T) {   // xi = 1, xi > j + 1, disabled widths
         const int l = l0 + e / nx, xi = x0 + e % nx;
         if (dp_cells && xi >= cA && xi <= cB) continue;
