@@ -22,7 +22,6 @@ __global__ void k_expand_s_p(const pp_batch* bp, int j, int rfirst, int rlast);
 __global__ void k_expand_m_p(const pp_batch* bp, int j, int rb);
 __global__ void k_combine_s_p(const pp_batch* bp, int j, int r0);
 __global__ void k_combine_bis_p(const pp_batch* bp, int j, int r0, int rg, int rb);
-__global__ void k_crit_step_p(const pp_batch* bp, int j, int ncl, int rg);
 __global__ void k_backtrack_p(const pp_batch* bp);
 __global__ void k_phi(pp_batch b);
 __global__ void k_base(pp_batch b, int full_rows);
@@ -111,12 +110,6 @@ static const int g_dp_split = getenv("PP_DP_SPLIT") ? atoi(getenv("PP_DP_SPLIT")
 static const int g_c1_parts = getenv("PP_C1_PARTS") ? std::max(1, std::min(64, atoi(getenv("PP_C1_PARTS")))) : 32;
 // programmatic dependent launch in the per-step chain (PP_PDL=0 disables)
 static const int g_pdl = getenv("PP_PDL") ? atoi(getenv("PP_PDL")) : 1;
-// split chain: the critical E1 + C1 of a step fused into one cluster launch
-// (combine_bis.cu k_crit_step_p); PP_CRIT_FUSED=0 keeps two launches; cluster size PP_CRIT_CLUSTER
-static const int g_crit_fused = getenv("PP_CRIT_FUSED") ? atoi(getenv("PP_CRIT_FUSED")) : 1;
-static const int g_crit_cluster = getenv("PP_CRIT_CLUSTER") ? std::max(2, std::min(16, atoi(getenv("PP_CRIT_CLUSTER")))) : 8;
-// timing experiment only (wrong results): the split chain without its bulk items
-static const int g_skip_bulk = getenv("PP_SKIP_BULK_EXPERIMENT") ? atoi(getenv("PP_SKIP_BULK_EXPERIMENT")) : 0;
 // combine kernel of the per-step schedule: 1 = crossing search (combine_bis.cu),
 // 0 = exhaustive register tiles (k_combine_s_p), 2 = auto; same bits either way
 static const int g_bis_rb = getenv("PP_BIS_RB") ? atoi(getenv("PP_BIS_RB")) : 0;   // rows per thread (0 = auto)
@@ -680,46 +673,13 @@ static int prm_chain_split_p(const pp_batch* b, const pp_batch* db, void* stream
     auto combine = [&](cudaStream_t st, int j, int r0, int nitems, int parts) -> int {
         return launch_combine(b, db, st, pdl, j, r0, nitems, parts, total_inst);
     };
-    auto crit = [&](cudaStream_t st, int j) -> int {
-        const int ncl = g_crit_cluster, rg = (maxL + ncl - 1) / ncl;
-        const size_t e_sm = (size_t)((maxL - 1 + ncl - 1) / ncl) * j;
-        const size_t smem = sizeof(double) * std::max(e_sm, combine_bis_smem_doubles(maxL, j, rg));
-        cudaLaunchAttribute at[2];
-        at[0] = pdl[0];
-        at[1].id = cudaLaunchAttributeClusterDimension;
-        at[1].val.clusterDim.x = ncl;
-        at[1].val.clusterDim.y = 1;
-        at[1].val.clusterDim.z = 1;
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(b->n_inst * ncl);
-        cfg.blockDim = dim3(256);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = st;
-        cfg.attrs = at;
-        cfg.numAttrs = 2;
-        if (cudaLaunchKernelEx(&cfg, k_crit_step_p, db, j, ncl, rg) != cudaSuccess)
-            return fail(PP_ECUDA, "k_crit_step launch: %s", cudaGetErrorString(cudaGetLastError()));
-        PP_CHECK_LAUNCH("k_crit_step");
-        return PP_OK;
-    };
-    if (g_crit_fused) {
-        cudaFuncSetAttribute(k_crit_step_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(double) * std::max((size_t)(maxL - 1 + g_crit_cluster - 1) / g_crit_cluster * maxV,
-                                                             combine_bis_smem_doubles(maxL, maxV,
-                                                                                      (maxL + g_crit_cluster - 1) / g_crit_cluster))));
-        if (g_crit_cluster > 8) cudaFuncSetAttribute(k_crit_step_p, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    }
     for (int j = 1; j < maxV; ++j) {
         if (j >= 3) cudaStreamWaitEvent(s0, cb[(j - 2) % 3], 0);
         if (j >= 4) cudaStreamWaitEvent(s0, cb[(j - 3) % 3], 0);
-        if (g_crit_fused) {
-            if ((rc = crit(s0, j))) return rc;
-        } else {
-            if ((rc = expand(s0, j, 1, 1))) return rc;
-            if ((rc = combine(s0, j, 1, 1, g_c1_parts))) return rc;
-        }
+        if ((rc = expand(s0, j, 1, 1))) return rc;
+        if ((rc = combine(s0, j, 1, 1, g_c1_parts))) return rc;
         cudaEventRecord(c1[j % 2], s0);
-        if (maxV - j >= 2 && !g_skip_bulk) {
+        if (maxV - j >= 2) {
             cudaStream_t sk = sx[j % 3];
             cudaStreamWaitEvent(sk, c1[(j - 1) % 2], 0);
             if (j >= 3) cudaStreamWaitEvent(sk, cb[(j - 2) % 3], 0);

@@ -216,76 +216,3 @@ __global__ void __launch_bounds__(CB_T, 2) k_combine_bis_p(const pp_batch* __res
 }
 
 }  // namespace pp
-
-namespace pp {
-
-// ----------------------------------------------------------------------------
-// The critical step of the split chain (capi.cu prm_chain_split_p), fused:
-// E1(j) — the expand of target r = 1 (X(l', xi, 1, j + 1), partition.py:132-137)
-// — and C1(j) — the combine of item (1, j + 1) (partition.py:126-141) — in ONE
-// launch of a thread-block cluster per instance, a cluster barrier between
-// them instead of a kernel boundary.  E: one thread per cell (l', xi), the
-// row's chan values (class table or the same division) staged per CTA; X goes
-// to global memory (the backtrack reads it) and, after barrier.cluster
-// (release / acquire: the other CTAs' X writes are visible), C runs
-// combine_item_bis on the CTA's row group.  Same expressions, same bits.
-// ----------------------------------------------------------------------------
-constexpr int CRIT_T = 256;
-
-__global__ void __launch_bounds__(CRIT_T, 1) k_crit_step_p(const pp_batch* __restrict__ bp, int j, int ncl, int rg) {
-    pdl_trigger_at<0>();
-    StepTrace tr;
-    tr.begin();
-    const pp_batch b = *bp;
-    const int inst = blockIdx.x / ncl, cr = blockIdx.x % ncl;
-    const pp_instance I = b.inst[inst];
-    const int L = I.L, V = I.V, M = I.M;
-    const bool live = j < V;   // uniform over the cluster (one instance)
-    extern __shared__ __align__(16) double cs_smem[];
-    const int t = threadIdx.x;
-    if (live && L > 1) {
-        const WsLayout lay = ws_layout(L, V);
-        double* ws = b.ws + I.ws_off;
-        const bool allow = I.flags & PP_ALLOW_REPLICATION;
-        const int i = j + 1, lm = L - 1;
-        const int per = (lm + ncl - 1) / ncl, ra = 1 + cr * per, rb = min(lm, ra + per - 1);
-        const int nrow = rb - ra + 1;
-        double* ch = cs_smem;   // [row][r'-1] = chan(l', r', 1, i)
-        if (nrow > 0) {
-            const int* rcls = reinterpret_cast<const int*>(ws + lay.chcls + CHAN_CLS);
-            const double* cross = ws + lay.cross;
-            for (int e = t; e < nrow * j; e += blockDim.x) {
-                const int k = e / j, rp = e - k * j + 1, lp = ra + k;
-                const int cls = rcls[lp];
-                if (cls >= 0) {
-                    ch[e] = ws[lay.chan + (int64_t)cls * tet(V) + chan_step(V, j) + (int64_t)(rp - 1) * (V - j)];
-                } else {
-                    const double Mp = (double)M * (b.efwd[I.layer_off + lp - 1] + b.ebwd[I.layer_off + lp - 1]);
-                    ch[e] = Mp / ((double)(rp * 1) * cross[cross_idx(V, i, 1, rp)]);   // partition.py:131,137
-                }
-            }
-        }
-        __syncthreads();
-        pdl_wait();   // W_j complete
-        const double* W = ws + lay.W;
-        double* X = ws + lay.X + X_base(L, i, 1);
-        for (int e = t; e < nrow * j; e += blockDim.x) {
-            const int k = e / j, c = e - k * j, lp = ra + k, xi = c + 2;
-            double acc = PP_INF;
-            if (xi - 1 <= lp) {   // W_j(l', xi', .) = inf for xi' > l'
-                const int kend = xi == 2 ? j : j - xi + 2;
-                const double* chr = ch + k * j;
-                for (int rp = (xi == 2 ? j : 1); rp <= kend; ++rp)
-                    acc = dmin(acc, dmax(W_at(W, L, j, lp, rp, xi - 1, allow), chr[rp - 1]));
-            }
-            X[(int64_t)(lp - 1) * j + c] = acc;
-        }
-    }
-    // every CTA of the cluster reaches the barrier (release: X written; acquire: X of all rows visible)
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-    if (live) combine_item_bis(b, I, j, 1, 1 + cr * rg, rg, 1, cs_smem);
-    pdl_trigger_at<2>();
-    tr.end(2, j);
-}
-
-}  // namespace pp
