@@ -2,18 +2,20 @@
 # Round-2 measurement set (GPU box, repo root; outputs in gpurun_out/r2m_*)
 set -x
 python bench.py --steps 50 --warmup 5 > gpurun_out/r2m_c3.json 2> gpurun_out/r2m_c3.err
+python tools/c5_full_dp.py > gpurun_out/r2m_c5_full_dp.txt 2>&1
+python tools/dp_combine_ab.py 1 12 24 > gpurun_out/r2m_dp_ab.txt 2>&1
 python bench.py --workload c4 --steps 10 --warmup 3 > gpurun_out/r2m_c4.json 2> gpurun_out/r2m_c4.err
 python bench.py --workload c5 --steps 20 --warmup 3 > gpurun_out/r2m_c5.json 2> gpurun_out/r2m_c5.err
 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r2m_ref.json 2> gpurun_out/r2m_ref.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2m_launches_c3.csv python bench.py --profile-steps 1 > /dev/null 2>&1
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --cache-control none --csv --log-file gpurun_out/r2m_traffic_warm.csv python bench.py --profile-steps 1 > /dev/null 2>&1
-python tools/dp_traffic.py gpurun_out/r2m_traffic_warm.csv profiles/r02_dp_traffic_warm.json 1 warm
+python tools/dp_traffic.py gpurun_out/r2m_traffic_warm.csv gpurun_out/r02_dp_traffic_warm.json 1 warm
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2m_traffic_cold.csv python bench.py --profile-steps 1 > /dev/null 2>&1
-python tools/dp_traffic.py gpurun_out/r2m_traffic_cold.csv profiles/r02_dp_traffic_cold.json 1
-for k in k_combine_s_p:120 k_expand_m_p:60 k_rdo_cut:0 k_rdo:0 k_pe_sweep_w:0 k_event_merge:0 k_select:0 k_backtrack_p:0 k_stab_big_p:0; do
+python tools/dp_traffic.py gpurun_out/r2m_traffic_cold.csv gpurun_out/r02_dp_traffic_cold.json 1
+for k in k_combine_s_p:120 k_expand_m_p:60 k_rdo_cut:0 "k_rdo<":0 k_pe_sweep_w:0 k_event_merge:0 k_select:0 k_backtrack_p:0 k_stab_big_p:0; do
   name=${k%%:*}; skip=${k##*:}
-  ncu --set full --import-source on --clock-control none -k regex:"${name}" -s $skip -c 1 -o /tmp/r2m_ncu_${name} python bench.py --profile-steps 1 > /dev/null 2>&1
-  (python tools/summarize_ncu.py /tmp/r2m_ncu_${name}.ncu-rep; python tools/ncu_lines.py /tmp/r2m_ncu_${name}.ncu-rep 25) > gpurun_out/r2m_ncu_${name}.txt 2>&1
+  ncu --set full --import-source on --clock-control none -k regex:"${name}" -s $skip -c 1 -o /tmp/r2m_ncu_${name//</_} python bench.py --profile-steps 1 > /dev/null 2>&1
+  (python tools/summarize_ncu.py /tmp/r2m_ncu_${name//</_}.ncu-rep; python tools/ncu_lines.py /tmp/r2m_ncu_${name//</_}.ncu-rep 25) > gpurun_out/r2m_ncu_${name//</_}.txt 2>&1
 done
 bash tools/prof_c4.sh > /dev/null 2>&1
 (python tools/summarize_ncu.py gpurun_out/dpinst_c4.ncu-rep; python tools/ncu_lines.py gpurun_out/dpinst_c4.ncu-rep 25) > gpurun_out/r2m_ncu_dp_inst_c4.txt 2>&1
