@@ -67,6 +67,9 @@ def parse():
     ap.add_argument("--profile-steps", type=int, default=0, help="(for ncu) run N untimed steps and exit")
     ap.add_argument("--workload", default="c3", choices=["c3", "c4", "c5"],
                     help="c3 = the headline (BASELINE.json metric); c4/c5 = secondary configs (strong scaling)")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="TEST ONLY: every rank on cuda:0 with gloo collectives (exercises the N-rank "
+                         "launch / sharding / min-loc path on a one-GPU box; not a scaling number)")
     ap.add_argument("--clock-soak-s", type=float, default=1.0,
                     help="untimed load steps right before the timed region, sampled for clocks with it")
     return ap.parse_args()
@@ -85,7 +88,7 @@ def maybe_self_launch(args):
         return
     import socket
     import torch
-    if torch.cuda.device_count() < args.gpus:
+    if torch.cuda.device_count() < args.gpus and not args.share_gpu:
         print(f"bench.py: --gpus {args.gpus} but only {torch.cuda.device_count()} visible", file=sys.stderr)
         sys.exit(2)
     s = socket.socket()
@@ -97,11 +100,17 @@ def maybe_self_launch(args):
     os.execv(sys.executable, cmd)
 
 
+SHARE_GPU = "--share-gpu" in sys.argv
+
+
 def init_dist(local):
     """NCCL process group (one rank per GPU); INIT logs to stderr so the
-    communicator's rank count is visible."""
+    communicator's rank count is visible.  --share-gpu: gloo (test only)."""
     import torch
     import torch.distributed as dist
+    if SHARE_GPU:
+        dist.init_process_group("gloo")
+        return
     os.environ.setdefault("NCCL_DEBUG", "INFO")
     os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
@@ -111,7 +120,7 @@ def init_dist(local):
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if SHARE_GPU else int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
 
 
@@ -372,6 +381,8 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "host": host_info(),
     }
+    if SHARE_GPU:
+        line["share_gpu_test"] = "all ranks on cuda:0, gloo collectives: exercises the N-rank path, not a scaling number"
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -648,6 +659,8 @@ def run_secondary(args):
             line["cpu_baseline"] = {"value": cexec / dt, "unit": "block executions/s", "cores": nt, "kind": "port",
                                     "sample": f"32 of the 256 plans (every 8th xi) on {nt} threads, {dt:.1f} s"}
     if rank == 0:
+        if SHARE_GPU:
+            line["share_gpu_test"] = "all ranks on cuda:0, gloo collectives: exercises the N-rank path, not a scaling number"
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
