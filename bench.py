@@ -607,7 +607,7 @@ def run_secondary(args):
         ids = sorted(spec.gpu_ids)
         pos = {g: k for k, g in enumerate(ids)}
         packed = _device.pack(profile, cluster)
-        db = _device.DeviceBatch([(packed, M, sum_flags(), None)], capture_events=False)
+        db = _device.DeviceBatch([(packed, M, sum_flags(), None)], capture_events=False, workspace=False)
         xis = [k + 1 for k in shard(256, rank, world)]
 
         def plans():

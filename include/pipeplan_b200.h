@@ -82,7 +82,10 @@ typedef struct {
     /* schedule of the selected plan (optional: NULL skips event capture) */
     double *ev_start, *ev_end;
     double *ar_start, *ar_end;
-    double *ws;                       /* fp64 workspace, pp_layout() doubles                      */
+    double *ws;                       /* fp64 workspace, pp_layout() doubles.  May be NULL for a
+                                         batch used only with pp_phi / pp_simulate (caller plans
+                                         need no DP tables); every other entry point then fails
+                                         with PP_EINVAL instead of touching it                  */
     double *gamma;                    /* [n_inst] cost.py:126-128, written by pp_phi; NULL skips  */
     /* schedule order of the selected plan's events (optional, needs ev_start):
      * ev_order[ev_off + k] = (m-1)*(4N-3) + pos-1 of the k-th event of the

@@ -138,9 +138,13 @@ class DeviceBatch:
     """A batch of planning instances resident on the GPU with all outputs.
 
     items: list of (Packed, M, flags, order_positions or None).
+    workspace=False skips the pp_layout fp64 workspace (RDO / DP / sweep
+    tables; L V^3 / 2 doubles at the largest shapes, 68 GB for 1024 x 256):
+    such a batch serves pp_phi and caller-plan simulation (pp_simulate) only,
+    and the library refuses the other entry points on it.
     """
 
-    def __init__(self, items, capture_events=True):
+    def __init__(self, items, capture_events=True, workspace=True):
         lib = _lib.load()
         dev = device()
         self.items = items
@@ -184,7 +188,7 @@ class DeviceBatch:
         # int32 outputs: [sweep_r | ls | le | dlo | dhi | best_xi | ev_order]
         self.i_off = np.cumsum([0, n_sweep, n_stage, n_stage, n_stage, n_stage, n, ev])
         self.d_iout = torch.empty(int(self.i_off[-1]), dtype=I32, device=dev)
-        self.d_ws = torch.empty(max(n_ws, 1), dtype=F64, device=dev)
+        self.d_ws = torch.empty(max(n_ws, 1), dtype=F64, device=dev) if workspace else None
         self.capture_events = capture_events
         self.n_ib = ib.size
         b = PPBatch()
@@ -212,7 +216,7 @@ class DeviceBatch:
         io_ = [io + 4 * int(x) for x in self.i_off]
         b.sweep_r, b.stage_ls, b.stage_le, b.stage_dlo, b.stage_dhi, b.best_xi = io_[:6]
         b.ev_order = io_[6] if capture_events else None
-        b.ws = self.d_ws.data_ptr()
+        b.ws = self.d_ws.data_ptr() if workspace else None
         self.batch = b
         self.lib = lib
 

@@ -40,7 +40,7 @@ def _plan_costs(stage_lists, profile: ModelProfile, cluster: ClusterGraph, M: in
     check_numeric_range(profile, cluster)
     packed = _device.pack(profile, cluster)
     pos = {g: k for k, g in enumerate(packed.ids)}
-    db = _device.DeviceBatch([(packed, M, sum_flags(), None)], capture_events=False)
+    db = _device.DeviceBatch([(packed, M, sum_flags(), None)], capture_events=False, workspace=False)
     sps = [_device.SimPlan(inst=0, M=M, stages=[(a, b, [pos[d] for d in devs]) for a, b, devs in st],
                            flags=_lib.PP_SIM_COSTS_ONLY) for st in stage_lists]
     return _device.SimRun(db, sps, capture_events=False, costs=True).fetch()
@@ -266,7 +266,8 @@ def block_duration(block: Block, plan: Plan, profile: ModelProfile, cluster: Clu
 
 def _gamma_phi(profile: ModelProfile, cluster: ClusterGraph) -> Tuple[float, float]:
     check_numeric_range(profile, cluster)
-    db = _device.DeviceBatch([(_device.pack(profile, cluster), 1, sum_flags(), None)], capture_events=False)
+    db = _device.DeviceBatch([(_device.pack(profile, cluster), 1, sum_flags(), None)], capture_events=False,
+                             workspace=False)
     db.run("phi")
     h = db.fetch()
     return float(h["gamma"][0]), float(h["phi"][0])

@@ -178,6 +178,9 @@ int pp_rdo_set_rounds(int32_t rounds) {
 // device memory, so it is read back once (small, stream-ordered) and every
 // instance's shape and workspace range validated before any kernel touches ws.
 static int check_ws(const pp_batch* b, void* stream) {
+    if (b->n_inst > 0 && b->ws == nullptr)
+        return fail(PP_EINVAL, "pp_batch.ws is NULL: RDO / DP / sweep need the pp_layout workspace "
+                               "(only pp_phi and pp_simulate run without one)");
     if (b->ws_doubles <= 0 || b->n_inst <= 0) return PP_OK;
     std::vector<pp_instance> h((size_t)b->n_inst);
     if (cudaMemcpyAsync(h.data(), b->inst, sizeof(pp_instance) * h.size(), cudaMemcpyDeviceToHost, S(stream)) !=
@@ -804,6 +807,7 @@ static int sim_block(int maxN) {
 
 int pp_pe_sweep(const pp_batch* b, void* stream) {
     if (b->n_inst <= 0) return PP_OK;
+    if (!b->ws) return fail(PP_EINVAL, "pp_pe_sweep: pp_batch.ws is NULL (the sweep reads the DP's slice tables)");
     dim3 g(b->n_inst, b->max_V);
     if (b->max_V <= PE_WARP_MAXN) {   // one warp per plan: registers + shuffles per pass
         k_pe_sweep_w<<<g, 32, 0, S(stream)>>>(*b);
@@ -817,6 +821,7 @@ int pp_pe_sweep(const pp_batch* b, void* stream) {
 
 int pp_select(const pp_batch* b, void* stream) {
     if (b->n_inst <= 0) return PP_OK;
+    if (b->ev_start && !b->ws) return fail(PP_EINVAL, "pp_select: pp_batch.ws is NULL (the replay reads the DP's slice tables)");
     k_select<<<b->n_inst, 32, 0, S(stream)>>>(*b);
     PP_CHECK_LAUNCH("k_select");
     if (b->ev_start) {
@@ -872,6 +877,7 @@ int pp_prm_query(const pp_batch* b, int32_t n_query, const int32_t* q_inst, cons
                  const int32_t* q_xi, const int32_t* q_r, const int32_t* q_i, int32_t max_xi, double* w,
                  int32_t* frag, int32_t* feasible, void* stream) {
     if (n_query <= 0) return PP_OK;
+    if (!b->ws) return fail(PP_EINVAL, "pp_prm_query: pp_batch.ws is NULL (queries read the DP slices)");
     k_query<<<n_query, 32, 0, S(stream)>>>(*b, n_query, q_inst, q_l, q_xi, q_r, q_i, max_xi, w, frag, feasible);
     PP_CHECK_LAUNCH("k_query");
     return PP_OK;
@@ -903,6 +909,7 @@ int pp_min_cut(const pp_batch* b, int32_t k, const int32_t* verts, int32_t n, ui
     if (n < 2) return fail(PP_EINVAL, "min cut needs at least 2 vertices");
     const int V = b->max_V;
     const int in_smem = V <= RDO_SMEM_MAX;
+    if (!in_smem && !b->ws) return fail(PP_EINVAL, "pp_min_cut: V=%d > %d needs pp_batch.ws", V, RDO_SMEM_MAX);
     const size_t smem = (in_smem ? sizeof(double) * V * V : 0) + rdo_state_bytes(V);
     if (in_smem) {
         cudaFuncSetAttribute(k_min_cut<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -220,7 +220,8 @@ def spp(profile: ModelProfile, cluster: ClusterGraph, microbatch_count: int) -> 
 def phi(profile: ModelProfile, cluster: ClusterGraph) -> float:
     """Bandwidth-heterogeneity penalty (cost.py:131-142), evaluated on the GPU."""
     check_numeric_range(profile, cluster)
-    db = _device.DeviceBatch([(_device.pack(profile, cluster), 1, sum_flags(), None)], capture_events=False)
+    db = _device.DeviceBatch([(_device.pack(profile, cluster), 1, sum_flags(), None)], capture_events=False,
+                             workspace=False)
     db.run("phi")
     return float(db.fetch()["phi"][0])
 

@@ -166,7 +166,8 @@ def _sim(plan, profile, cluster, queue_lists=None, forward_barrier=False, captur
     _check_plan(plan, profile, cluster)
     packed = _device.pack(profile, cluster)
     pos = {g: k for k, g in enumerate(packed.ids)}
-    db = _device.DeviceBatch([(packed, plan.microbatch_count, sum_flags(), None)], capture_events=False)
+    db = _device.DeviceBatch([(packed, plan.microbatch_count, sum_flags(), None)], capture_events=False,
+                             workspace=False)
     stages = [(s.layer_start, s.layer_end, [pos[d] for d in s.devices]) for s in plan.stages]
     flags = (_lib.PP_SIM_FORWARD_BARRIER if forward_barrier else 0)
     if cycle:
@@ -263,7 +264,7 @@ def simulate_pe_many(plans: Sequence[Plan], profile: ModelProfile, cluster: Clus
     packed = _device.pack(profile, cluster)
     pos = {g: k for k, g in enumerate(packed.ids)}
     db = _device.DeviceBatch([(packed, max(p.microbatch_count for p in plans), sum_flags(), None)],
-                             capture_events=False)
+                             capture_events=False, workspace=False)
     sps = [_device.SimPlan(inst=0, M=p.microbatch_count,
                            stages=[(s.layer_start, s.layer_end, [pos[d] for d in s.devices]) for s in p.stages],
                            flags=_lib.PP_SIM_PE_ORDER) for p in plans]

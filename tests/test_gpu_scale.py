@@ -66,7 +66,13 @@ def test_c5_candidate_simulation_vs_oracle():
         st = W.even_split_plan(spec.L, order, xi)
         plans.append(P.Plan(tuple(P.Stage(n + 1, a, b, d) for n, (a, b, d) in enumerate(st)), M))
         oplans.append(O.Plan([(a, b, tuple(pos[g] for g in d)) for a, b, d in st], M))
+    import torch
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats()
+    base = torch.cuda.memory_allocated()
     got = P.simulate_pe_many(plans, profile, cluster)
+    # caller-plan simulation allocates no DP workspace (68 GB at 1024 x 256)
+    assert torch.cuda.max_memory_allocated() - base < 1 << 30
     want = O.simulate_pe_batch(inst, oplans, 16)
     assert [m for m, _ in got] == list(want)
     best = min(range(256), key=lambda k: (got[k][0], k))
@@ -92,3 +98,21 @@ def test_c5_scaled_chunked_dp_vs_oracle_golden():
         assert [[e.stage_count, e.feasible, h(e.workload), h(e.makespan), h(e.bound)] for e in r.sweep] == c["sweep"]
         assert [[s.layer_start, s.layer_end, list(s.devices)] for s in r.plan.stages] == c["plan"]["stages"]
         assert (h(r.makespan), h(r.phi), h(r.theorem_factor)) == (c["makespan"], c["phi"], c["theorem_factor"])
+
+
+def test_batch_without_workspace_serves_simulation_only():
+    """DeviceBatch(workspace=False) (pp_batch.ws = NULL): pp_phi and pp_simulate
+    run; RDO, the DP, the sweep and the select+replay refuse instead of touching
+    a NULL workspace."""
+    from paper_2204_10562_b200 import _device
+    from paper_2204_10562_b200.partition import sum_flags
+    spec = W.c4_batch(1)[0]
+    profile, cluster, M = spec.to_model()
+    db = _device.DeviceBatch([(_device.pack(profile, cluster), M, sum_flags(), None)], capture_events=True,
+                             workspace=False)
+    assert db.d_ws is None
+    db.run("phi")
+    assert db.fetch()["phi"][0] == P.phi(profile, cluster)
+    for what in ("rdo", "prm", "sweep", "select", "spp"):
+        with pytest.raises(RuntimeError, match="ws is NULL"):
+            db.run(what)
