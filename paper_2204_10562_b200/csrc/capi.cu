@@ -37,7 +37,7 @@ __global__ void k_backtrack(pp_batch b);
 __global__ void k_query(pp_batch b, int n, const int* qi, const int* ql, const int* qx, const int* qr,
                         const int* qd, int max_xi, double* w, int* frag, int* feas);
 template <bool SMEM> __global__ void k_rdo(pp_batch b, int resume);
-__global__ void k_rdo_plan(pp_batch b, int round, int predict);
+template <int MAXS> __global__ void k_rdo_plan(pp_batch b, int round, int predict);
 __global__ void k_rdo_hash(pp_batch b, int dedup);
 __global__ void k_rdo_rep(pp_batch b);
 __global__ void k_rdo_copy(pp_batch b);
@@ -222,17 +222,20 @@ int pp_rdo(const pp_batch* b, void* stream) {
     const int in_smem = V <= RDO_SMEM_MAX;
     const int rounds = V >= 2 ? g_rdo_rounds.load() : 0;
     if (rounds > 0) {
-        const size_t plan_smem = sizeof(int) * (size_t)V * (3 + RDO_WARPS);
+        const size_t plan_smem = rdo_plan_smem(V);
         const size_t cut_smem = (in_smem ? sizeof(double) * V * V : 0) + sizeof(int) * V + V + 16;
         // a batch above RDO_SMEM_MAX may still hold instances below it: their cuts run
         // in the shared-memory variant (k_rdo_cut<false> has no scratch for them)
         const int vs = V < RDO_SMEM_MAX ? V : RDO_SMEM_MAX;
         const size_t cut_smem_s = sizeof(double) * vs * vs + sizeof(int) * vs + vs + 16;
-        cudaFuncSetAttribute(k_rdo_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan_smem);
+        // register slots of the largest group: the plan kernel instantiated for the batch's V
+        void (*plan)(pp_batch, int, int) = V <= 32 ? k_rdo_plan<1> : V <= 64 ? k_rdo_plan<2> :
+                                           V <= 128 ? k_rdo_plan<4> : V <= 256 ? k_rdo_plan<8> : k_rdo_plan<16>;
+        cudaFuncSetAttribute(plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan_smem);
         cudaFuncSetAttribute(k_rdo_cut<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cut_smem_s);
         const dim3 gc(b->n_inst, V - 1);
         for (int r = 0; r <= rounds; ++r) {
-            k_rdo_plan<<<b->n_inst, 32 * RDO_WARPS, plan_smem, S(stream)>>>(*b, r, r < rounds);
+            plan<<<b->n_inst, 32 * RDO_WARPS, plan_smem, S(stream)>>>(*b, r, r < rounds);
             PP_CHECK_LAUNCH("k_rdo_plan");
             if (r == rounds) break;
             k_rdo_cut<true><<<gc, 32, cut_smem_s, S(stream)>>>(*b);

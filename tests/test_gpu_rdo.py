@@ -68,6 +68,19 @@ def clusters():
     # two dense blocks joined weakly: balanced splits, so chain predictions miss
     ids = list(range(1, 41))
     out.append(("blocks", ids, clique(ids, lambda a, b: 100e9 if (a <= 17) == (b <= 17) else rng.uniform(1e9, 2e9))))
+    # tree prediction (rdo.cu): three tiers, uneven nodes, a block cut that ties a
+    # singleton peel exactly, maximum-bandwidth links forming a path
+    ids = list(range(1, 33))
+    out.append(("tier3", ids, clique(ids, lambda a, b: 450e9 if (a - 1) // 4 == (b - 1) // 4 else
+                                      (50e9 if (a - 1) // 16 == (b - 1) // 16 else 12.5e9))))
+    sizes = (2, 3, 5, 8, 1, 4)
+    node = [k for k, n in enumerate(sizes) for _ in range(n)]
+    ids = list(range(1, len(node) + 1))
+    out.append(("uneven-nodes", ids, clique(ids, lambda a, b: 300e9 if node[a - 1] == node[b - 1] else 10e9)))
+    ids = list(range(1, 7))   # pairs: a GPU's degree 40 + 4 x 10 equals a pair's cut 2 x 4 x 10
+    out.append(("tie-pairs", ids, clique(ids, lambda a, b: 40e9 if (a - 1) // 2 == (b - 1) // 2 else 10e9)))
+    ids = list(range(1, 13))
+    out.append(("max-path", ids, clique(ids, lambda a, b: 100e9 if abs(a - b) == 1 and a <= 8 and b <= 8 else 5e9)))
     # non-contiguous ids, shuffled per-node structure
     ids = [3 * k + 7 for k in range(30)]
     grp = {g: rng.randrange(4) for g in ids}

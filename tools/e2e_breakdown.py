@@ -1,10 +1,11 @@
-"""Host-side breakdown of one spp_many() call on the C3 batch (run on the GPU box)."""
+"""Host-side breakdown of one spp_many() call on the C3 batch, or the C4 batch
+with `c4` (run on the GPU box; `--profile` adds a cProfile of 5 calls)."""
 import sys, time
 sys.path.insert(0, ".")
 import torch
 from paper_2204_10562_b200 import planner, _device, workloads as W
 
-specs = W.c3_sweep()
+specs = W.c4_batch(4096) if "c4" in sys.argv else W.c3_sweep()
 models = W.models_of(specs)
 planner.spp_many(models)
 torch.cuda.synchronize()
