@@ -40,6 +40,7 @@ template <bool SMEM> __global__ void k_rdo(pp_batch b, int resume);
 template <int MAXS> __global__ void k_rdo_plan(pp_batch b, int round, int predict);
 __global__ void k_rdo_hash(pp_batch b, int dedup);
 __global__ void k_rdo_rep(pp_batch b);
+__global__ void k_rdo_insert(pp_batch b);
 __global__ void k_rdo_copy(pp_batch b);
 template <bool SMEM> __global__ void k_rdo_cut(pp_batch b);
 template <bool SMEM>
@@ -216,6 +217,8 @@ int pp_rdo(const pp_batch* b, void* stream) {
     k_rdo_hash<<<b->n_inst, 32, 0, S(stream)>>>(*b, dedup);
     PP_CHECK_LAUNCH("k_rdo_hash");
     if (dedup) {
+        k_rdo_insert<<<(b->n_inst + 127) / 128, 128, 0, S(stream)>>>(*b);
+        PP_CHECK_LAUNCH("k_rdo_insert");
         k_rdo_rep<<<b->n_inst, 32, 0, S(stream)>>>(*b);
         PP_CHECK_LAUNCH("k_rdo_rep");
     }

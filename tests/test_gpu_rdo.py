@@ -163,3 +163,29 @@ def test_batch_dedup_of_identical_clusters():
         _lib.rdo_dedup(prev)
     for s, r in zip(specs, res):
         assert r.device_order == oracle_order(s.gpu_ids, s.links), s.name
+
+
+def test_batch_dedup_hash_table_many_instances():
+    """Hundreds of instances drawn from a few clusters in shuffled order: the
+    open-addressing table (one slot per instance, k_rdo_insert) must map every
+    duplicate to a representative with the same matrix."""
+    import math
+    rng = random.Random(11)
+    base = W.c3_gpt96(M=8, L=6, nodes=2, per_node=4)
+    pool = []
+    for k in range(6):
+        rids = list(range(1, 9))
+        pool.append((rids, clique(rids, lambda x, y: math.exp(rng.uniform(20, 25)))))
+    pool.append(W.two_tier_cluster(2, 4))
+    specs = []
+    for k in range(400):
+        ids, links = pool[rng.randrange(len(pool))]
+        specs.append(W.InstanceSpec(f"i{k}", base.fwd, base.bwd, base.param, base.efwd, base.ebwd, ids, links, 8))
+    prev = _lib.rdo_dedup(2)
+    try:
+        res = spp_many([s.to_model() for s in specs])
+    finally:
+        _lib.rdo_dedup(prev)
+    want = {id(l): oracle_order(i, l) for i, l in pool}
+    for s, r in zip(specs, res):
+        assert r.device_order == want[id(s.links)], s.name
