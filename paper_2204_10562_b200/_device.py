@@ -76,6 +76,76 @@ def pack(profile, cluster) -> Packed:
     return Packed(ids, *pack_profile(profile), bw)
 
 
+def pack_clusters(clusters):
+    """pack_cluster for many clusters at once, or None unless EVERY cluster is in
+    the common valid form — each unordered pair once as an int key (a, b) with
+    a < b, both GPUs known, bandwidth in [1e-100, 1e100] (what validate_cluster
+    and check_cluster_range accept without a loop); callers then fall back to
+    the per-cluster path, which raises the reference's first error.  One pass
+    over all the bandwidth dicts, one sort and one searchsorted for the whole
+    batch instead of a dozen numpy calls per cluster."""
+    import itertools
+    chain = itertools.chain.from_iterable
+    n = len(clusters)
+    Vs, Es = [], []
+    for c in clusters:
+        V = len(c.gpu_ids)
+        if V == 0 or len(c.bandwidth) != V * (V - 1) // 2:
+            return None
+        Vs.append(V)
+        Es.append(len(c.bandwidth))
+    nv, ne = sum(Vs), sum(Es)
+    try:
+        ids_all = np.fromiter(chain(c.gpu_ids for c in clusters), dtype=np.int64, count=nv)
+        keys = np.fromiter(chain(chain(c.bandwidth.keys() for c in clusters)), dtype=np.int64,
+                           count=2 * ne).reshape(ne, 2)
+        vals = np.fromiter(chain(c.bandwidth.values() for c in clusters), dtype=np.float64, count=ne)
+    except (TypeError, ValueError, OverflowError):
+        return None
+    lim = 1 << 31
+    if ((ids_all < -lim) | (ids_all >= lim)).any() or ((keys < -lim) | (keys >= lim)).any():
+        return None
+    Varr = np.asarray(Vs, dtype=np.int64)
+    cv = np.repeat(np.arange(n, dtype=np.int64), Varr)
+    ce = np.repeat(np.arange(n, dtype=np.int64), np.asarray(Es, dtype=np.int64))
+    comb = np.sort((cv << 32) | (ids_all + lim))   # (cluster, id) sorted: each cluster's ids ascending
+    if (np.diff(comb) == 0).any():
+        return None
+    a, b = keys[:, 0], keys[:, 1]
+    if not (a < b).all() or not ((vals >= 1e-100) & (vals <= 1e100)).all():
+        return None
+    voff = np.concatenate(([0], np.cumsum(Varr)))
+    sid_np = (comb & 0xffffffff) - lim
+    # id -> position in its cluster's sorted ids: a dense table over each cluster's id
+    # span when the spans are compact (the usual 0..V-1 / 1..V numbering), else a search
+    lo_c, hi_c = sid_np[voff[:-1]], sid_np[voff[1:] - 1]
+    span = hi_c - lo_c + 1
+    if int(span.sum()) <= 8 * nv + 1024:
+        soff = np.concatenate(([0], np.cumsum(span)))
+        tab = np.full(int(soff[-1]), -1, dtype=np.int64)
+        tab[np.repeat(soff[:-1] - lo_c, Varr) + sid_np] = np.arange(nv) - np.repeat(voff[:-1], Varr)
+        lo_e, hi_e, so_e = lo_c[ce], hi_c[ce], soff[:-1][ce] - lo_c[ce]
+        if ((a < lo_e) | (b > hi_e)).any():
+            return None
+        pa, pb = tab[so_e + a], tab[so_e + b]
+        if ((pa < 0) | (pb < 0)).any():
+            return None
+    else:
+        ka, kb = (ce << 32) | (a + lim), (ce << 32) | (b + lim)
+        ia, ib = np.searchsorted(comb, ka), np.searchsorted(comb, kb)
+        if ((ia >= nv) | (ib >= nv)).any() or not ((comb[np.minimum(ia, nv - 1)] == ka) &
+                                                  (comb[np.minimum(ib, nv - 1)] == kb)).all():
+            return None
+        pa, pb = ia - voff[ce], ib - voff[ce]
+    moff = np.concatenate(([0], np.cumsum(Varr * Varr)))
+    Ve, mo = Varr[ce], moff[:-1][ce]
+    flat = np.zeros(int(moff[-1]))
+    flat[mo + pa * Ve + pb] = vals
+    flat[mo + pb * Ve + pa] = vals
+    sid = sid_np.tolist()
+    return [(tuple(sid[voff[k]:voff[k + 1]]), flat[moff[k]:moff[k + 1]].reshape(Vs[k], Vs[k])) for k in range(n)]
+
+
 def bandwidth_arrays(cluster):
     """(keys [n, 2] int64, values [n] float64) of cluster.bandwidth, in dict order."""
     import itertools
@@ -134,6 +204,10 @@ def device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_INST_DTYPE = np.dtype([(name, np.int32 if t is C.c_int32 else np.int64) for name, t in PPInstance._fields_])
+assert _INST_DTYPE.itemsize == C.sizeof(PPInstance)
+
+
 class DeviceBatch:
     """A batch of planning instances resident on the GPU with all outputs.
 
@@ -153,6 +227,7 @@ class DeviceBatch:
         Ls = np.array([p.L for p, _, _, _ in items], dtype=np.int32)
         Vs = np.array([p.V for p, _, _, _ in items], dtype=np.int32)
         Ms = np.array([m for _, m, _, _ in items], dtype=np.int32)
+        self.Ms = Ms.astype(np.int64)
         fl = np.array([f for _, _, f, _ in items], dtype=np.int32)
         inst = (PPInstance * n)()
         tot = [C.c_int64() for _ in range(8)]
@@ -220,6 +295,14 @@ class DeviceBatch:
         self.batch = b
         self.lib = lib
 
+    def inst_offsets(self):
+        """Per-instance V and output offsets (order, sweep, stage, ar, ev) as int64 arrays."""
+        if getattr(self, "_offs", None) is None:
+            a = np.frombuffer(bytes(self.inst_host), dtype=_INST_DTYPE)
+            self._offs = {"V": a["V"].astype(np.int64), "order": a["order_off"], "sweep": a["sweep_off"],
+                          "stage": a["stage_off"], "ar": a["ar_off"], "ev": a["ev_off"]}
+        return self._offs
+
     # -- launches -------------------------------------------------------------
     def run(self, what="spp"):
         fn = {"spp": self.lib.pp_spp, "rdo": self.lib.pp_rdo, "prm": self.lib.pp_prm,
@@ -248,23 +331,23 @@ class DeviceBatch:
         f.update(g)
         f["order"] = order
         if self.capture_events:
-            bx = g["best_xi"]
+            bx = g["best_xi"].astype(np.int64)
             ev_s = self.d_fout[fe:int(self.f_off[9])]
             ev_e = self.d_fout[int(self.f_off[9]):int(self.f_off[10])]
             ev_o = self.d_iout[ie:int(self.i_off[7])]
-            parts_s, parts_e, parts_o, coff, c = [], [], [], np.zeros(self.n, np.int64), 0
-            for k in range(self.n):
-                x = int(bx[k])
-                cnt = self.items[k][1] * (4 * x - 3) if x > 0 else 0
-                coff[k] = c
-                if cnt:
-                    o = self.inst_host[k].ev_off
-                    parts_s.append(ev_s[o:o + cnt]); parts_e.append(ev_e[o:o + cnt]); parts_o.append(ev_o[o:o + cnt])
-                    c += cnt
+            # used prefix of instance k: M_k (4 xi_k - 3) events from its ev_off, gathered
+            # on the device with one index (built there from n offsets / counts)
+            cnt = np.where(bx > 0, self.Ms * (4 * bx - 3), 0)
+            coff = np.concatenate(([0], np.cumsum(cnt)[:-1])).astype(np.int64)
+            c = int(cnt.sum())
             self._d2h_events = c
             if c:
-                dev_f = torch.cat(parts_s + parts_e)
-                dev_i = torch.cat(parts_o)
+                dev = self.d_fout.device
+                shift = torch.from_numpy(self.inst_offsets()["ev"] - coff).to(dev)
+                idx = torch.repeat_interleave(shift, torch.from_numpy(cnt).to(dev), output_size=c)
+                idx += torch.arange(c, device=dev)
+                dev_f = torch.cat((ev_s.index_select(0, idx), ev_e.index_select(0, idx)))
+                dev_i = ev_o.index_select(0, idx)
                 hf = torch.empty(dev_f.shape, dtype=dev_f.dtype, pin_memory=True)
                 hi = torch.empty(dev_i.shape, dtype=dev_i.dtype, pin_memory=True)
                 hf.copy_(dev_f, non_blocking=True)

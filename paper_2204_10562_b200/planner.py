@@ -7,6 +7,7 @@ capture.  spp_many() runs that pipeline for a whole batch of instances in
 one launch sequence (every kernel's grid carries the instance dimension).
 """
 
+import gc
 import math
 from collections import abc
 import sys
@@ -16,10 +17,11 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _device, _lib
-from .model import (ClusterGraph, ModelProfile, Plan, Schedule, Stage, check_cluster_range, check_numeric_range,
-                    check_profile_range, validate_cluster, validate_profile)
+from .model import (AllReduceWindow, ClusterGraph, LazyEvents, ModelProfile, Plan, Schedule, Stage,
+                    check_cluster_range, check_numeric_range, check_profile_range, validate_cluster,
+                    validate_profile)
 from .partition import sum_flags
-from .scheduler import _build_schedule
+from .scheduler import _labels
 
 
 @dataclass(frozen=True)
@@ -81,9 +83,25 @@ def _items(instances):
     cluster OBJECT (e.g. one cluster planned for several models or M values)
     is validated and packed once; profiles (immutable) are also remembered
     across calls, clusters (mutable bandwidth dict) are not."""
+    gc_on = gc.isenabled()
+    gc.disable()   # no reference cycles below; skip the cyclic collector's rescans
+    try:
+        return _items_loop(instances)
+    finally:
+        if gc_on:
+            gc.enable()
+
+
+def _items_loop(instances):
     items, packs = [], []
     seen_p, seen_c, seen_pc = {}, {}, {}
     flags = _lib.PP_ALLOW_REPLICATION | sum_flags()
+    # all distinct clusters validated and packed in one vectorised pass when every
+    # one of them is in the common valid form (else the per-instance path below)
+    cl = list({id(c): c for _, c, _ in instances}.values())
+    fast = _device.pack_clusters(cl) if len(cl) > 1 else None
+    if fast is not None:
+        seen_c = {id(c): (c, f) for c, f in zip(cl, fast)}
     for profile, cluster, M in instances:
         # same check order as validate_profile, validate_cluster, check_numeric_range
         pp, cc = seen_p.get(id(profile)), seen_c.get(id(cluster))
@@ -173,34 +191,74 @@ def _frozen(cls, **fields):
 
 
 def _decode(db: _device.DeviceBatch, h, k: int, M: int, packed) -> SppResult:
-    I = db.inst_host[k]
-    V = I.V
-    ids = packed.ids
-    order = tuple(ids[x] for x in h["order"][I.order_off:I.order_off + V].tolist())
-    so = I.sweep_off
-    rs = h["sweep_r"][so:so + V].tolist()
-    ws = h["sweep_w"][so:so + V].tolist()
-    mks = h["sweep_mk"][so:so + V].tolist()
-    bds = h["sweep_bound"][so:so + V].tolist()
-    sweep = LazySweep(rs, ws, mks, bds)
-    xi = int(h["best_xi"][k])
-    base = I.stage_off + xi * (xi - 1) // 2
-    ls, le = h["ls"][base:base + xi].tolist(), h["le"][base:base + xi].tolist()
-    dlo, dhi = h["dlo"][base:base + xi].tolist(), h["dhi"][base:base + xi].tolist()
-    stages = tuple(Stage(index=n + 1, layer_start=ls[n], layer_end=le[n], devices=order[dlo[n] - 1:dhi[n]])
-                   for n in range(xi))
-    plan = Plan(stages=stages, microbatch_count=M)
-    J = 4 * xi - 3
-    mk = float(h["best_mk"][k])
-    eo = int(h["ev_coff"][k])   # compact events of the chosen plans (_device.DeviceBatch.fetch)
-    rec = dict(makespan=mk,
-               ev_start=h["ev_start"][eo:eo + M * J], ev_end=h["ev_end"][eo:eo + M * J],
-               ev_order=h["ev_order"][eo:eo + M * J],
-               ar_start=h["ar_start"][I.ar_off:I.ar_off + xi], ar_end=h["ar_end"][I.ar_off:I.ar_off + xi])
-    schedule = _build_schedule(plan, rec)
-    p = float(h["phi"][k])
-    return _frozen(SppResult, plan=plan, schedule=schedule, makespan=mk, sweep=sweep,
-                   device_order=order, theorem_factor=bound_factor(V, M) * (1.0 + p), phi=p)
+    """One instance's SppResult (see _decode_all)."""
+    return _decode_all(db, h, [M if q == k else 0 for q in range(db.n)], [packed if q == k else None
+                                                                        for q in range(db.n)], only=k)[0]
+
+
+def _decode_all(db: _device.DeviceBatch, h, Ms, packs, only=None) -> List[SppResult]:
+    """SppResult objects of a fetched batch.  Everything array-shaped is sliced
+    once per batch (the chosen plans' stage rows gathered with one fancy index,
+    whole columns converted to Python lists once), then each instance builds
+    its frozen result objects without per-field validation."""
+    n = db.n
+    ks = range(n) if only is None else (only,)
+    offs = db.inst_offsets()
+    V = offs["V"]
+    bx = h["best_xi"].tolist()
+    bmk = h["best_mk"].tolist()
+    phis = h["phi"].tolist()
+    order_all = h["order"].tolist()
+    sr, sw = h["sweep_r"].tolist(), h["sweep_w"].tolist()
+    smk, sbd = h["sweep_mk"].tolist(), h["sweep_bound"].tolist()
+    # the chosen plans' stage rows and allreduce windows, gathered in one pass
+    xs = np.maximum(np.asarray(bx, dtype=np.int64), 0)
+    cum = np.concatenate(([0], np.cumsum(xs)))
+    rel = np.arange(int(cum[-1]), dtype=np.int64) - np.repeat(cum[:-1], xs)
+    base = np.repeat(offs["stage"] + xs * (xs - 1) // 2, xs) + rel
+    ls, le = h["ls"][base].tolist(), h["le"][base].tolist()
+    dlo, dhi = h["dlo"][base].tolist(), h["dhi"][base].tolist()
+    arb = np.repeat(offs["ar"], xs) + rel
+    ars, are = h["ar_start"][arb].tolist(), h["ar_end"][arb].tolist()
+    coff = h["ev_coff"]
+    ev_s, ev_e, ev_o = h["ev_start"], h["ev_end"], h["ev_order"]
+    # the objects built below hold no reference cycles: keep the cyclic collector from
+    # rescanning every live object each few hundred allocations (C4: 57 k objects per call)
+    gc_on = gc.isenabled()
+    gc.disable()
+    try:
+        return _decode_loop(ks, V, Ms, packs, offs, order_all, sr, sw, smk, sbd, bx, cum, ls, le, dlo, dhi, ars, are,
+                            bmk, coff, ev_s, ev_e, ev_o, phis)
+    finally:
+        if gc_on:
+            gc.enable()
+
+
+def _decode_loop(ks, V, Ms, packs, offs, order_all, sr, sw, smk, sbd, bx, cum, ls, le, dlo, dhi, ars, are, bmk,
+                 coff, ev_s, ev_e, ev_o, phis):
+    out = []
+    for k in ks:
+        Vk, M, packed = int(V[k]), Ms[k], packs[k]
+        ids = packed.ids
+        oo, so = int(offs["order"][k]), int(offs["sweep"][k])
+        order = tuple([ids[x] for x in order_all[oo:oo + Vk]])
+        sweep = LazySweep(sr[so:so + Vk], sw[so:so + Vk], smk[so:so + Vk], sbd[so:so + Vk])
+        xi, c0 = bx[k], int(cum[k])
+        stages = tuple([_frozen(Stage, index=q + 1, layer_start=ls[c0 + q], layer_end=le[c0 + q],
+                                devices=order[dlo[c0 + q] - 1:dhi[c0 + q]]) for q in range(xi)])
+        plan = _frozen(Plan, stages=stages, microbatch_count=M)
+        mk = bmk[k]
+        cnt = M * (4 * xi - 3)
+        eo = int(coff[k])
+        res, lab, _ = _labels(xi)
+        events = LazyEvents.from_order(res, lab, 4 * xi - 3, ev_o[eo:eo + cnt], ev_s[eo:eo + cnt], ev_e[eo:eo + cnt])
+        windows = tuple([_frozen(AllReduceWindow, stage=q + 1, start=ars[c0 + q], end=are[c0 + q])
+                         for q in range(xi) if dhi[c0 + q] > dlo[c0 + q]])
+        schedule = _frozen(Schedule, events=events, allreduce=windows, makespan=mk)
+        p = phis[k]
+        out.append(_frozen(SppResult, plan=plan, schedule=schedule, makespan=mk, sweep=sweep,
+                           device_order=order, theorem_factor=bound_factor(Vk, M) * (1.0 + p), phi=p))
+    return out
 
 
 def spp_many(instances: Sequence[Tuple[ModelProfile, ClusterGraph, int]]) -> List[SppResult]:
@@ -209,7 +267,7 @@ def spp_many(instances: Sequence[Tuple[ModelProfile, ClusterGraph, int]]) -> Lis
     db = _device.DeviceBatch(items, capture_events=True)
     db.run("spp")
     h = db.fetch()
-    return [_decode(db, h, k, items[k][1], packs[k]) for k in range(len(items))]
+    return _decode_all(db, h, [it[1] for it in items], packs)
 
 
 def spp(profile: ModelProfile, cluster: ClusterGraph, microbatch_count: int) -> SppResult:

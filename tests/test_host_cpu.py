@@ -132,6 +132,37 @@ def test_cluster_validation_fast_and_slow_paths_agree():
             P.validate_cluster(clu)
 
 
+def test_batched_cluster_packing_matches_per_cluster_and_defers_errors():
+    """_device.pack_clusters (spp_many's one-pass validation + packing of all
+    distinct clusters) gives the per-cluster pack_cluster results, and returns
+    None — so the per-instance path raises the reference's first error — when
+    any cluster is outside the common valid form."""
+    import random
+    from paper_2204_10562_b200 import _device, planner
+    rng = random.Random(5)
+    cls = [c for _, c, _ in W.models_of(W.c4_batch(40))]
+    for k in range(20):   # sparse / negative ids take the searchsorted branch
+        ids = rng.sample(range(-10 ** 7, 10 ** 7), rng.randrange(2, 12))
+        cls.append(P.ClusterGraph(tuple(ids), {(a, b) if a < b else (b, a): rng.uniform(1e9, 1e11)
+                                               for i, a in enumerate(ids) for b in ids[i + 1:]}))
+    cls.append(P.make_cluster([7], []))
+    fast = _device.pack_clusters(cls)
+    for (fi, fb), c in zip(fast, cls):
+        si, sb = _device.pack_cluster(c)
+        assert fi == si and np.array_equal(fb, sb)
+    bad = [P.ClusterGraph((1, 2), {(2, 1): 1.0}),          # reversed key: slow path (legal)
+           P.ClusterGraph((1, 2), {(1, 2): 0.0}),          # non-positive
+           P.ClusterGraph((1, 2), {(1, 5): 1.0}),          # unknown GPU
+           P.ClusterGraph((1, 2), {(1, 2): 1e101}),        # outside the numeric domain
+           P.ClusterGraph((1, 2, 3), {(1, 2): 1.0, (1, 3): 1.0})]   # missing pair
+    for b in bad:
+        assert _device.pack_clusters(cls[:3] + [b]) is None
+    # spp_many's packing: a bad cluster in the middle raises the per-instance error
+    prof, _, M = W.c4_batch(1)[0].to_model()
+    with pytest.raises(P.ValidationError, match="non-positive"):
+        planner._items([(prof, cls[0], M), (prof, bad[1], M), (prof, cls[1], M)])
+
+
 def test_lazy_events_behave_like_tuples():
     from paper_2204_10562_b200.model import LazyEvents, ScheduleEvent
     res = [None, "stage1", "chan1", "stage2"]

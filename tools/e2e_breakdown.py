@@ -19,7 +19,7 @@ for _ in range(3):
     t3 = time.perf_counter()
     h = db.fetch()
     t4 = time.perf_counter()
-    res = [planner._decode(db, h, k, items[k][1], packs[k]) for k in range(len(items))]
+    res = planner._decode_all(db, h, [it[1] for it in items], packs)
     t5 = time.perf_counter()
     print(f"validate+pack {1e3*(t1-t0):.1f} ms | DeviceBatch (H2D+alloc) {1e3*(t2-t1):.1f} | enqueue {1e3*(t3-t2):.1f} "
           f"| fetch (sync+D2H) {1e3*(t4-t3):.1f} | decode {1e3*(t5-t4):.1f} | total {1e3*(t5-t0):.1f}")
