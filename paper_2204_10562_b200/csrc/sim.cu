@@ -216,13 +216,42 @@ __device__ void pe_simulate(const P& p, const InstView& I, int N, int M, int nth
     }
 }
 
+// One resource's pass of the PE recurrence, branch-free: the B / FB / Y block
+// (p1) then the F / X block (p2) of this pass, each applied only while its
+// microbatch index is in 1..M (inactive blocks are computed and discarded by a
+// select, so the S resources of a lane are straight-line code the compiler
+// interleaves — with per-resource branches their chains ran one after another:
+// C3 n = 12 sweep ~590 cycles per pass for S = 4).  p1 / p2 far out of range
+// disable a block (no F / X block on FB_N; resources past R).  Same fp64
+// operations in the same order as pe_simulate when a block is active.
+template <bool EV>
+__device__ __forceinline__ void pe_pass_slot(int pass, int M, int J, int p1, int p2, bool from_left, double left,
+                                             double right, double dA, double dB, double& rf, double& fn, double& bn,
+                                             double* ev_s, double* ev_e) {
+    const int m1 = pass - p1, m2 = pass - p2;   // microbatch - 1 of each block
+    const bool a1 = (unsigned)m1 < (unsigned)M, a2 = (unsigned)m2 < (unsigned)M;
+    const double st1 = dmax(rf, from_left ? left : right);
+    const double en1 = st1 + dB;                 // B / FB / Y
+    const double r1 = a1 ? en1 : rf;
+    bn = a1 ? en1 : bn;
+    const double st2 = dmax(r1, left);
+    const double en2 = st2 + dA;                 // F / X
+    rf = a2 ? en2 : r1;
+    fn = a2 ? en2 : fn;
+    if (EV) {
+        if (a1) { const int64_t x = (int64_t)m1 * J + p1 - 1; ev_s[x] = st1; ev_e[x] = en1; }
+        if (a2) { const int64_t x = (int64_t)m2 * J + p2 - 1; ev_s[x] = st2; ev_e[x] = en2; }
+    }
+}
+constexpr int PE_OFF = -(1 << 29);   // p1 / p2 of a block that never runs
+
 // ---- PE sweep, one WARP per plan (R = 2N-1 <= 32 S resources) ---------------
 // Lane L holds resources q = L*S + s (contiguous blocks): a predecessor on the
 // neighbouring resource is in the same lane's registers or one shuffle away, so
 // a pass is register work plus two shuffles instead of a shared-memory round
 // trip and a CTA barrier.  Same recurrence, same fp64 operations in the same
 // order per resource as pe_simulate (bit-identical).
-template <int S, class P>
+template <int S, bool EV, class P>
 __device__ void pe_simulate_warp(const P& p, const InstView& I, int N, int M, double* o_mk, double* o_bound,
                                  double* ev_s, double* ev_e, double* ar_s, double* ar_e) {
     const unsigned FULL = 0xffffffffu;
@@ -245,8 +274,9 @@ __device__ void pe_simulate_warp(const P& p, const InstView& I, int N, int M, do
         const int n = q / 2 + 1;
         if (st) {
             if (n < N) { p1[s] = 4 * N - 1 - 2 * n; p2[s] = 2 * n - 1; }   // B_n, F_n
-            else { p1[s] = 2 * N - 1; p2[s] = 0; }                       // FB_N
+            else { p1[s] = 2 * N - 1; p2[s] = PE_OFF; }                  // FB_N (no F / X block)
         } else { p1[s] = 4 * N - 2 - 2 * n; p2[s] = 2 * n; }              // Y_n, X_n
+        if (!act[s]) { p1[s] = PE_OFF; p2[s] = PE_OFF; }
         from_left[s] = st && n == N;
         fe[s] = 0.0; be[s] = 0.0; rf[s] = 0.0;
     }
@@ -265,28 +295,11 @@ __device__ void pe_simulate_warp(const P& p, const InstView& I, int N, int M, do
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             fn[s] = fe[s]; bn[s] = be[s];
-            if (!act[s]) continue;
             const int q = lane * S + s;
             const double left = q == 0 ? 0.0 : (s > 0 ? fe[s - 1] : fe_in);
             const double right = q + 1 >= R ? 0.0 : (s + 1 < S ? be[s + 1] : be_in);
-            int m = pass - p1[s] + 1;
-            if ((unsigned)(m - 1) < (unsigned)M) {   // 1 <= m <= M
-                const double st = dmax(rf[s], from_left[s] ? left : right);
-                const double en = st + dB[s];   // B / FB / Y
-                rf[s] = en;
-                bn[s] = en;
-                if (ev_s) { const int64_t x = (int64_t)(m - 1) * J + p1[s] - 1; ev_s[x] = st; ev_e[x] = en; }
-            }
-            if (p2[s]) {
-                m = pass - p2[s] + 1;
-                if ((unsigned)(m - 1) < (unsigned)M) {
-                    const double st = dmax(rf[s], left);
-                    const double en = st + dA[s];   // F / X
-                    rf[s] = en;
-                    fn[s] = en;
-                    if (ev_s) { const int64_t x = (int64_t)(m - 1) * J + p2[s] - 1; ev_s[x] = st; ev_e[x] = en; }
-                }
-            }
+            pe_pass_slot<EV>(pass, M, J, p1[s], p2[s], from_left[s], left, right, dA[s], dB[s], rf[s], fn[s], bn[s],
+                             ev_s, ev_e);
         }
 #pragma unroll
         for (int s = 0; s < S; ++s) { fe[s] = fn[s]; be[s] = bn[s]; }
@@ -317,7 +330,7 @@ __device__ void pe_simulate_warp(const P& p, const InstView& I, int N, int M, do
 // xi = 256 plan: 1532 passes at ~1.4 k cycles each before).  Same recurrence,
 // same fp64 operations in the same order per resource (bit-identical).
 // smem: xch[2][2][nw] (fe, be boundary values per pass parity) + red[2 nw]
-template <int S, class P>
+template <int S, bool EV, class P>
 __device__ void pe_simulate_mw(const P& p, const InstView& I, int N, int M, int nw, double* sm, double* o_mk,
                                double* o_bound, double* ev_s, double* ev_e, double* ar_s, double* ar_e) {
     const unsigned FULL = 0xffffffffu;
@@ -345,8 +358,9 @@ __device__ void pe_simulate_mw(const P& p, const InstView& I, int N, int M, int 
         const int n = q / 2 + 1;
         if (st) {
             if (n < N) { p1[s] = 4 * N - 1 - 2 * n; p2[s] = 2 * n - 1; }   // B_n, F_n
-            else { p1[s] = 2 * N - 1; p2[s] = 0; }                       // FB_N
+            else { p1[s] = 2 * N - 1; p2[s] = PE_OFF; }                  // FB_N (no F / X block)
         } else { p1[s] = 4 * N - 2 - 2 * n; p2[s] = 2 * n; }              // Y_n, X_n
+        if (!act[s]) { p1[s] = PE_OFF; p2[s] = PE_OFF; }
         from_left[s] = st && n == N;
         fe[s] = 0.0; be[s] = 0.0; rf[s] = 0.0;
     }
@@ -373,28 +387,11 @@ __device__ void pe_simulate_mw(const P& p, const InstView& I, int N, int M, int 
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             fn[s] = fe[s]; bn[s] = be[s];
-            if (!act[s]) continue;
             const int q = q0 + s;
             const double left = q == 0 ? 0.0 : (s > 0 ? fe[s - 1] : fe_in);
             const double right = q + 1 >= R ? 0.0 : (s + 1 < S ? be[s + 1] : be_in);
-            int m = pass - p1[s] + 1;
-            if ((unsigned)(m - 1) < (unsigned)M) {   // 1 <= m <= M
-                const double st = dmax(rf[s], from_left[s] ? left : right);
-                const double en = st + dB[s];   // B / FB / Y
-                rf[s] = en;
-                bn[s] = en;
-                if (ev_s) { const int64_t x = (int64_t)(m - 1) * J + p1[s] - 1; ev_s[x] = st; ev_e[x] = en; }
-            }
-            if (p2[s]) {
-                m = pass - p2[s] + 1;
-                if ((unsigned)(m - 1) < (unsigned)M) {
-                    const double st = dmax(rf[s], left);
-                    const double en = st + dA[s];   // F / X
-                    rf[s] = en;
-                    fn[s] = en;
-                    if (ev_s) { const int64_t x = (int64_t)(m - 1) * J + p2[s] - 1; ev_s[x] = st; ev_e[x] = en; }
-                }
-            }
+            pe_pass_slot<EV>(pass, M, J, p1[s], p2[s], from_left[s], left, right, dA[s], dB[s], rf[s], fn[s], bn[s],
+                             ev_s, ev_e);
         }
 #pragma unroll
         for (int s = 0; s < S; ++s) { fe[s] = fn[s]; be[s] = bn[s]; }
@@ -434,10 +431,17 @@ template <class P>
 __device__ void pe_simulate_warp_any(const P& p, const InstView& I, int N, int M, double* o_mk, double* o_bound,
                                      double* ev_s, double* ev_e, double* ar_s, double* ar_e) {
     const int R = 2 * N - 1;
-    if (R <= 32) pe_simulate_warp<1>(p, I, N, M, o_mk, o_bound, ev_s, ev_e, ar_s, ar_e);
-    else if (R <= 64) pe_simulate_warp<2>(p, I, N, M, o_mk, o_bound, ev_s, ev_e, ar_s, ar_e);
-    else if (R <= 96) pe_simulate_warp<3>(p, I, N, M, o_mk, o_bound, ev_s, ev_e, ar_s, ar_e);
-    else pe_simulate_warp<4>(p, I, N, M, o_mk, o_bound, ev_s, ev_e, ar_s, ar_e);
+    if (ev_s) {
+        if (R <= 32) pe_simulate_warp<1, true>(p, I, N, M, o_mk, o_bound, ev_s, ev_e, ar_s, ar_e);
+        else if (R <= 64) pe_simulate_warp<2, true>(p, I, N, M, o_mk, o_bound, ev_s, ev_e, ar_s, ar_e);
+        else if (R <= 96) pe_simulate_warp<3, true>(p, I, N, M, o_mk, o_bound, ev_s, ev_e, ar_s, ar_e);
+        else pe_simulate_warp<4, true>(p, I, N, M, o_mk, o_bound, ev_s, ev_e, ar_s, ar_e);
+    } else {
+        if (R <= 32) pe_simulate_warp<1, false>(p, I, N, M, o_mk, o_bound, ev_s, ev_e, ar_s, ar_e);
+        else if (R <= 64) pe_simulate_warp<2, false>(p, I, N, M, o_mk, o_bound, ev_s, ev_e, ar_s, ar_e);
+        else if (R <= 96) pe_simulate_warp<3, false>(p, I, N, M, o_mk, o_bound, ev_s, ev_e, ar_s, ar_e);
+        else pe_simulate_warp<4, false>(p, I, N, M, o_mk, o_bound, ev_s, ev_e, ar_s, ar_e);
+    }
 }
 
 // k_pe_sweep / k_replay with one warp per plan (every N of the batch <= PE_WARP_MAXN)
@@ -607,7 +611,7 @@ __global__ void __launch_bounds__(1024) k_pe_sweep(pp_batch b) {
     const int64_t st = I.stage_off + (int64_t)xi * (xi - 1) / 2;
     SppPlanView p{b.stage_ls + st, b.stage_le + st, b.stage_dlo + st, b.stage_dhi + st, b.order + I.order_off};
     InstView iv(b, I);
-    pe_simulate_mw<PE_MW_S>(p, iv, xi, I.M, nw, smem_d, b.sweep_mk + so, b.sweep_bound + so, nullptr, nullptr,
+    pe_simulate_mw<PE_MW_S, false>(p, iv, xi, I.M, nw, smem_d, b.sweep_mk + so, b.sweep_bound + so, nullptr, nullptr,
                             nullptr, nullptr);
 }
 
@@ -644,7 +648,7 @@ __global__ void __launch_bounds__(1024) k_replay(pp_batch b) {
     const int64_t st = I.stage_off + (int64_t)xi * (xi - 1) / 2;
     SppPlanView p{b.stage_ls + st, b.stage_le + st, b.stage_dlo + st, b.stage_dhi + st, b.order + I.order_off};
     InstView iv(b, I);
-    pe_simulate_mw<PE_MW_S>(p, iv, xi, I.M, nw, smem_d, &s_mk, &s_bd, b.ev_start + I.ev_off, b.ev_end + I.ev_off,
+    pe_simulate_mw<PE_MW_S, true>(p, iv, xi, I.M, nw, smem_d, &s_mk, &s_bd, b.ev_start + I.ev_off, b.ev_end + I.ev_off,
                             b.ar_start + I.ar_off, b.ar_end + I.ar_off);
 }
 
