@@ -324,12 +324,16 @@ __device__ __forceinline__ void stab_fill(const pp_batch& b, const pp_instance& 
     const double den = (double)r * ws[lay.minpair + (int64_t)(i - r) * V + (i - 1)];
     const uint64_t pol = l2_evict_last_policy();   // re-read by the combine of every step
     const double num = 2.0 * (double)(r - 1);
+    // both divisors are fixed for the triangle: reciprocals hoisted (div_fixed, '/' bits)
+    const double dr = (double)r, yr = div_recip(dr);
+    const bool den_ok = div_fixed_ok(den);
+    const double yd = den_ok ? div_recip(den) : 0.0;
     for (int lp = 1 + warp; lp < L; lp += nw) {
         const int off = (lp - 1) * L - (lp - 1) * lp / 2;
         const double pl = prefix[lp];
         for (int l = lp + 1 + lane; l <= L; l += 32) {
-            double sv = (double)M * (prefix[l] - pl) / (double)r;
-            if (r > 1) sv += num * psum[(int64_t)lp * L + (l - 1)] / den;
+            double sv = div_fixed((double)M * (prefix[l] - pl), dr, yr, true);
+            if (r > 1) sv += div_fixed(num * psum[(int64_t)lp * L + (l - 1)], den, yd, den_ok);
             st_evict_last(out + off + (l - lp - 1), sv, pol);
         }
     }
@@ -508,6 +512,12 @@ __device__ __forceinline__ void mbar_wait0(uint64_t* bar) {   // phase 0 (single
         asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}\n"
                      : "=r"(ok) : "r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity) {   // reused barrier
+    unsigned ok = 0;
+    while (!ok)
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(double* dst, const double* src, unsigned bytes, uint64_t* bar, uint64_t pol) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n"
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
@@ -565,6 +575,8 @@ __global__ void __launch_bounds__(EX_T) k_expand(pp_batch b, int j, int planes_r
         const double den = (double)r * ws[lay.minpair + (int64_t)(i - r) * V + (i - 1)];
     const uint64_t pol = l2_evict_last_policy();   // re-read by the combine of every step
         const double num = 2.0 * (double)(r - 1);
+        const bool den_ok = div_fixed_ok(den);
+        const double yd = den_ok ? div_recip(den) : 0.0;   // fixed divisor: '/' bits via div_fixed
         double* S = ws + lay.S + stage_idx(L, r, 0, 1);
 #pragma unroll 4
         for (int e = t; e < L * L; e += EX_T) {
@@ -572,7 +584,7 @@ __global__ void __launch_bounds__(EX_T) k_expand(pp_batch b, int j, int planes_r
             double s = PP_INF;
             if (lp >= 1 && l > lp) {
                 s = T1[stage_idx(L, r, lp, l)];
-                if (r > 1) s += num * psum[(int64_t)lp * L + (l - 1)] / den;
+                if (r > 1) s += div_fixed(num * psum[(int64_t)lp * L + (l - 1)], den, yd, den_ok);
             }
             S[e] = s;
         }
@@ -1476,6 +1488,7 @@ __device__ __forceinline__ int warp_first(bool match) {
     return mask ? __ffs(mask) - 1 : -1;
 }
 
+constexpr int WALK_U = 4;
 __device__ void dp_walk(const pp_batch& b, const pp_instance& I, int l, int x, int r, int i, double w,
                         int* o_ls, int* o_le, int* o_dlo, int* o_dhi) {
     const int L = I.L, V = I.V, M = I.M;
@@ -1502,36 +1515,56 @@ __device__ void dp_walk(const pp_batch& b, const pp_instance& I, int l, int x, i
         // its triangles in shared memory): the scalar stage_term, same expression
         const int slot = tables ? sidx[(r - 1) * V + (i - 1)] : -1;
         const double* St = slot >= 0 ? ws + lay.Stab + (int64_t)slot * tri : nullptr;
+        // the candidates of a stage are scanned WALK_U x 32 at a time with all their
+        // loads in flight (one memory round trip per chunk instead of per 32)
         int lp = -1;
-        for (int base = x - 1; base <= l - 1 && lp < 0; base += 32) {
-            const int c = base + lane;
-            bool match = false;
-            if (c <= l - 1) {
-                const double stc = St ? St[(c - 1) * L - (c - 1) * c / 2 + (l - c - 1)]
-                                      : stage_term(M, L, V, prefix, psum, minpair, c, l, r, i);
-                match = dmax(X[(int64_t)(c - 1) * j + (x - 2)], stc) == w;
+        for (int base = x - 1; base <= l - 1 && lp < 0; base += 32 * WALK_U) {
+            bool match[WALK_U];
+#pragma unroll
+            for (int u = 0; u < WALK_U; ++u) {
+                const int c = base + 32 * u + lane;
+                match[u] = false;
+                if (c <= l - 1) {
+                    const double stc = St ? St[(c - 1) * L - (c - 1) * c / 2 + (l - c - 1)]
+                                          : stage_term(M, L, V, prefix, psum, minpair, c, l, r, i);
+                    match[u] = dmax(X[(int64_t)(c - 1) * j + (x - 2)], stc) == w;
+                }
             }
-            const int f = warp_first(match);
-            if (f >= 0) lp = base + f;
+#pragma unroll
+            for (int u = 0; u < WALK_U; ++u) {
+                const int f = warp_first(match[u]);
+                if (lp < 0 && f >= 0) lp = base + 32 * u + f;
+            }
         }
         int rp = -1;
+        double w_next = PP_INF;   // W(lp, x-1, rp, j): the next stage's target, from the winning lane
         if (lp > 0) {
             const double st = St ? St[(lp - 1) * L - (lp - 1) * lp / 2 + (l - lp - 1)]
                                  : stage_term(M, L, V, prefix, psum, minpair, lp, l, r, i);
             const double Mp = (double)M * (b.efwd[I.layer_off + lp - 1] + b.ebwd[I.layer_off + lp - 1]);
             const int cls = tables ? rcls[lp] : -1;
             const double* Tj = cls >= 0 ? ws + lay.chan + cls * tcls + chan_step(V, j) : nullptr;
-            for (int base = 1; base <= j && rp < 0; base += 32) {
-                const int c = base + lane;
-                bool match = false;
-                if (c <= j) {
-                    const double sub = W_at(W, L, j, lp, c, x - 1, allow);
-                    const double chan = Tj ? Tj[(c - 1) * (V - j) + (r - 1)]
-                                           : Mp / ((double)(c * r) * cross[cross_idx(V, i, r, c)]);
-                    match = dmax(dmax(sub, chan), st) == w;
+            for (int base = 1; base <= j && rp < 0; base += 32 * WALK_U) {
+                bool match[WALK_U];
+                double sub[WALK_U];
+#pragma unroll
+                for (int u = 0; u < WALK_U; ++u) {
+                    const int c = base + 32 * u + lane;
+                    match[u] = false;
+                    sub[u] = PP_INF;
+                    if (c <= j) {
+                        sub[u] = W_at(W, L, j, lp, c, x - 1, allow);
+                        const double chan = Tj ? Tj[(c - 1) * (V - j) + (r - 1)]
+                                               : Mp / ((double)(c * r) * cross[cross_idx(V, i, r, c)]);
+                        match[u] = dmax(dmax(sub[u], chan), st) == w;
+                    }
                 }
-                const int f = warp_first(match);
-                if (f >= 0) rp = base + f;
+#pragma unroll
+                for (int u = 0; u < WALK_U; ++u) {
+                    const int f = warp_first(match[u]);
+                    const double sw = __shfl_sync(0xffffffffu, sub[u], f < 0 ? 0 : f);
+                    if (rp < 0 && f >= 0) { rp = base + 32 * u + f; w_next = sw; }
+                }
             }
         }
         if (rp < 0) {   // cannot happen for a consistent table; leave a detectable hole
@@ -1539,7 +1572,7 @@ __device__ void dp_walk(const pp_batch& b, const pp_instance& I, int l, int x, i
             return;
         }
         if (lane == 0) { o_ls[x - 1] = lp + 1; o_le[x - 1] = l; o_dlo[x - 1] = i - r + 1; o_dhi[x - 1] = i; }
-        w = W_at(W, L, j, lp, rp, x - 1, allow);
+        w = w_next;   // == W_at(W, L, j, lp, rp, x - 1, allow)
         l = lp; i = j; r = rp; --x;
     }
     if (lane == 0) { o_ls[0] = 1; o_le[0] = l; o_dlo[0] = 1; o_dhi[0] = i; }
