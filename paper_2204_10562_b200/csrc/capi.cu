@@ -114,7 +114,8 @@ static const int g_pdl = getenv("PP_PDL") ? atoi(getenv("PP_PDL")) : 1;
 // combine kernel of the per-step schedule: 1 = crossing search (combine_bis.cu),
 // 0 = exhaustive register tiles (k_combine_s_p), 2 = auto; same bits either way
 static const int g_bis_rb = getenv("PP_BIS_RB") ? atoi(getenv("PP_BIS_RB")) : 0;   // rows per thread (0 = auto)
-static const double g_bis_waves = getenv("PP_BIS_WAVES") ? atof(getenv("PP_BIS_WAVES")) : 2.0;
+// (n = 1 C3 DP: 0.98 ms at 2 waves, 0.94 at 1-1.5)
+static const double g_bis_waves = getenv("PP_BIS_WAVES") ? atof(getenv("PP_BIS_WAVES")) : 1.5;
 static std::atomic<int> g_combine_kind{getenv("PP_COMBINE_BIS") ? atoi(getenv("PP_COMBINE_BIS")) : 2};
 // auto (kind 2): the crossing search for batches of at most this many instances
 // (latency-bound chains), the register tiles above it (throughput)
@@ -327,6 +328,8 @@ static int prm_inst(const pp_batch* b, void* stream) {
         cudaFuncSetAttribute(k_dp_inst2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
         k_dp_inst2<<<b->n_inst, DI2_T, smem2, S(stream)>>>(*b);
         PP_CHECK_LAUNCH("k_dp_inst2");
+        // (the backtrack as the tail of k_dp_inst2, one warp per xi while its tables are
+        // hot in L2, measured slower: C4 DP 4.91 -> 5.09 ms — it holds the CTA's 88 KB)
         dim3 gb(b->n_inst, maxV);
         k_backtrack<<<gb, 32, 0, S(stream)>>>(*b);
         PP_CHECK_LAUNCH("k_backtrack");

@@ -1579,14 +1579,13 @@ __device__ void dp_walk(const pp_batch& b, const pp_instance& I, int l, int x, i
 }
 
 // best_partition(xi) for every xi (partition.py:144-162).  grid (n_inst, maxV), block 32.
-__device__ __forceinline__ void backtrack_body(const pp_batch& b) {
-    const pp_instance I = b.inst[blockIdx.x];
-    const int xi = blockIdx.y + 1;
+// one warp: best W(L, xi, r, V) over r and its plan's stages (partition.py:144-162)
+__device__ __forceinline__ void backtrack_xi(const pp_batch& b, const pp_instance& I, int xi) {
     const int L = I.L, V = I.V;
     if (xi > V) return;
     const WsLayout lay = ws_layout(L, V);
     const double* W = b.ws + I.ws_off + lay.W;
-    const int lane = threadIdx.x;
+    const int lane = threadIdx.x & 31;
     double best = PP_INF;
     int br = 0;
     for (int r = 1 + lane; r <= V; r += 32) {
@@ -1604,6 +1603,10 @@ __device__ __forceinline__ void backtrack_body(const pp_batch& b) {
     if (br == 0) return;
     const int64_t st = I.stage_off + (int64_t)xi * (xi - 1) / 2;
     dp_walk(b, I, L, xi, br, V, best, b.stage_ls + st, b.stage_le + st, b.stage_dlo + st, b.stage_dhi + st);
+}
+__device__ __forceinline__ void backtrack_body(const pp_batch& b) {
+    const pp_instance I = b.inst[blockIdx.x];
+    backtrack_xi(b, I, blockIdx.y + 1);
 }
 __global__ void __launch_bounds__(32) k_backtrack(pp_batch b) { backtrack_body(b); }
 __global__ void __launch_bounds__(32) k_backtrack_p(const pp_batch* __restrict__ bp) {
