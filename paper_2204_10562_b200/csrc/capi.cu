@@ -550,10 +550,13 @@ static int prm_steps_graph(const pp_batch* b, void* stream) {
 static int prm_prep(const pp_batch* b, void* stream, bool tables) {
     const int maxL = b->max_L, maxV = b->max_V;
     dim3 gp(b->n_inst, maxL > maxV ? maxL : maxV);
-    k_prep<<<gp, 128, maxV <= PREP_CM_MAX ? sizeof(double) * maxV * maxV : 0, S(stream)>>>(*b);
+    // small instances (C4: L 32, V 16) leave most of a 128-thread row CTA idle and
+    // the rows are latency-bound: 32-thread CTAs fit twice as many rows per SM
+    const int pt = (maxL <= 32 && maxV <= 32) ? 32 : 128;
+    k_prep<<<gp, pt, maxV <= PREP_CM_MAX ? sizeof(double) * maxV * maxV : 0, S(stream)>>>(*b);
     PP_CHECK_LAUNCH("k_prep");
     dim3 gbase(b->n_inst, maxL > maxV ? maxL : maxV);
-    k_base<<<gbase, 128, 0, S(stream)>>>(*b, !(maxL <= SR_MAX && maxV <= SR_MAX));
+    k_base<<<gbase, pt, 0, S(stream)>>>(*b, !(maxL <= SR_MAX && maxV <= SR_MAX));
     PP_CHECK_LAUNCH("k_base");
     if (tables && maxL <= SR_MAX && maxV <= SR_MAX) {
         k_sdedup<<<dim3(b->n_inst, (maxV - 1 + 7) / 8 > 0 ? (maxV - 1 + 7) / 8 : 1), 256, 0, S(stream)>>>(*b);

@@ -1501,10 +1501,13 @@ __device__ void dp_walk(const pp_batch& b, const pp_instance& I, int l, int x, i
     const double* W = ws + lay.W;
     const bool allow = I.flags & PP_ALLOW_REPLICATION;
     const int lane = threadIdx.x & 31;
-    // shared-memory-path batches hold every stage term in the k_stab triangles and
-    // the chan quotients of multi-row payload classes in k_base's tables: the same
-    // expressions, so lookups give the bits the divisions would
-    const bool tables = b.max_L <= SR_MAX && b.max_V <= SR_MAX;
+    // Shared-memory-path batches hold every stage term in the k_stab triangles and
+    // the chan quotients of multi-row payload classes in k_base's tables (the same
+    // expressions, so lookups give the bits the divisions would).  The walk does
+    // not use them: a table lookup is two dependent global loads (slot / class id,
+    // then the entry) where the scalar expression's operands are one independent
+    // round, and the walk is a chain of such rounds (C3 n = 1: ~63 stages).
+    const bool tables = false;
     const int* sidx = reinterpret_cast<const int*>(ws + lay.sidx);
     const int* rcls = reinterpret_cast<const int*>(ws + lay.chcls + CHAN_CLS);
     const int64_t tri = (int64_t)(L - 1) * L / 2, tcls = (int64_t)tet(V);
