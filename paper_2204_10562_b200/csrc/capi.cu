@@ -42,7 +42,7 @@ __global__ void k_rdo_hash(pp_batch b, int dedup);
 __global__ void k_rdo_rep(pp_batch b);
 __global__ void k_rdo_insert(pp_batch b);
 __global__ void k_rdo_copy(pp_batch b);
-template <bool SMEM> __global__ void k_rdo_cut(pp_batch b);
+template <bool SMEM> __global__ void k_rdo_cut(pp_batch b, int per_warp);
 template <bool SMEM>
 __global__ void k_min_cut(pp_batch b, int k, const int* verts, int n, unsigned char* in_a, double* weight);
 __global__ void k_pe_sweep(pp_batch b);
@@ -236,14 +236,19 @@ int pp_rdo(const pp_batch* b, void* stream) {
         void (*plan)(pp_batch, int, int) = V <= 32 ? k_rdo_plan<1> : V <= 64 ? k_rdo_plan<2> :
                                            V <= 128 ? k_rdo_plan<4> : V <= 256 ? k_rdo_plan<8> : k_rdo_plan<16>;
         cudaFuncSetAttribute(plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan_smem);
-        cudaFuncSetAttribute(k_rdo_cut<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cut_smem_s);
-        const dim3 gc(b->n_inst, V - 1);
+        // cuts per CTA (one per warp; per-warp shared slices 16-byte aligned).  Four
+        // per CTA for V <= 32 measured slower on C4 (RDO 0.50 -> 0.62 ms,
+        // profiles/r02b_rdo_cut_wpc_ab.txt): one warp per CTA
+        const int wpc = 1;
+        const size_t pw_s = (cut_smem_s + 15) & ~size_t(15), pw = (cut_smem + 15) & ~size_t(15);
+        cudaFuncSetAttribute(k_rdo_cut<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(pw_s * wpc));
+        const dim3 gc(b->n_inst, (V - 1 + wpc - 1) / wpc);
         for (int r = 0; r <= rounds; ++r) {
             plan<<<b->n_inst, 32 * RDO_WARPS, plan_smem, S(stream)>>>(*b, r, r < rounds);
             PP_CHECK_LAUNCH("k_rdo_plan");
             if (r == rounds) break;
-            k_rdo_cut<true><<<gc, 32, cut_smem_s, S(stream)>>>(*b);
-            if (!in_smem) k_rdo_cut<false><<<gc, 32, cut_smem, S(stream)>>>(*b);
+            k_rdo_cut<true><<<gc, 32 * wpc, pw_s * wpc, S(stream)>>>(*b, (int)pw_s);
+            if (!in_smem) k_rdo_cut<false><<<gc, 32 * wpc, pw * wpc, S(stream)>>>(*b, (int)pw);
             PP_CHECK_LAUNCH("k_rdo_cut");
         }
     }

@@ -723,27 +723,32 @@ __global__ void __launch_bounds__(32 * RDO_WARPS) k_rdo_plan(pp_batch b, int rou
 // One warp per predicted tree node: exact global_min_cut of S_{c,k}, and
 // whether it splits S the predicted way (a singleton {t}, or block child A
 // against the rest).
+// blockDim = 32 x wpc: warp w of CTA (instance, y) cuts item y * wpc + w, in
+// its own slice of `per_warp` bytes of dynamic shared memory (small instances:
+// the 32-CTA-per-SM limit, not registers or shared memory, capped the number
+// of concurrent cuts at one warp per CTA)
 template <bool SMEM>
-__global__ void __launch_bounds__(32) k_rdo_cut(pp_batch b) {
+__global__ void __launch_bounds__(128) k_rdo_cut(pp_batch b, int per_warp) {
     const pp_instance I = b.inst[blockIdx.x];
     if (rdo_skip(b, I, blockIdx.x)) return;
     const int V = I.V;
     // the global-memory variant's per-item scratch (rdo_iw) exists only for
     // V > RDO_SMEM_MAX: a mixed batch runs both variants, each on its instances
     if ((V <= RDO_SMEM_MAX) != SMEM) return;
-    const int item = blockIdx.y;
+    const int wpc = blockDim.x >> 5, warp = threadIdx.x >> 5;
+    const int item = blockIdx.y * wpc + warp;
     if (item >= V - 1) return;
     const RdoState st = rdo_spec_state(b, I);
     const int c = st.it_c[item];
     if (c < 0) return;
     extern __shared__ double smem_d[];
-    char* sm = (char*)smem_d;
+    char* sm = (char*)smem_d + (size_t)warp * per_warp;
     double* W;
-    if constexpr (SMEM) { W = smem_d; sm += sizeof(double) * V * V; }
+    if constexpr (SMEM) { W = reinterpret_cast<double*>(sm); sm += sizeof(double) * V * V; }
     else W = b.ws + I.ws_off + ws_layout(I.L, V).rdo_iw + (int64_t)item * V * V;
     int* mem = (int*)sm;
     unsigned char* side = (unsigned char*)(mem + V);
-    const int lane = threadIdx.x;
+    const int lane = threadIdx.x & 31;
     const int k = st.it_k[item], tv = st.it_t[item];
     const int n = warp_list(V, mem, [&](int v) { return in_item(st, c, k, v); });
     warp_min_cut(W, b.bw + I.bw_off, V, mem, n, side);
@@ -874,8 +879,8 @@ template __global__ void k_rdo_plan<8>(pp_batch, int, int);
 template __global__ void k_rdo_plan<16>(pp_batch, int, int);
 template __global__ void k_rdo<true>(pp_batch, int);
 template __global__ void k_rdo<false>(pp_batch, int);
-template __global__ void k_rdo_cut<true>(pp_batch);
-template __global__ void k_rdo_cut<false>(pp_batch);
+template __global__ void k_rdo_cut<true>(pp_batch, int);
+template __global__ void k_rdo_cut<false>(pp_batch, int);
 template __global__ void k_min_cut<true>(pp_batch, int, const int*, int, unsigned char*, double*);
 template __global__ void k_min_cut<false>(pp_batch, int, const int*, int, unsigned char*, double*);
 
