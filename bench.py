@@ -298,7 +298,7 @@ def run_ours(args):
     dp_ops = 2 * sum(t_fact(s.L, s.V) for s in specs)   # one max + one min per factored candidate
     dp_achieved = dp_ops / (phase["dp"] / 1e3)
     traffic, traffic_src = None, None
-    for name in ("r02_dp_traffic_warm.json", "ncu_dp_traffic.json"):   # newest measurement first
+    for name in ("r02b_dp_traffic_warm.json", "r02_dp_traffic_warm.json", "ncu_dp_traffic.json"):   # newest first
         tpath = os.path.join(REPO, "profiles", name)
         if os.path.exists(tpath):
             try:
