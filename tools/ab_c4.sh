@@ -3,7 +3,7 @@
 for lib in main "$@"; do
   if [ "$lib" = main ]; then unset PP_LIB_OVERRIDE; else export PP_LIB_OVERRIDE=$PWD/$lib; fi
   echo "== $lib"
-  python tools/phases.py c4 2>&1 | tail -2
-  python tools/phases.py c3 12 2>&1 | tail -1
-  python tools/phases.py c3 1 2>&1 | tail -1
+  timeout 180 python tools/phases.py c4 2>&1 | tail -2
+  timeout 180 python tools/phases.py c3 12 2>&1 | tail -1
+  timeout 180 python tools/phases.py c3 1 2>&1 | tail -1
 done
