@@ -75,6 +75,19 @@ double or_pysum(const double *x, int64_t n, int32_t mode)
     return f;
 }
 
+/* allocation failure is reported, not dereferenced (the dense DP table is
+   ~0.33 GB per 96 x 64 instance; a thread pool of them can exhaust host RAM) */
+static void *or_xalloc(void *p, size_t bytes)
+{
+    if (!p && bytes) {
+        fprintf(stderr, "pipeplan_oracle: out of host memory (%zu bytes)\n", bytes);
+        abort();
+    }
+    return p;
+}
+#define malloc(n) or_xalloc(malloc(n), (size_t)(n))
+#define calloc(n, s) or_xalloc(calloc((n), (s)), (size_t)(n) * (size_t)(s))
+
 static inline double pymax2(double a, double b) { return (b > a) ? b : a; }
 static inline double pymin2(double a, double b) { return (b < a) ? b : a; }
 static inline double BW(const or_inst *I, int a, int b) { return I->bw[(int64_t)a * I->V + b]; }

@@ -46,6 +46,10 @@ __device__ __forceinline__ double warp_min_cut_t(double* wl, const double* bw, i
         const int k = lane + 32 * s;
         alive[s] = k < n; grp[s] = k; side[s] = false; inadj[s] = false; adj[s] = 0.0;
     }
+    const char* colk[SLOTS];   // this lane's columns: wt(v, k) at colk[s] + v * n8 bytes
+    const int n8 = 8 * n;
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) colk[s] = reinterpret_cast<const char*>(wl + lane + 32 * s);
     double best_weight = PP_INF;
     for (int n_alive = n; n_alive > 1; --n_alive) {
 #pragma unroll
@@ -67,17 +71,22 @@ __device__ __forceinline__ double warp_min_cut_t(double* wl, const double* bw, i
             // (ties are the common case on structured clusters: three REDUX beat ballot fast paths)
             const unsigned hi = (unsigned)(bu >> 32), lo = (unsigned)bu;
             const unsigned mhi = __reduce_max_sync(FULL, hi);
+            // the lane's candidate while its high word ties the max (bk is the
+            // 0x7fffffff sentinel when the lane has none): one select after each REDUX
+            const unsigned cand = hi == mhi ? (unsigned)bk : 0x7fffffffu;
             const unsigned mlo = __reduce_max_sync(FULL, hi == mhi ? lo : 0u);
-            const bool win = bk != 0x7fffffff && hi == mhi && lo == mlo;
-            const int nk = (int)__reduce_min_sync(FULL, win ? (unsigned)bk : 0x7fffffffu);
+            const int nk = (int)__reduce_min_sync(FULL, lo == mlo ? cand : 0x7fffffffu);
             cut = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
             sv = tv; tv = nk;
-            const double* row = wl + nk * n;
+            const int rowoff = nk * n8;   // bytes: one IMAD from nk to the load address
 #pragma unroll
             for (int s = 0; s < SLOTS; ++s) {   // adj[u] += wt(next_v, u)  (ordering.py:69-70)
                 const int k = lane + 32 * s;
+                // the row entry is loaded whatever the lane's state (its predicate is
+                // known before nk), so the load does not wait for the flag update
+                const double x = k < n ? *reinterpret_cast<const double*>(colk[s] + rowoff) : 0.0;
                 if (k == nk) inadj[s] = false;
-                if (inadj[s]) adj[s] = adj[s] + row[k];
+                if (inadj[s]) adj[s] = adj[s] + x;
             }
         }
         if (cut < best_weight) {   // first minimum cut-of-phase (ordering.py:73-75)

@@ -76,6 +76,14 @@ def oracle_spp_parallel(specs, threads=None):
     import oracle as O
     insts = [oracle_instance(s) for s in specs]
     n = threads or max(1, min(len(insts), len(os.sched_getaffinity(0)), 32))
+    # the oracle's dense DP table is ~V^3 L * 13 bytes per instance (0.33 GB at
+    # 96 x 64): keep the concurrent ones within half the host's free memory
+    per = max(13 * max(t[0].V for t in insts) ** 3 * max(t[0].L for t in insts), 1)
+    try:
+        free = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+        n = max(1, min(n, int(0.5 * free // per)))
+    except (ValueError, OSError):
+        pass
     with ThreadPoolExecutor(n) as ex:
         outs = list(ex.map(lambda t: O.spp(t[0]), insts))
     return [(w, ids) for w, (_, ids) in zip(outs, insts)]

@@ -1,0 +1,8 @@
+timeout 900 python -m pytest tests/test_gpu_rdo.py tests/test_gpu_parity.py tests/test_gpu_c3_headline.py tests/test_gpu_dp_modes.py tests/test_gpu_scale.py -q -x > gpurun_out/r17_pytest.txt 2>&1; tail -3 gpurun_out/r17_pytest.txt
+for lib in main build/v12.so build/head.so main; do
+  if [ "$lib" = main ]; then unset PP_LIB_OVERRIDE; else export PP_LIB_OVERRIDE=$PWD/$lib; fi
+  echo "== $lib"
+  timeout 180 python tools/phases.py c3 1 2>&1 | tail -2
+  timeout 180 python tools/phases.py c3 12 2>&1 | tail -1
+  timeout 180 python tools/phases.py c4 2>&1 | tail -1
+done
