@@ -82,9 +82,9 @@ __device__ __forceinline__ double warp_min_cut_t(double* wl, const double* bw, i
 #pragma unroll
             for (int s = 0; s < SLOTS; ++s) {   // adj[u] += wt(next_v, u)  (ordering.py:69-70)
                 const int k = lane + 32 * s;
-                // the row entry is loaded whatever the lane's state (its predicate is
-                // known before nk), so the load does not wait for the flag update
-                const double x = k < n ? *reinterpret_cast<const double*>(colk[s] + rowoff) : 0.0;
+                // the row entry of every live vertex is loaded (that predicate is known
+                // before nk), so the load does not wait for the in-set flag update
+                const double x = alive[s] ? *reinterpret_cast<const double*>(colk[s] + rowoff) : 0.0;
                 if (k == nk) inadj[s] = false;
                 if (inadj[s]) adj[s] = adj[s] + x;
             }
